@@ -1,0 +1,191 @@
+/*
+ * svdsc.h -- C ABI of the B200-native svds-C hot path (libsvdsc.so).
+ *
+ * The library computes the k largest singular triplets of a sparse (CSR) or
+ * dense fp64 matrix A (Eq. (1): A ~ U_k Sigma_k V_k^T) with the
+ * augmented-restart Lanczos bidiagonalization of svds-C (Alg. 1 + full
+ * re-orthogonalization; Alg. 2).  Every
+ * step of the method runs in the library's own sm_100a kernels on the
+ * caller's CUDA stream; there is no CPU fallback.
+ *
+ * Conventions (all entry points):
+ *   - Pointers documented as "device" must be CUDA device pointers (e.g. torch
+ *     CUDA tensors); "host" pointers are ordinary host memory.
+ *   - Dense matrices and bases are column-major (the paper's `mat`,
+ *     PAPER.md:298-302) with an explicit leading dimension >= nrows.
+ *   - CSR matrices are 0-based: row_ptr[nrows+1] int64 (monotone, row_ptr[0]=0),
+ *     col_idx[nnz] int32 in [0, ncols), values[nnz] fp64, finite.  Columns
+ *     need not be sorted; duplicate (row, col) entries act as their sum
+ *     (SPEC.md:112).  The paper's 1-based pointerB/pointerE layout
+ *      is converted to this form by the caller
+ *     (reading Q13).
+ *   - Ownership: every input array stays owned by the caller and must stay
+ *     valid and unmodified while a handle/matrix that references it lives.
+ *     Outputs are caller-allocated (a departure from "mallocated
+ *     automatically", so that the caller's allocator owns all
+ *     device memory).  Objects created by the library are freed by the
+ *     matching *_destroy call.
+ *   - Errors: every function returns an svdsc_status.  Contract violations
+ *     return SVDSC_EINVAL before any device work; a message is available from
+ *     svdsc_last_error(handle).  CUDA/NCCL failures return SVDSC_ECUDA /
+ *     SVDSC_ENCCL.  Functions are synchronous with respect to the host unless
+ *     documented as "enqueued".
+ *   - Threading: one call at a time per handle; distinct handles are
+ *     independent.
+ */
+#ifndef SVDSC_H
+#define SVDSC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SVDSC_API __attribute__((visibility("default")))
+#else
+#define SVDSC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SVDSC_OK = 0,
+    SVDSC_NOT_CONVERGED = 1,  /* results valid, some residual >= tol */
+    SVDSC_EINVAL = -1,        /* contract violation; nothing was computed        */
+    SVDSC_ENOMEM = -2,        /* device allocation failed                        */
+    SVDSC_ECUDA = -3,         /* CUDA runtime error                               */
+    SVDSC_ENCCL = -4,         /* NCCL error or NCCL library unavailable           */
+    SVDSC_ESVD_NOCONV = -5,   /* small Jacobi SVD: no convergence in 50 sweeps    */
+    SVDSC_ERANKDEF = -6       /* sigma_j = 0 with non-negligible residual */
+} svdsc_status;
+
+typedef struct svdsc_handle svdsc_handle;
+typedef struct svdsc_matrix svdsc_matrix;
+
+/* Options of Alg. 2 (defaults). */
+typedef struct {
+    int32_t k;            /* rank parameter, >= 1                                      */
+    double tol;           /* relative residual tolerance of Eq. (4), > 0 (default 1e-10)*/
+    int32_t t;            /* subspace dimension; <= 0 -> max(15, 3k) (Alg. 2 step 1),  */
+                          /* clamped to min(m,n)-1; EINVAL if then t < k+2 (reading Q14)*/
+    int32_t maxit;        /* r: maximum number of passes (reading Q5); <= 0 -> 10       */
+    uint64_t seed;        /* seed of the internal start vector / breakdown streams      */
+    const double *v0;     /* device, length ncols (global), or NULL -> internal N(0,1)  */
+    int32_t fixed_passes; /* > 0: run exactly this many passes (parity hook, Q18)        */
+    int32_t reorth;       /* 2 = CGS2 (default when 0 is not requested: pass 2);         */
+                          /* 0 = off, test-only                            */
+} svdsc_opts;
+
+typedef struct {
+    int32_t passes, restarts, converged, t_used;
+    int64_t steps;        /* Lanczos steps (one A^T u and one A v product each)          */
+    int64_t matvecs;      /* products with A or A^T actually performed                   */
+    int64_t breakdowns;   /* breakdown replacements (reading Q7)                          */
+    double max_resid;     /* max_j of Eq. (4) residuals at the final check               */
+    double seconds_total; /* host wall time of svdsc_solve                                */
+    int64_t launches;     /* kernels launched by the library during the solve            */
+    int64_t bytes_model;  /* algorithmic HBM bytes of the Lanczos steps */
+} svdsc_info;
+
+/* ---- handles --------------------------------------------------------------- */
+/* Create a handle bound to the current CUDA device and `stream` (a cudaStream_t;
+ * NULL = legacy default stream).  Owns internal scratch (device). */
+SVDSC_API svdsc_status svdsc_create(svdsc_handle **h, void *stream);
+SVDSC_API svdsc_status svdsc_set_stream(svdsc_handle *h, void *stream);
+SVDSC_API void svdsc_destroy(svdsc_handle *h);
+/* Last error message of this handle (static storage owned by the handle). */
+SVDSC_API const char *svdsc_last_error(const svdsc_handle *h);
+/* Library version string, e.g. "svdsc 0.1 sm_100a". */
+SVDSC_API const char *svdsc_version(void);
+
+/* ---- matrices ---------------------------------------------------------------
+ * Analysis (once per matrix, "mallocate ... at the beginning"):
+ * validation, row-length binning, and a device-built CSC copy used for A^T u.
+ * For a row-partitioned multi-GPU run each rank passes its local rows
+ * [row_offset, row_offset + nrows) of the m_global x ncols matrix with global
+ * column indices.  Single GPU: row_offset = 0,
+ * m_global = nrows.  Device arrays: row_ptr, col_idx, values / data. */
+SVDSC_API svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int64_t nnz,
+                              const int64_t *row_ptr, const int32_t *col_idx,
+                              const double *values, int64_t row_offset, int64_t m_global,
+                              svdsc_matrix **M);
+SVDSC_API svdsc_status svdsc_matrix_dense(svdsc_handle *h, int64_t nrows, int64_t ncols, int64_t ld,
+                                const double *data, int64_t row_offset, int64_t m_global,
+                                svdsc_matrix **M);
+SVDSC_API void svdsc_matrix_destroy(svdsc_matrix *M);
+
+/* ---- the solve (Alg. 2) -----------------------------------------------------
+ * Device workspace bytes needed by svdsc_solve for these options. */
+SVDSC_API svdsc_status svdsc_workspace_size(svdsc_matrix *M, const svdsc_opts *o, size_t *bytes);
+/* Compute S[k] (descending), U (m_local x k, ld ldu >= m_local), V (ncols x k,
+ * ld ldv >= ncols; replicated on every rank), resid[k] (Eq. (4) residuals).
+ * S, U, V, resid are device pointers (resid may be NULL).  workspace: device,
+ * >= svdsc_workspace_size bytes, or NULL (the library allocates and frees it).
+ * info: host, may be NULL.  Returns after the results are complete on the
+ * handle's stream.  SVDSC_NOT_CONVERGED still fills every output. */
+SVDSC_API svdsc_status svdsc_solve(svdsc_matrix *M, const svdsc_opts *o, void *workspace,
+                         size_t ws_bytes, double *S, double *U, int64_t ldu, double *V,
+                         int64_t ldv, double *resid, svdsc_info *info);
+
+/* End-to-end convenience with HOST buffers: copies A (and v0 if given) from
+ * host memory, analyses, solves, copies S, U (m x k, ld m), V (n x k, ld n) and
+ * resid back to host.  All pointers here are host pointers (pinned memory is
+ * fastest); opts->v0, if non-NULL, is a HOST pointer of length n. */
+SVDSC_API svdsc_status svdsc_solve_host_csr(svdsc_handle *h, int64_t m, int64_t n, int64_t nnz,
+                                  const int64_t *row_ptr, const int32_t *col_idx,
+                                  const double *values, const svdsc_opts *o, double *S,
+                                  double *U, double *V, double *resid, svdsc_info *info);
+SVDSC_API svdsc_status svdsc_solve_host_dense(svdsc_handle *h, int64_t m, int64_t n,
+                                    const double *data /* col-major, ld m */,
+                                    const svdsc_opts *o, double *S, double *U, double *V,
+                                    double *resid, svdsc_info *info);
+
+/* ---- step-level entry points (the hot-path rows of SURVEY.md 8(a)) -------- */
+/* a1 / a5: y = op(A) x - c * yprev, op = A (trans=0, Alg. 1 line 7) or A^T
+ * (trans=1, Alg. 1 line 5).  x, y, yprev device; c_dev is a device pointer to
+ * the scalar c (may be NULL: c = 0, yprev ignored).  Enqueued on the stream. */
+SVDSC_API svdsc_status svdsc_op_matvec(svdsc_matrix *M, int trans, const double *x, double *y,
+                             const double *c_dev, const double *yprev);
+/* a2-a4 / a6: two-pass classical Gram-Schmidt of w (length N) against the first
+ * ncols columns of the column-major basis Q (ld >= N), then
+ * *norm_dev = ||w|| (device scalar).  w is overwritten.  Enqueued. */
+SVDSC_API svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const double *Q,
+                           int64_t ldq, double *w, double *norm_dev);
+/* a7: SVD of the p x p column-major device matrix Tm (Alg. 2 step 4) by the
+ * device one-sided Jacobi: U, V (p x p, ld p) and S (p, descending), sign rule
+ * of SPEC.md:158.  Returns SVDSC_ESVD_NOCONV after 50 sweeps.  Synchronous. */
+SVDSC_API svdsc_status svdsc_op_small_svd(svdsc_handle *h, int32_t p, const double *Tm, double *U,
+                                double *S, double *V, int32_t *sweeps);
+/* a8 / a9: Qout(:, 0:k) = Q(:, 0:t) W(:, 0:k) for N rows; Qout may equal Q (in
+ * place, the restart's Ritz recombination, Alg. 2 step 8).  W is t x >=k
+ * column-major device (ld ldw).  Enqueued. */
+SVDSC_API svdsc_status svdsc_op_recombine(svdsc_handle *h, int64_t N, int32_t t, int32_t k,
+                                const double *Q, int64_t ldq, const double *W, int32_t ldw,
+                                double *Qout, int64_t ldo);
+/* One first pass LBP(A, t+1) from v0 (device, length ncols): bases U
+ * (m x (t+1), ld ldu), V (n x (t+1), ld ldv) and T ((t+1) x (t+1), col-major,
+ * device).  The GPU path does not form u_{t+1} (reading Q2): column t of U
+ * and T(t,t) are left zero.  Synchronous. */
+SVDSC_API svdsc_status svdsc_op_lbp(svdsc_matrix *M, const svdsc_opts *o, int32_t t, const double *v0,
+                          double *U, int64_t ldu, double *V, int64_t ldv, double *T,
+                          svdsc_info *info);
+
+/* ---- multi-GPU (row-partitioned A) -------------------------- */
+/* Rank 0 creates an NCCL unique id (128 bytes, host) that the caller
+ * broadcasts (e.g. torch.distributed.broadcast); every rank then calls
+ * svdsc_comm_init collectively.  NCCL is loaded at run time (libnccl.so.2);
+ * SVDSC_ENCCL if unavailable. */
+SVDSC_API svdsc_status svdsc_comm_unique_id(unsigned char id[128]);
+SVDSC_API svdsc_status svdsc_comm_init(svdsc_handle *h, int nranks, int rank, const unsigned char id[128]);
+/* Host-only partitioner (no GPU needed): contiguous row blocks of a CSR
+ * matrix (host row_ptr, m+1 entries) balanced by the per-step byte cost
+ * w_r = 24 nnz_r + 24 basis_cols.  bounds: host,
+ * nparts+1 entries, bounds[0] = 0, bounds[nparts] = m. */
+SVDSC_API svdsc_status svdsc_partition_rows(int64_t m, const int64_t *row_ptr, int64_t basis_cols,
+                                  int nparts, int64_t *bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVDSC_H */

@@ -175,8 +175,11 @@ int or_jacobi_svd(int64_t p, int64_t q, const double *M, double *U, double *S,
     memcpy(W, M, sizeof(double) * (size_t)(p * q));
     for (int64_t j = 0; j < q; j++)
         for (int64_t i = 0; i < q; i++) Vw[i + j * q] = (i == j) ? 1.0 : 0.0;
-    /* rotation threshold: |gamma| > sqrt(p) * eps * sqrt(alpha*beta) */
-    const double ctol = sqrt((double)p) * 2.220446049250313e-16;
+    /* rotation threshold: |gamma| > 2 p eps sqrt(alpha*beta).  2 p eps bounds the
+     * rounding error of a length-p dot product (gamma_p), so a pair that is
+     * orthogonal to working precision is never rotated again and the sweep
+     * loop terminates (reading Q10a). */
+    const double ctol = 2.0 * (double)p * 2.220446049250313e-16;
     int sweeps = 0, converged = 0;
     for (sweeps = 1; sweeps <= max_sweeps; sweeps++) {
         int rotated = 0;

@@ -1,0 +1,129 @@
+// internal.h -- private declarations of libsvdsc (B200 / sm_100a).
+//
+// Layout in HBM:
+//   U basis  m_local x (t+1) column-major, ld = roundup(m_local, 32)
+//   V basis  n_local x (t+1) column-major, ld = roundup(n_local, 32)
+//   T        (t+1) x (t+1) column-major (device, Alg. 2 step 9 layout)
+//   every reduction is two-level and deterministic: per-CTA partials stored
+//   [column][block], reduced in fixed order by the last CTA to finish.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/svdsc.h"
+
+namespace svdsc {
+
+constexpr int kMaxBlocks = 1184;  // 8 x 148: max CTAs contributing partials
+constexpr int kWarp = 32;
+
+// Device-resident control block (one per solve workspace).
+struct Ctrl {
+    double amax[2];       // largest accepted alpha/beta so far (ring by check parity)
+    double inv;           // 1 / norm of the vector being normalized
+    int abort;            // != 0: breakdown pending; step kernels are no-ops
+    int abort_check;      // check index that broke down
+    int svd_status;       // 0 ok, SVDSC_ESVD_NOCONV
+    int svd_sweeps;
+    int converged;
+    int rankdef;
+    double max_resid;
+    unsigned int cnt[16]; // last-block counters (one per reduction site)
+};
+
+// ---- CSR operand (device) prepared by analysis --------------------------------
+struct CsrOp {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    const int64_t *row_ptr = nullptr;  // nrows+1
+    const int32_t *col = nullptr;      // nnz
+    const double *val = nullptr;       // nnz
+    // row bins: rows grouped by length class, one list per kernel variant
+    int32_t *bin_rows = nullptr;       // concatenated row lists
+    int64_t bin_off[8] = {0};          // offsets into bin_rows; bin b = [off[b], off[b+1])
+    // long rows (> kLongRow nnz) split into chunks
+    int32_t *long_rows = nullptr;      // row id per long row
+    int64_t *chunk_first = nullptr;    // first chunk index per long row (+1 sentinel)
+    int32_t *chunk_row = nullptr;      // long-row slot per chunk
+    int64_t n_long = 0, n_chunks = 0;
+    double *chunk_partial = nullptr;   // n_chunks
+    std::vector<void *> owned;         // allocations owned by this operand
+};
+
+struct DenseOp {
+    int64_t nrows = 0, ncols = 0, ld = 0;
+    const double *data = nullptr;
+    double *partial = nullptr;         // split-K partial sums
+    int splits_n = 1, splits_t = 1;
+};
+
+void csr_analyze(CsrOp &op, cudaStream_t s);       // bins + long-row chunks
+void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s);  // device CSC -> CSR of A^T
+void csr_free(CsrOp &op);
+
+// y = A x - c yprev (c = *c_dev if c_dev, else 0).  abort: skip if *abort.
+void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev,
+              const double *yprev, const int *abort, cudaStream_t s);
+void gemv_n(const DenseOp &A, const double *x, double *y, const double *c_dev,
+            const double *yprev, const int *abort, cudaStream_t s);
+void gemv_t(const DenseOp &A, const double *x, double *y, const double *c_dev,
+            const double *yprev, const int *abort, cudaStream_t s);
+
+// ---- CGS2 sweeps (column-major basis Q, N rows, ncols active columns) ----------
+struct RedBuf {
+    double *partial;      // (kMaxCols) x kMaxBlocks, [col][block]
+    int pstride;          // = kMaxBlocks
+    double *h1, *h2, *nrm;// reduced outputs (device)
+    unsigned int *cnt;    // counters (Ctrl::cnt)
+};
+int cgs_blocks(int64_t N, int num_sms);
+// h1 = Q^T w
+void cgs_p1(int64_t N, int ncols, const double *Q, int64_t ldq, const double *w,
+            const RedBuf &r, const int *abort, int nsm, cudaStream_t s);
+// w <- w - Q h1 (in place), h2 = Q^T w, nrm[0] = ||w||^2
+void cgs_p2(int64_t N, int ncols, const double *Q, int64_t ldq, double *w,
+            const RedBuf &r, const int *abort, int nsm, cudaStream_t s);
+// w <- w - Q h (h = r.h2, or `h` if given), nrm[0] = ||w||^2 (ncols may be 0)
+void cgs_p3(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *h,
+            const RedBuf &r, const int *abort, int nsm, cudaStream_t s);
+// Finalize the norm of a freshly orthogonalized vector (check index `check`):
+//   nrm = sqrt(r.nrm[0]); breakdown if nrm <= 1e-14 max(amax, 1) (reading Q7);
+//   T entry *t_entry = nrm (or 0 and ctrl->abort = 1 on breakdown);
+//   w /= nrm unless breakdown.  force: no breakdown test, T entry untouched.
+void normalize(int64_t N, double *w, const RedBuf &r, Ctrl *ctrl, double *t_entry, int check,
+               int force, int nsm, cudaStream_t s);
+// breakdown replacement vector (counter RNG, bit-exact with the oracle's definition)
+void breakdown_vector(int64_t N, int64_t row_offset, double *w, uint64_t seed, uint64_t stream,
+                      cudaStream_t s);
+// deterministic N(0,1) start vector (library default when v0 == NULL)
+void random_start(int64_t N, int64_t row_offset, double *w, uint64_t seed, cudaStream_t s);
+void axpy_dev(int64_t N, double *y, const double *c_dev, const double *x, const int *abort,
+              cudaStream_t s);  // y -= c x
+
+// ---- small SVD / restart ---------------------------------------------------------
+// Jacobi SVD of the p x p matrix stored (ld p) in W; outputs Uh, Sh, Vh (ld p),
+// writes ctrl->svd_status / svd_sweeps.  Vw is scratch (p x p).  kneed: number
+// of leading columns whose zero-sigma completion is required.
+void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double *Uh, double *Sh,
+               double *Vh, int kneed, Ctrl *ctrl, const int *abort, cudaStream_t s);
+// Eq. (4) residuals, convergence flag (Alg. 2 step 5)
+void residuals(int t, int k, const double *T, int ldt, const double *Uh, const double *Sh,
+               double tol, double *resid, Ctrl *ctrl, const int *abort, cudaStream_t s);
+// Alg. 2 step 9: rho = beta_t Uh(t,1:k); T = 0; T(j,j) = Sh_j; T(j,k) = rho_j
+void restart_T(int t, int k, double *T, int ldt, const double *Uh, const double *Sh,
+               double *rho, cudaStream_t s);
+void recombine(int64_t N, int t, int k, const double *Q, int64_t ldq, const double *W, int ldw,
+               double *Qout, int64_t ldo, int nsm, cudaStream_t s);
+void copy_col(int64_t N, const double *src, double *dst, cudaStream_t s);
+void fill_zero(double *p, int64_t n, cudaStream_t s);
+
+// ---- launch bookkeeping ----------------------------------------------------------
+extern thread_local int64_t g_launches;
+inline void count_launch() { ++g_launches; }
+
+}  // namespace svdsc
+
+#define SVDSC_CUDA_CHECK_LAUNCH() ::svdsc::count_launch()

@@ -1,0 +1,634 @@
+// matvec.cu -- the two products of every Lanczos step:
+//   a1: w = A^T u_i - alpha_i v_i   (Alg. 1 line 5)
+//   a5: z = A v_{i+1} - beta_i u_i  (Alg. 1 line 7)
+// The paper calls MKL_dcsrmv / an OpenMP SpMV and cblas_dgemv for
+// dense A.  Here:
+//   * CSR SpMV with rows binned by length: sub-warp "vector" groups of 2..32
+//     lanes, CTA-per-row, and multi-CTA chunks for rows > kLongRow nnz; every
+//     row sum is a fixed-shape tree, so results are run-to-run deterministic.
+//   * A^T u runs the same SpMV on a device-built CSC copy (= CSR of A^T) whose
+//     in-column order is by row, i.e. the oracle's accumulation order.
+//   * dense GEMV N/T: 128-bit coalesced loads of the column-major A, split over
+//     columns (N) or rows (T) into a grid of ~8 CTAs per SM, deterministic
+//     split-K reduction fused with the epilogue.
+// All kernels are HBM-bandwidth bound; the epilogue (- c * yprev) is fused.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "internal.h"
+
+namespace svdsc {
+
+thread_local int64_t g_launches = 0;
+
+namespace {
+
+constexpr int kLongRow = 65536;   // rows longer than this are split into chunks
+constexpr int kCtaThreads = 256;
+
+__device__ __forceinline__ bool aborted(const int *abort) {
+    return abort != nullptr && *(volatile const int *)abort != 0;
+}
+
+// bin of a row of length L: 0..4 = vector groups of 2,4,8,16,32 lanes,
+// 5 = CTA per row, 6 = long (chunked)
+__host__ __device__ __forceinline__ int row_bin(int64_t L) {
+    if (L <= 4) return 0;
+    if (L <= 8) return 1;
+    if (L <= 16) return 2;
+    if (L <= 64) return 3;
+    if (L <= 2048) return 4;
+    if (L <= kLongRow) return 5;
+    return 6;
+}
+
+__global__ void k_bin_count(int64_t nrows, const int64_t *__restrict__ rp, unsigned long long *cnt) {
+    __shared__ unsigned int sc[8];
+    if (threadIdx.x < 8) sc[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&sc[row_bin(rp[r + 1] - rp[r])], 1u);
+    __syncthreads();
+    if (threadIdx.x < 8 && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
+}
+
+__global__ void k_bin_fill(int64_t nrows, const int64_t *__restrict__ rp,
+                           unsigned long long *cursor, const int64_t *off, int32_t *rows) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int b = row_bin(rp[r + 1] - rp[r]);
+        unsigned long long pos = atomicAdd(&cursor[b], 1ull);
+        rows[off[b] + (int64_t)pos] = (int32_t)r;
+    }
+}
+
+// y[row] = sum - c*yprev[row]
+__device__ __forceinline__ void epilogue_store(double *y, int64_t r, double sum, double c,
+                                               const double *yprev) {
+    if (yprev) sum -= c * yprev[r];
+    y[r] = sum;
+}
+
+// G lanes per row; the whole warp iterates in lock-step so full-mask shuffles are legal.
+template <int G>
+__global__ void __launch_bounds__(256) k_spmv_vec(const int32_t *__restrict__ rows, int64_t count,
+                                                  const int64_t *__restrict__ rp,
+                                                  const int32_t *__restrict__ col,
+                                                  const double *__restrict__ val,
+                                                  const double *__restrict__ x, double *__restrict__ y,
+                                                  const double *c_dev, const double *__restrict__ yprev,
+                                                  const int *abort) {
+    if (aborted(abort)) return;
+    constexpr int GPW = kWarp / G;  // groups per warp
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % G;
+    const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double c = c_dev ? *c_dev : 0.0;
+    for (int64_t base = warp_g * GPW; base < count; base += nwarps * GPW) {
+        const int64_t g = base + lane / G;
+        double sum = 0.0;
+        int32_t r = -1;
+        if (g < count) {
+            r = rows[g];
+            const int64_t p0 = rp[r], p1 = rp[r + 1];
+            for (int64_t p = p0 + sub; p < p1; p += G) sum = fma(val[p], __ldg(x + col[p]), sum);
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, G);
+        if (sub == 0 && r >= 0) epilogue_store(y, r, sum, c, yprev);
+    }
+}
+
+__device__ __forceinline__ double block_sum_256(double v, double *sh /* >= 8 */) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) s += sh[i];
+    return s;  // valid on thread 0
+}
+
+// one CTA per row (rows of 2k..64k nnz)
+__global__ void __launch_bounds__(256) k_spmv_cta(const int32_t *__restrict__ rows, int64_t count,
+                                                  const int64_t *__restrict__ rp,
+                                                  const int32_t *__restrict__ col,
+                                                  const double *__restrict__ val,
+                                                  const double *__restrict__ x, double *__restrict__ y,
+                                                  const double *c_dev, const double *__restrict__ yprev,
+                                                  const int *abort) {
+    if (aborted(abort)) return;
+    __shared__ double sh[8];
+    const double c = c_dev ? *c_dev : 0.0;
+    for (int64_t g = blockIdx.x; g < count; g += gridDim.x) {
+        const int32_t r = rows[g];
+        const int64_t p0 = rp[r], p1 = rp[r + 1];
+        double sum = 0.0;
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) sum = fma(val[p], __ldg(x + col[p]), sum);
+        sum = block_sum_256(sum, sh);
+        if (threadIdx.x == 0) epilogue_store(y, r, sum, c, yprev);
+    }
+}
+
+// chunks of long rows: partial[ch] = sum over the chunk
+__global__ void __launch_bounds__(256) k_spmv_chunks(int64_t n_chunks, const int32_t *__restrict__ chunk_row,
+                                                     const int64_t *__restrict__ chunk_first,
+                                                     const int32_t *__restrict__ long_rows,
+                                                     const int64_t *__restrict__ rp,
+                                                     const int32_t *__restrict__ col,
+                                                     const double *__restrict__ val,
+                                                     const double *__restrict__ x, double *partial,
+                                                     const int *abort) {
+    if (aborted(abort)) return;
+    __shared__ double sh[8];
+    for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+        const int32_t slot = chunk_row[ch];
+        const int32_t r = long_rows[slot];
+        const int64_t k = ch - chunk_first[slot];
+        const int64_t p0 = rp[r] + k * kLongRow;
+        const int64_t p1 = min(rp[r + 1], p0 + (int64_t)kLongRow);
+        double sum = 0.0;
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) sum = fma(val[p], __ldg(x + col[p]), sum);
+        sum = block_sum_256(sum, sh);
+        if (threadIdx.x == 0) partial[ch] = sum;
+    }
+}
+
+__global__ void k_spmv_chunks_fix(int64_t n_long, const int32_t *__restrict__ long_rows,
+                                  const int64_t *__restrict__ chunk_first, const double *partial,
+                                  double *y, const double *c_dev, const double *yprev, const int *abort) {
+    if (aborted(abort)) return;
+    const double c = c_dev ? *c_dev : 0.0;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_long;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        double sum = 0.0;
+        for (int64_t ch = chunk_first[s]; ch < chunk_first[s + 1]; ch++) sum += partial[ch];
+        epilogue_store(y, long_rows[s], sum, c, yprev);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// device CSR -> CSC (CSR of A^T), deterministic: in-column order by (row, position)
+__global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ col, int32_t *cnt) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[col[p]], 1);
+}
+
+// exclusive scan of int32 counts into int64 offsets: per-block scan of 1024 items
+__global__ void k_scan_block(int64_t n, const int32_t *__restrict__ in, int64_t *out, int64_t *bsum) {
+    __shared__ int64_t wsum[32];
+    const int64_t i = blockIdx.x * 1024ll + threadIdx.x;
+    int64_t v = (i < n) ? in[i] : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int64_t s = wsum[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int64_t o = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += o;
+        }
+        wsum[lane] = s;  // inclusive warp sums
+    }
+    __syncthreads();
+    int64_t excl = incl - v + (w > 0 ? wsum[w - 1] : 0);
+    if (i < n) out[i] = excl;
+    if (threadIdx.x == 1023) bsum[blockIdx.x] = excl + v;
+}
+
+__global__ void k_scan_add(int64_t n, int64_t *out, const int64_t *boff) {
+    const int64_t i = blockIdx.x * 1024ll + threadIdx.x;
+    if (i < n) out[i] += boff[blockIdx.x];
+}
+
+// warp per row: claim a slot in each column; key = (row << 32) | in-row index
+__global__ void k_csc_fill(int64_t nrows, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           unsigned long long *cursor, uint64_t *key) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t p0 = rp[r], p1 = rp[r + 1];
+        for (int64_t p = p0 + lane; p < p1; p += 32) {
+            unsigned long long pos = atomicAdd(&cursor[col[p]], 1ull);
+            key[pos] = ((uint64_t)r << 32) | (uint64_t)(p - p0);
+        }
+    }
+}
+
+// bitonic sort of one segment held in shared memory (n2 = power of two >= len)
+__device__ void bitonic_smem(uint64_t *s, int n2) {
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    bool up = ((i & k) == 0);
+                    uint64_t a = s[i], b = s[ixj];
+                    if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+constexpr int kSegSmem = 4096;  // keys sorted per CTA in shared memory
+
+// segments of length <= kSegSmem: one CTA per segment (grid-stride)
+__global__ void __launch_bounds__(256) k_seg_sort(int64_t nseg, const int64_t *__restrict__ off, uint64_t *key) {
+    __shared__ uint64_t s[kSegSmem];
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const int64_t a = off[g], len = off[g + 1] - a;
+        if (len <= 1 || len > kSegSmem) continue;
+        int n2 = 1;
+        while (n2 < len) n2 <<= 1;
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) s[i] = (i < len) ? key[a + i] : ~0ull;
+        __syncthreads();
+        bitonic_smem(s, n2);
+        for (int i = threadIdx.x; i < len; i += blockDim.x) key[a + i] = s[i];
+        __syncthreads();
+    }
+}
+
+// sort chunk `blockIdx.x` (kSegSmem keys) of one long segment
+__global__ void __launch_bounds__(256) k_chunk_sort(uint64_t *key, int64_t len) {
+    __shared__ uint64_t s[kSegSmem];
+    const int64_t a = blockIdx.x * (int64_t)kSegSmem;
+    const int64_t l = min((int64_t)kSegSmem, len - a);
+    for (int i = threadIdx.x; i < kSegSmem; i += blockDim.x) s[i] = (i < l) ? key[a + i] : ~0ull;
+    __syncthreads();
+    bitonic_smem(s, kSegSmem);
+    for (int i = threadIdx.x; i < l; i += blockDim.x) key[a + i] = s[i];
+}
+
+// merge sorted runs of width w pairwise by rank (keys are unique)
+__global__ void k_merge_runs(const uint64_t *__restrict__ in, uint64_t *out, int64_t len, int64_t w) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t run = i / w, pair0 = (run & ~1ll) * w;
+        const bool left = (run & 1) == 0;
+        const int64_t o0 = left ? pair0 + w : pair0;          // other run start
+        const int64_t o1 = min(len, o0 + w);
+        const int64_t myrun0 = left ? pair0 : pair0 + w;
+        if (o0 >= len) { out[i] = in[i]; continue; }
+        const uint64_t v = in[i];
+        int64_t lo = o0, hi = o1;  // number of keys < v in the other run
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (in[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        out[pair0 + (i - myrun0) + (lo - o0)] = v;
+    }
+}
+
+__global__ void k_csc_gather(int64_t nnz, const uint64_t *__restrict__ key, const int64_t *__restrict__ rp,
+                             const double *__restrict__ val, int32_t *tcol, double *tval) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = key[s];
+        const int64_t r = (int64_t)(k >> 32);
+        const int64_t p = rp[r] + (int64_t)(k & 0xffffffffull);
+        tcol[s] = (int32_t)r;
+        tval[s] = val[p];
+    }
+}
+
+inline void check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+T *dev_alloc(CsrOp &op, size_t n) {
+    void *p = nullptr;
+    check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    op.owned.push_back(p);
+    return (T *)p;
+}
+
+int grid_for(int64_t work, int threads, int cap = 148 * 16) {
+    int64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+}  // namespace
+
+void csr_free(CsrOp &op) {
+    for (void *p : op.owned) cudaFree(p);
+    op.owned.clear();
+}
+
+void csr_analyze(CsrOp &op, cudaStream_t s) {
+    unsigned long long *cnt = dev_alloc<unsigned long long>(op, 16);
+    check(cudaMemsetAsync(cnt, 0, 16 * sizeof(unsigned long long), s), "memset");
+    k_bin_count<<<grid_for(op.nrows, 256), 256, 0, s>>>(op.nrows, op.row_ptr, cnt);
+    unsigned long long hc[8];
+    check(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    int64_t off[9];
+    off[0] = 0;
+    for (int b = 0; b < 8; b++) off[b + 1] = off[b] + (int64_t)hc[b];
+    for (int b = 0; b < 8; b++) op.bin_off[b] = off[b];
+    op.bin_rows = dev_alloc<int32_t>(op, (size_t)op.nrows);
+    int64_t *doff = dev_alloc<int64_t>(op, 9);
+    check(cudaMemcpyAsync(doff, off, sizeof(off), cudaMemcpyHostToDevice, s), "H2D");
+    unsigned long long *cur = cnt + 8;
+    check(cudaMemsetAsync(cur, 0, 8 * sizeof(unsigned long long), s), "memset");
+    k_bin_fill<<<grid_for(op.nrows, 256), 256, 0, s>>>(op.nrows, op.row_ptr, cur, doff, op.bin_rows);
+    // long rows: host-side deterministic chunk table (few rows)
+    op.n_long = off[7] - off[6];
+    if (op.n_long > 0) {
+        std::vector<int32_t> lr(op.n_long);
+        check(cudaMemcpyAsync(lr.data(), op.bin_rows + off[6], op.n_long * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, s), "D2H");
+        check(cudaStreamSynchronize(s), "sync");
+        std::sort(lr.begin(), lr.end());
+        std::vector<int64_t> first(op.n_long + 1);
+        std::vector<int32_t> crow;
+        int64_t nch = 0;
+        for (int64_t i = 0; i < op.n_long; i++) {
+            int64_t rr[2];
+            check(cudaMemcpy(rr, op.row_ptr + lr[i], 2 * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+            int64_t L = rr[1] - rr[0];
+            first[i] = nch;
+            int64_t c = (L + kLongRow - 1) / kLongRow;
+            for (int64_t q = 0; q < c; q++) crow.push_back((int32_t)i);
+            nch += c;
+        }
+        first[op.n_long] = nch;
+        op.n_chunks = nch;
+        op.long_rows = dev_alloc<int32_t>(op, op.n_long);
+        op.chunk_first = dev_alloc<int64_t>(op, op.n_long + 1);
+        op.chunk_row = dev_alloc<int32_t>(op, nch);
+        op.chunk_partial = dev_alloc<double>(op, nch);
+        check(cudaMemcpyAsync(op.long_rows, lr.data(), op.n_long * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
+        check(cudaMemcpyAsync(op.chunk_first, first.data(), (op.n_long + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s), "H2D");
+        check(cudaMemcpyAsync(op.chunk_row, crow.data(), nch * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
+    }
+    check(cudaStreamSynchronize(s), "sync");
+    check(cudaGetLastError(), "analyze");
+}
+
+void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
+    const int64_t n = a.ncols, nnz = a.nnz;
+    at.nrows = n;
+    at.ncols = a.nrows;
+    at.nnz = nnz;
+    int32_t *cnt = dev_alloc<int32_t>(at, (size_t)n);
+    int64_t *tp = dev_alloc<int64_t>(at, (size_t)n + 1);
+    int32_t *tcol = dev_alloc<int32_t>(at, (size_t)nnz);
+    double *tval = dev_alloc<double>(at, (size_t)nnz);
+    check(cudaMemsetAsync(cnt, 0, n * sizeof(int32_t), s), "memset");
+    k_col_count<<<grid_for(nnz, 256), 256, 0, s>>>(nnz, a.col, cnt);
+    // exclusive scan -> tp[0..n-1], tp[n] = nnz
+    const int64_t nb = (n + 1023) / 1024;
+    int64_t *bsum = nullptr, *boff = nullptr;
+    check(cudaMalloc(&bsum, std::max<int64_t>(nb, 1) * sizeof(int64_t)), "cudaMalloc");
+    check(cudaMalloc(&boff, std::max<int64_t>(nb, 1) * sizeof(int64_t)), "cudaMalloc");
+    k_scan_block<<<(unsigned)nb, 1024, 0, s>>>(n, cnt, tp, bsum);
+    std::vector<int64_t> hb(nb), ho(nb);
+    check(cudaMemcpyAsync(hb.data(), bsum, nb * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    int64_t acc = 0;
+    for (int64_t i = 0; i < nb; i++) { ho[i] = acc; acc += hb[i]; }
+    check(cudaMemcpyAsync(boff, ho.data(), nb * sizeof(int64_t), cudaMemcpyHostToDevice, s), "H2D");
+    k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(n, tp, boff);
+    check(cudaMemcpyAsync(tp + n, &nnz, sizeof(int64_t), cudaMemcpyHostToDevice, s), "H2D");
+    // fill keys
+    unsigned long long *cursor = nullptr;
+    uint64_t *key = nullptr, *tmp = nullptr;
+    check(cudaMalloc(&cursor, std::max<int64_t>(n, 1) * sizeof(unsigned long long)), "cudaMalloc");
+    check(cudaMalloc(&key, std::max<int64_t>(nnz, 1) * sizeof(uint64_t)), "cudaMalloc");
+    static_assert(sizeof(unsigned long long) == sizeof(int64_t), "");
+    check(cudaMemcpyAsync(cursor, tp, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s), "D2D");
+    k_csc_fill<<<grid_for(a.nrows * 32, 256), 256, 0, s>>>(a.nrows, a.row_ptr, a.col, cursor, key);
+    k_seg_sort<<<148 * 8, 256, 0, s>>>(n, tp, key);
+    // long columns (> kSegSmem): chunk sort + rank merges (host driven, rare)
+    std::vector<int64_t> htp(n + 1);
+    check(cudaMemcpyAsync(htp.data(), tp, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    for (int64_t c = 0; c < n; c++) {
+        int64_t len = htp[c + 1] - htp[c];
+        if (len <= kSegSmem) continue;
+        if (!tmp) check(cudaMalloc(&tmp, nnz * sizeof(uint64_t)), "cudaMalloc");
+        uint64_t *seg = key + htp[c], *alt = tmp + htp[c];
+        k_chunk_sort<<<(unsigned)((len + kSegSmem - 1) / kSegSmem), 256, 0, s>>>(seg, len);
+        for (int64_t w = kSegSmem; w < len; w <<= 1) {
+            k_merge_runs<<<grid_for(len, 256), 256, 0, s>>>(seg, alt, len, w);
+            std::swap(seg, alt);
+        }
+        if (seg != key + htp[c])
+            check(cudaMemcpyAsync(key + htp[c], seg, len * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s), "D2D");
+    }
+    k_csc_gather<<<grid_for(nnz, 256), 256, 0, s>>>(nnz, key, a.row_ptr, a.val, tcol, tval);
+    check(cudaStreamSynchronize(s), "sync");
+    check(cudaGetLastError(), "transpose");
+    cudaFree(bsum);
+    cudaFree(boff);
+    cudaFree(cursor);
+    cudaFree(key);
+    if (tmp) cudaFree(tmp);
+    at.row_ptr = tp;
+    at.col = tcol;
+    at.val = tval;
+    csr_analyze(at, s);
+}
+
+void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
+              const int *abort, cudaStream_t s) {
+    const int64_t *o = A.bin_off;
+    const int cap = 148 * 8;
+#define LAUNCH_VEC(G, b)                                                                       \
+    if (o[b + 1] > o[b]) {                                                                     \
+        int64_t cnt = o[b + 1] - o[b];                                                         \
+        k_spmv_vec<G><<<grid_for(cnt * G, 256, cap), 256, 0, s>>>(A.bin_rows + o[b], cnt, A.row_ptr, \
+                                                                  A.col, A.val, x, y, c_dev, yprev, abort); \
+        count_launch();                                                                        \
+    }
+    LAUNCH_VEC(2, 0)
+    LAUNCH_VEC(4, 1)
+    LAUNCH_VEC(8, 2)
+    LAUNCH_VEC(16, 3)
+    LAUNCH_VEC(32, 4)
+#undef LAUNCH_VEC
+    if (o[6] > o[5]) {
+        int64_t cnt = o[6] - o[5];
+        k_spmv_cta<<<(unsigned)std::min<int64_t>(cnt, cap), 256, 0, s>>>(A.bin_rows + o[5], cnt, A.row_ptr, A.col,
+                                                                          A.val, x, y, c_dev, yprev, abort);
+        count_launch();
+    }
+    if (A.n_long > 0) {
+        k_spmv_chunks<<<(unsigned)std::min<int64_t>(A.n_chunks, cap), 256, 0, s>>>(
+            A.n_chunks, A.chunk_row, A.chunk_first, A.long_rows, A.row_ptr, A.col, A.val, x, A.chunk_partial, abort);
+        k_spmv_chunks_fix<<<grid_for(A.n_long, 128), 128, 0, s>>>(A.n_long, A.long_rows, A.chunk_first,
+                                                                  A.chunk_partial, y, c_dev, yprev, abort);
+        count_launch();
+        count_launch();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dense GEMV
+namespace {
+
+// y_partial[split][r] = sum over this split's columns of A[r, c] x[c]
+// CTA = 8 warps over a 64-row strip; warp w takes columns c0 + w + 8q.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_gemv_n(int64_t m, int64_t n, const double *__restrict__ A, int64_t ld,
+                                                const double *__restrict__ x, double *partial, int64_t cols_per_split,
+                                                const int *abort) {
+    if (aborted(abort)) return;
+    __shared__ double red[8][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r0 = blockIdx.x * 64ll;
+    const int64_t c0 = blockIdx.y * cols_per_split;
+    const int64_t c1 = min(n, c0 + cols_per_split);
+    const int64_t r = r0 + 2 * lane;
+    double a0 = 0.0, a1 = 0.0;
+    if (VEC && r + 1 < m) {
+        const double *base = A + r;
+        int64_t c = c0 + w;
+        for (; c + 8 * 7 < c1; c += 8 * 8) {
+            double2 v[8];
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                v[u] = __ldcs(reinterpret_cast<const double2 *>(base + (c + 8 * u) * ld));
+                xv[u] = __ldg(x + c + 8 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                a0 = fma(v[u].x, xv[u], a0);
+                a1 = fma(v[u].y, xv[u], a1);
+            }
+        }
+        for (; c < c1; c += 8) {
+            double2 v = __ldcs(reinterpret_cast<const double2 *>(base + c * ld));
+            double xv = __ldg(x + c);
+            a0 = fma(v.x, xv, a0);
+            a1 = fma(v.y, xv, a1);
+        }
+    } else {
+        for (int64_t c = c0 + w; c < c1; c += 8) {
+            double xv = __ldg(x + c);
+            if (r < m) a0 = fma(A[r + c * ld], xv, a0);
+            if (r + 1 < m) a1 = fma(A[r + 1 + c * ld], xv, a1);
+        }
+    }
+    red[w][2 * lane] = a0;
+    red[w][2 * lane + 1] = a1;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) s += red[q][threadIdx.x];
+        const int64_t rr = r0 + threadIdx.x;
+        if (rr < m) partial[blockIdx.y * m + rr] = s;
+    }
+}
+
+// y_partial[split][c] = sum over rows of split of A[r,c] x[r]; warp per column.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_gemv_t(int64_t m, int64_t n, const double *__restrict__ A, int64_t ld,
+                                                const double *__restrict__ x, double *partial, int64_t rows_per_split,
+                                                const int *abort) {
+    if (aborted(abort)) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t c = blockIdx.x * 8ll + w;
+    const int64_t r0 = blockIdx.y * rows_per_split;
+    const int64_t r1 = min(m, r0 + rows_per_split);
+    if (c >= n) return;
+    const double *col = A + c * ld;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (VEC) {
+        int64_t r = r0 + 2 * lane;
+        for (; r + 64 * 7 + 1 < r1; r += 64 * 8) {
+            double2 v[8], xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                v[u] = __ldcs(reinterpret_cast<const double2 *>(col + r + 64 * u));
+                xv[u] = __ldg(reinterpret_cast<const double2 *>(x + r + 64 * u));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                acc0 = fma(v[u].x, xv[u].x, acc0);
+                acc1 = fma(v[u].y, xv[u].y, acc1);
+            }
+        }
+        for (; r + 1 < r1; r += 64) {
+            double2 v = __ldcs(reinterpret_cast<const double2 *>(col + r));
+            double2 xv = __ldg(reinterpret_cast<const double2 *>(x + r));
+            acc0 = fma(v.x, xv.x, acc0);
+            acc1 = fma(v.y, xv.y, acc1);
+        }
+        if (r < r1) acc0 = fma(col[r], x[r], acc0);
+    } else {
+        for (int64_t r = r0 + lane; r < r1; r += 32) acc0 = fma(col[r], x[r], acc0);
+    }
+    double s = acc0 + acc1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) partial[blockIdx.y * n + c] = s;
+}
+
+__global__ void k_split_reduce(int64_t len, int splits, const double *__restrict__ partial, double *y,
+                               const double *c_dev, const double *yprev, const int *abort) {
+    if (aborted(abort)) return;
+    const double c = c_dev ? *c_dev : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < splits; q++) s += partial[q * len + i];
+        epilogue_store(y, i, s, c, yprev);
+    }
+}
+
+}  // namespace
+
+void gemv_n(const DenseOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
+            const int *abort, cudaStream_t s) {
+    const int64_t m = A.nrows, n = A.ncols;
+    const int64_t rb = (m + 63) / 64;
+    const int splits = A.splits_n;
+    const int64_t cps = (n + splits - 1) / splits;
+    dim3 grid((unsigned)rb, (unsigned)splits);
+    const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0);
+    if (vec) k_gemv_n<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, cps, abort);
+    else k_gemv_n<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, cps, abort);
+    k_split_reduce<<<grid_for(m, 256), 256, 0, s>>>(m, splits, A.partial, y, c_dev, yprev, abort);
+    count_launch();
+    count_launch();
+}
+
+void gemv_t(const DenseOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
+            const int *abort, cudaStream_t s) {
+    const int64_t m = A.nrows, n = A.ncols;
+    const int splits = A.splits_t;
+    int64_t rps = (m + splits - 1) / splits;
+    rps = (rps + 1) & ~1ll;  // even, keeps 16-byte alignment of every split start
+    dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
+    const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if (vec) k_gemv_t<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    else k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    k_split_reduce<<<grid_for(n, 256), 256, 0, s>>>(n, splits, A.partial, y, c_dev, yprev, abort);
+    count_launch();
+    count_launch();
+}
+
+}  // namespace svdsc

@@ -1,0 +1,975 @@
+// svdsc.cu -- C ABI (include/svdsc.h) and the host driver of Alg. 2.
+//
+// The host issues every kernel of a pass asynchronously on the handle's stream
+// and synchronizes ONCE per pass (to read the convergence flag of Alg. 2
+// step 5).  Data-dependent rare events (Lanczos breakdown,
+// DESIGN.md reading Q7) do not need a per-step sync: the normalizing kernel
+// raises a device flag, every later kernel of the pass becomes a no-op, and
+// the host repairs the broken vector at the pass-end sync and resumes.
+//
+// Multi-GPU: A is row-partitioned; U rows follow A's rows;
+// V is split into equal slices of n_pad / P rows.  Per Lanczos step:
+// reduce-scatter of the partial A^T u, all-gather of v_{i+1}, and all-reduces
+// of the CGS2 coefficient vectors and of the squared norms (NCCL, loaded with
+// dlopen so the library itself has no link-time NCCL dependency).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace svdsc;
+
+// ---------------------------------------------------------------------------
+// NCCL (runtime-loaded)
+namespace {
+typedef struct ncclComm *ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+struct Nccl {
+    bool tried = false, ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+
+bool nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+#define SYM(name, field) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(lib, name))
+    SYM("ncclGetUniqueId", GetUniqueId);
+    SYM("ncclCommInitRank", CommInitRank);
+    SYM("ncclCommDestroy", CommDestroy);
+    SYM("ncclAllReduce", AllReduce);
+    SYM("ncclReduceScatter", ReduceScatter);
+    SYM("ncclAllGather", AllGather);
+    SYM("ncclGetErrorString", GetErrorString);
+#undef SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
+                g_nccl.AllGather;
+    return g_nccl.ok;
+}
+
+struct SvdscError : std::runtime_error {
+    svdsc_status st;
+    SvdscError(svdsc_status s, const std::string &m) : std::runtime_error(m), st(s) {}
+};
+
+inline void ck(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw SvdscError(SVDSC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+inline void ckn(ncclResult_t r, const char *what) {
+    if (r != 0)
+        throw SvdscError(SVDSC_ENCCL, std::string(what) + ": " +
+                                          (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
+}
+inline void einval(bool bad, const std::string &m) {
+    if (bad) throw SvdscError(SVDSC_EINVAL, m);
+}
+}  // namespace
+
+struct svdsc_handle {
+    int device = 0, nsm = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    Ctrl *hctrl = nullptr;       // pinned host mirror of the control block
+    void *scratch = nullptr;     // op-level scratch
+    size_t scratch_bytes = 0;
+};
+
+struct svdsc_matrix {
+    svdsc_handle *h = nullptr;
+    int kind = 0;  // 0 CSR, 1 dense
+    int64_t m_local = 0, n = 0, row_offset = 0, m_global = 0, nnz = 0;
+    CsrOp A, At;
+    DenseOp D;
+    double *dense_partial = nullptr;
+};
+
+namespace {
+
+template <typename F>
+svdsc_status guarded(svdsc_handle *h, F &&f) {
+    try {
+        f();
+        return SVDSC_OK;
+    } catch (const SvdscError &e) {
+        if (h) h->err = e.what();
+        return e.st;
+    } catch (const std::exception &e) {
+        if (h) h->err = e.what();
+        return SVDSC_ECUDA;
+    }
+}
+
+int64_t roundup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// validation kernels (contract checks before any compute)
+__global__ void k_validate_csr(int64_t m, int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col,
+                               const double *val, int *bad) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = tid; r < m; r += stride)
+        if (rp[r + 1] < rp[r]) atomicOr(bad, 1);
+    for (int64_t p = tid; p < nnz; p += stride) {
+        if (col[p] < 0 || col[p] >= n) atomicOr(bad, 2);
+        if (!isfinite(val[p])) atomicOr(bad, 4);
+    }
+    if (tid == 0 && (rp[0] != 0 || rp[m] != nnz)) atomicOr(bad, 8);
+}
+
+__global__ void k_validate_dense(int64_t m, int64_t n, int64_t ld, const double *a, int *bad) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx % m, c = idx / m;
+        if (!isfinite(a[r + c * ld])) atomicOr(bad, 4);
+    }
+}
+
+// V(:, 0:k) of every rank's slice, gathered slice-major -> column-major n x k
+void copy_gathered(const double *tmp, int64_t ns, int k, int P, int64_t n, double *V, int64_t ldv, cudaStream_t s) {
+    for (int q = 0; q < P; q++) {
+        const int64_t rows = std::min(ns, n - q * ns);
+        if (rows <= 0) continue;
+        ck(cudaMemcpy2DAsync(V + q * ns, ldv * sizeof(double), tmp + (int64_t)q * ns * k, ns * sizeof(double),
+                             rows * sizeof(double), k, cudaMemcpyDeviceToDevice, s),
+           "memcpy2D");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+struct Ws {
+    double *U = nullptr, *V = nullptr, *T = nullptr;
+    double *W = nullptr, *Vw = nullptr, *Uh = nullptr, *Vh = nullptr, *Sh = nullptr;
+    double *partial = nullptr, *h1 = nullptr, *h2 = nullptr, *nrm = nullptr, *rho = nullptr, *resid = nullptr;
+    double *yfull = nullptr, *vfull = nullptr, *vtmp = nullptr;
+    Ctrl *ctrl = nullptr;
+    int64_t ldu = 0, ldv = 0, nv = 0, n_pad = 0;
+    int ldt = 0;
+};
+
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    T *take(size_t n) {
+        off = roundup((int64_t)off, 256);
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += std::max<size_t>(n, 1) * sizeof(T);
+        return p;
+    }
+};
+
+size_t carve(Ws &w, void *base, int64_t m, int64_t n, int t, int k, int P) {
+    Carver c{reinterpret_cast<char *>(base)};
+    w.n_pad = roundup(n, P);
+    w.nv = w.n_pad / P;
+    w.ldu = roundup(std::max<int64_t>(m, 1), 32);
+    w.ldv = roundup(std::max<int64_t>(w.nv, 1), 32);
+    w.ldt = t + 1;
+    w.ctrl = c.take<Ctrl>(1);
+    w.U = c.take<double>((size_t)w.ldu * (t + 1));
+    w.V = c.take<double>((size_t)w.ldv * (t + 1));
+    w.T = c.take<double>((size_t)(t + 1) * (t + 1));
+    w.W = c.take<double>((size_t)t * t);
+    w.Vw = c.take<double>((size_t)t * t);
+    w.Uh = c.take<double>((size_t)t * t);
+    w.Vh = c.take<double>((size_t)t * t);
+    w.Sh = c.take<double>(t);
+    w.partial = c.take<double>((size_t)(t + 2) * kMaxBlocks);
+    w.h1 = c.take<double>(t + 2);
+    w.h2 = c.take<double>(t + 2);
+    w.nrm = c.take<double>(4);
+    w.rho = c.take<double>(k);
+    w.resid = c.take<double>(k);
+    if (P > 1) {
+        w.yfull = c.take<double>(w.n_pad);
+        w.vfull = c.take<double>(w.n_pad);
+        w.vtmp = c.take<double>((size_t)w.n_pad * k);
+    }
+    return c.off + 256;
+}
+
+int resolve_t(const svdsc_opts *o, int64_t m_global, int64_t n) {
+    int64_t t = o->t > 0 ? o->t : std::max<int64_t>(15, 3 * (int64_t)o->k);
+    t = std::min<int64_t>(t, std::min(m_global, n) - 1);
+    return (int)t;
+}
+
+void check_opts(const svdsc_matrix *M, const svdsc_opts *o) {
+    einval(!o, "opts is NULL");
+    einval(o->k < 1, "k must be >= 1");
+    einval(!(o->tol > 0.0), "tol must be > 0");
+    const int t = resolve_t(o, M->m_global, M->n);
+    einval(t < o->k + 2, "subspace dimension t = min(max(15,3k), min(m,n)-1) < k+2 (SPEC.md:309)");
+    einval(t > 1023, "t > 1023 is not supported");
+    einval(o->reorth != 0 && o->reorth != 2, "reorth must be 0 or 2");
+}
+
+// ---------------------------------------------------------------------------
+// the solver for one call
+struct Solver {
+    svdsc_matrix *M;
+    svdsc_handle *H;
+    const svdsc_opts *o;
+    Ws w;
+    RedBuf rb;
+    cudaStream_t s;
+    int t, k, P, rank, nsm;
+    int64_t m, nv, n;
+    const int *abort;
+    int64_t matvecs = 0, steps = 0, breakdowns = 0, bytes_model = 0;
+    uint64_t bd_stream = 0;
+    int check = 0;
+    int64_t bytesA = 0;
+
+    // ---- collectives (no-ops for P = 1) ----
+    void allreduce(double *buf, size_t count) {
+        if (P > 1) ckn(g_nccl.AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, H->comm, s), "ncclAllReduce");
+    }
+
+    // z = A x - c zprev on the local rows (x = V column slice)
+    void Av(const double *vcol, double *z, const double *c_dev, const double *zprev) {
+        const double *x = vcol;
+        if (P > 1) {
+            ckn(g_nccl.AllGather(vcol, w.vfull, (size_t)nv, kNcclFloat64, H->comm, s), "ncclAllGather");
+            x = w.vfull;
+        }
+        if (M->kind == 0) spmv_csr(M->A, x, z, c_dev, zprev, abort, s);
+        else gemv_n(M->D, x, z, c_dev, zprev, abort, s);
+        matvecs++;
+    }
+    // wslice = (A^T u)_slice - c wprev
+    void Atu(const double *u, double *wcol, const double *c_dev, const double *wprev) {
+        if (P == 1) {
+            if (M->kind == 0) spmv_csr(M->At, u, wcol, c_dev, wprev, abort, s);
+            else gemv_t(M->D, u, wcol, c_dev, wprev, abort, s);
+        } else {
+            if (M->kind == 0) spmv_csr(M->At, u, w.yfull, nullptr, nullptr, abort, s);
+            else gemv_t(M->D, u, w.yfull, nullptr, nullptr, abort, s);
+            ckn(g_nccl.ReduceScatter(w.yfull, wcol, (size_t)nv, kNcclFloat64, kNcclSum, H->comm, s),
+                "ncclReduceScatter");
+            if (c_dev) axpy_dev(nv, wcol, c_dev, wprev, abort, s);
+        }
+        matvecs++;
+    }
+    // two-pass CGS against Q(:, 0:ncols) then ||w||^2 in rb.nrm
+    void cgs2(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, bool force_reorth) {
+        if (ncols > 0 && (o->reorth != 0 || force_reorth)) {
+            cgs_p1(N, ncols, Q, ldq, wv, rb, abort, nsm, s);
+            allreduce(rb.h1, ncols);
+            cgs_p2(N, ncols, Q, ldq, wv, rb, abort, nsm, s);
+            allreduce(rb.h2, ncols + 1);
+            cgs_p3(N, ncols, Q, ldq, wv, rb.h2, rb, abort, nsm, s);
+        } else {
+            cgs_p3(N, 0, Q, ldq, wv, nullptr, rb, abort, nsm, s);
+        }
+        allreduce(rb.nrm, 1);
+    }
+
+    double *Ucol(int j) { return w.U + (int64_t)j * w.ldu; }
+    double *Vcol(int j) { return w.V + (int64_t)j * w.ldv; }
+    double *Tm(int i, int j) { return w.T + i + (int64_t)j * w.ldt; }
+
+    // half-steps: 0 start (u_1), 1 V side of step i, 2 U side of step i, 3 restart u_{k+1}
+    struct Half {
+        int kind, i;
+    };
+
+    void run_half(const Half &h, int chk) {
+        switch (h.kind) {
+            case 0:  // Alg. 1 lines 2-3
+                Av(Vcol(0), Ucol(0), nullptr, nullptr);
+                cgs2(m, 0, w.U, w.ldu, Ucol(0), false);
+                normalize(m, Ucol(0), rb, w.ctrl, Tm(0, 0), chk, 0, nsm, s);
+                bytes_model += bytesA + 8 * m * 5;
+                break;
+            case 1: {  // Alg. 1 lines 5-6 + re-orthogonalization
+                const int i = h.i;
+                Atu(Ucol(i - 1), Vcol(i), Tm(i - 1, i - 1), Vcol(i - 1));
+                cgs2(nv, i, w.V, w.ldv, Vcol(i), false);
+                normalize(nv, Vcol(i), rb, w.ctrl, Tm(i - 1, i), chk, 0, nsm, s);
+                steps++;
+                bytes_model += bytesA + 8 * nv * (3 * (int64_t)i + 5);
+                break;
+            }
+            case 2: {  // Alg. 1 lines 7-8 + re-orthogonalization
+                const int i = h.i;
+                Av(Vcol(i), Ucol(i), Tm(i - 1, i), Ucol(i - 1));
+                cgs2(m, i, w.U, w.ldu, Ucol(i), false);
+                normalize(m, Ucol(i), rb, w.ctrl, Tm(i, i), chk, 0, nsm, s);
+                bytes_model += bytesA + 8 * m * (3 * (int64_t)i + 5);
+                break;
+            }
+            case 3: {  // Alg. 2 steps 10-11: u_{k+1} = A v_{k+1} - Uk rho, re-orth
+                Av(Vcol(k), Ucol(k), nullptr, nullptr);
+                cgs_p3(m, k, w.U, w.ldu, Ucol(k), w.rho, rb, abort, nsm, s);
+                cgs2(m, k, w.U, w.ldu, Ucol(k), false);
+                normalize(m, Ucol(k), rb, w.ctrl, Tm(k, k), chk, 0, nsm, s);
+                break;
+            }
+        }
+    }
+
+    // breakdown repair (reading Q7): replacement vector, CGS2, normalize
+    void fix(const Half &h) {
+        double *col;
+        const double *Q;
+        int64_t N, ldq, off;
+        int ncols;
+        if (h.kind == 1) {
+            col = Vcol(h.i), Q = w.V, N = nv, ldq = w.ldv, ncols = h.i, off = (int64_t)rank * nv;
+        } else {
+            const int j = h.kind == 0 ? 0 : (h.kind == 2 ? h.i : k);
+            col = Ucol(j), Q = w.U, N = m, ldq = w.ldu, ncols = j, off = M->row_offset;
+        }
+        const int64_t valid = (h.kind == 1) ? std::max<int64_t>(0, std::min(nv, n - off)) : N;
+        if (valid < N) ck(cudaMemsetAsync(col + valid, 0, (N - valid) * sizeof(double), s), "memset");
+        breakdown_vector(valid, off, col, o->seed, bd_stream++, s);
+        cgs2(N, ncols, Q, ldq, col, true);
+        normalize(N, col, rb, w.ctrl, nullptr, 0, 1, nsm, s);
+        breakdowns++;
+    }
+
+    Ctrl read_ctrl() {
+        ck(cudaMemcpyAsync(H->hctrl, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H ctrl");
+        ck(cudaStreamSynchronize(s), "sync");
+        ck(cudaGetLastError(), "kernels");
+        return *H->hctrl;
+    }
+
+    // runs the plan from pos; handles breakdowns; returns with the pass complete
+    void run_plan(const std::vector<Half> &plan, int c0, bool with_svd) {
+        size_t pos = 0;
+        for (;;) {
+            for (size_t idx = pos; idx < plan.size(); idx++) run_half(plan[idx], c0 + (int)idx);
+            if (with_svd) {
+                small_svd(t, w.T, w.ldt, w.W, w.Vw, w.Uh, w.Sh, w.Vh, k, w.ctrl, abort, s);
+                residuals(t, k, w.T, w.ldt, w.Uh, w.Sh, o->tol, w.resid, w.ctrl, abort, s);
+            }
+            Ctrl c = read_ctrl();
+            if (!c.abort) return;
+            const int idx = c.abort_check - c0;
+            if (idx < 0 || idx >= (int)plan.size()) throw SvdscError(SVDSC_ECUDA, "breakdown bookkeeping");
+            const int zero = 0;
+            ck(cudaMemcpyAsync(&w.ctrl->abort, &zero, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+            fix(plan[idx]);
+            pos = idx + 1;
+        }
+    }
+
+    svdsc_status solve(void *ws_base, double *S, double *Uout, int64_t ldu_out, double *Vout, int64_t ldv_out,
+                       double *resid, svdsc_info *info, bool lbp_only, double *Tout) {
+        const int maxit = o->maxit > 0 ? o->maxit : 10;
+        carve(w, ws_base, m, n, t, k, P);
+        nv = w.nv;
+        rb = RedBuf{w.partial, kMaxBlocks, w.h1, w.h2, w.nrm, w.ctrl->cnt};
+        abort = &w.ctrl->abort;
+        bytesA = M->kind == 0 ? 12 * M->nnz + 4 * (m + 1) : 8 * m * n;
+        ck(cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s), "memset");
+        ck(cudaMemsetAsync(w.T, 0, sizeof(double) * (t + 1) * (t + 1), s), "memset");
+        if (P > 1) {
+            ck(cudaMemsetAsync(w.V, 0, sizeof(double) * w.ldv * (t + 1), s), "memset");
+            ck(cudaMemsetAsync(w.yfull, 0, sizeof(double) * w.n_pad, s), "memset");
+        }
+        if (lbp_only) ck(cudaMemsetAsync(w.U, 0, sizeof(double) * w.ldu * (t + 1), s), "memset");
+        // Alg. 1 line 1: v_1 = v0 / ||v0||
+        const int64_t off = (int64_t)rank * nv, valid = std::max<int64_t>(0, std::min(nv, n - off));
+        if (o->v0) {
+            if (valid > 0)
+                ck(cudaMemcpyAsync(Vcol(0), o->v0 + off, valid * sizeof(double), cudaMemcpyDeviceToDevice, s), "v0");
+        } else {
+            random_start(valid, off, Vcol(0), o->seed, s);
+        }
+        cgs2(nv, 0, w.V, w.ldv, Vcol(0), false);
+        double nv0 = 0.0;
+        ck(cudaMemcpyAsync(&nv0, w.nrm, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+        einval(!(nv0 > 0.0) || !std::isfinite(nv0), "start vector v0 is zero or not finite");
+        normalize(nv, Vcol(0), rb, w.ctrl, nullptr, 0, 1, nsm, s);
+
+        std::vector<Half> plan;
+        plan.push_back({0, 0});
+        for (int i = 1; i <= t; i++) {
+            plan.push_back({1, i});
+            if (i < t) plan.push_back({2, i});  // u_{t+1} is not needed (reading Q2)
+        }
+        int c0 = 0, passes = 0;
+        Ctrl c{};
+        if (lbp_only) {
+            run_plan(plan, c0, false);
+            for (int j = 0; j <= t; j++) {
+                ck(cudaMemcpyAsync(Uout + (int64_t)j * ldu_out, Ucol(j), m * sizeof(double), cudaMemcpyDeviceToDevice, s),
+                   "copy U");
+                ck(cudaMemcpyAsync(Vout + (int64_t)j * ldv_out, Vcol(j), n * sizeof(double), cudaMemcpyDeviceToDevice, s),
+                   "copy V");
+            }
+            ck(cudaMemcpyAsync(Tout, w.T, sizeof(double) * (t + 1) * (t + 1), cudaMemcpyDeviceToDevice, s), "copy T");
+            ck(cudaStreamSynchronize(s), "sync");
+            passes = 1;
+        } else {
+            for (;;) {
+                run_plan(plan, c0, true);
+                c = *H->hctrl;
+                if (c.svd_status != 0) throw SvdscError(SVDSC_ESVD_NOCONV, "small Jacobi SVD did not converge in 50 sweeps");
+                if (c.rankdef) throw SvdscError(SVDSC_ERANKDEF, "zero Ritz value with non-negligible residual");
+                passes++;
+                const bool stop = o->fixed_passes > 0 ? passes >= o->fixed_passes : (c.converged || passes >= maxit);
+                if (stop) break;
+                // augmented restart, Alg. 2 steps 8-12
+                recombine(m, t, k, w.U, w.ldu, w.Uh, t, w.U, w.ldu, nsm, s);
+                recombine(nv, t, k, w.V, w.ldv, w.Vh, t, w.V, w.ldv, nsm, s);
+                copy_col(nv, Vcol(t), Vcol(k), s);  // v_{k+1} = v_{t+1}
+                restart_T(t, k, w.T, w.ldt, w.Uh, w.Sh, w.rho, s);
+                matvecs += 0;
+                c0 += (int)plan.size();
+                plan.clear();
+                plan.push_back({3, 0});
+                for (int i = k + 1; i <= t; i++) {
+                    plan.push_back({1, i});
+                    if (i < t) plan.push_back({2, i});
+                }
+            }
+            // Alg. 2 steps 15-16: S, U_k = U(:,1:t) Uh(:,1:k), V_k likewise
+            ck(cudaMemcpyAsync(S, w.Sh, k * sizeof(double), cudaMemcpyDeviceToDevice, s), "S");
+            if (resid) ck(cudaMemcpyAsync(resid, w.resid, k * sizeof(double), cudaMemcpyDeviceToDevice, s), "resid");
+            recombine(m, t, k, w.U, w.ldu, w.Uh, t, Uout, ldu_out, nsm, s);
+            if (P == 1) {
+                recombine(nv, t, k, w.V, w.ldv, w.Vh, t, Vout, ldv_out, nsm, s);
+            } else {
+                recombine(nv, t, k, w.V, w.ldv, w.Vh, t, w.vtmp + (int64_t)rank * nv * k, nv, nsm, s);
+                ckn(g_nccl.AllGather(w.vtmp + (int64_t)rank * nv * k, w.vtmp, (size_t)nv * k, kNcclFloat64, H->comm, s),
+                    "ncclAllGather");
+                copy_gathered(w.vtmp, nv, k, P, n, Vout, ldv_out, s);
+            }
+            ck(cudaStreamSynchronize(s), "sync");
+            ck(cudaGetLastError(), "final");
+        }
+        if (info) {
+            info->passes = passes;
+            info->restarts = std::max(0, passes - 1);
+            info->converged = lbp_only ? 0 : c.converged;
+            info->t_used = t;
+            info->steps = steps;
+            info->matvecs = matvecs;
+            info->breakdowns = breakdowns;
+            info->max_resid = lbp_only ? 0.0 : c.max_resid;
+            info->bytes_model = bytes_model;
+        }
+        if (!lbp_only && !c.converged) return SVDSC_NOT_CONVERGED;
+        return SVDSC_OK;
+    }
+};
+
+svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o, void *ws, size_t ws_bytes, double *S, double *U,
+                        int64_t ldu, double *V, int64_t ldv, double *resid, svdsc_info *info, bool lbp_only,
+                        int t_override, double *Tout) {
+    svdsc_handle *H = M->h;
+    svdsc_status ret = SVDSC_OK;
+    const int64_t l0 = g_launches;
+    auto t0 = std::chrono::steady_clock::now();
+    svdsc_status st = guarded(H, [&] {
+        if (!lbp_only) check_opts(M, o);
+        einval(o->reorth != 0 && o->reorth != 2, "reorth must be 0 or 2");
+        Solver sv{};
+        sv.M = M;
+        sv.H = H;
+        sv.o = o;
+        sv.s = H->stream;
+        sv.k = o->k;
+        sv.t = t_override > 0 ? t_override : resolve_t(o, M->m_global, M->n);
+        sv.P = H->nranks;
+        sv.rank = H->rank;
+        sv.nsm = H->nsm;
+        sv.m = M->m_local;
+        sv.n = M->n;
+        einval(!lbp_only && (!S || !U || !V), "S, U and V must be non-NULL");
+        einval(!lbp_only && ldu < std::max<int64_t>(1, M->m_local), "ldu < m_local");
+        einval(!lbp_only && ldv < std::max<int64_t>(1, M->n), "ldv < ncols");
+        Ws probe;
+        const size_t need = carve(probe, nullptr, M->m_local, M->n, sv.t, sv.k, sv.P);
+        void *base = ws;
+        bool own = false;
+        if (!base) {
+            ck(cudaMallocAsync(&base, need, sv.s), "cudaMallocAsync workspace");
+            own = true;
+        } else {
+            einval(ws_bytes < need, "workspace too small (see svdsc_workspace_size)");
+        }
+        try {
+            ret = sv.solve(base, S, U, ldu, V, ldv, resid, info, lbp_only, Tout);
+        } catch (...) {
+            if (own) {
+                cudaFreeAsync(base, sv.s);
+                cudaStreamSynchronize(sv.s);
+            }
+            throw;
+        }
+        if (own) {
+            ck(cudaFreeAsync(base, sv.s), "cudaFreeAsync");
+            ck(cudaStreamSynchronize(sv.s), "sync");
+        }
+    });
+    if (info) {
+        info->seconds_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        info->launches = g_launches - l0;
+    }
+    return st != SVDSC_OK ? st : ret;
+}
+
+void matrix_common_dense_setup(svdsc_matrix *M) {
+    DenseOp &D = M->D;
+    const int64_t m = D.nrows, n = D.ncols;
+    const int nsm = M->h->nsm;
+    const int64_t rb = (m + 63) / 64;
+    D.splits_n = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)nsm * 8 + rb - 1) / std::max<int64_t>(rb, 1)));
+    D.splits_n = (int)std::min<int64_t>(D.splits_n, std::max<int64_t>(1, n / 16));
+    const int64_t cb = (n + 7) / 8;
+    D.splits_t = (int)std::max<int64_t>(1, std::min<int64_t>({64, ((int64_t)nsm * 8 + cb - 1) / cb, std::max<int64_t>(1, m / 1024)}));
+    const size_t need = std::max<size_t>((size_t)D.splits_n * m, (size_t)D.splits_t * n);
+    ck(cudaMalloc(&M->dense_partial, need * sizeof(double)), "cudaMalloc");
+    D.partial = M->dense_partial;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+const char *svdsc_version(void) { return "svdsc 0.1 sm_100a"; }
+
+svdsc_status svdsc_create(svdsc_handle **h, void *stream) {
+    if (!h) return SVDSC_EINVAL;
+    *h = nullptr;
+    svdsc_handle *H = new svdsc_handle();
+    svdsc_status st = guarded(H, [&] {
+        ck(cudaGetDevice(&H->device), "cudaGetDevice");
+        ck(cudaDeviceGetAttribute(&H->nsm, cudaDevAttrMultiProcessorCount, H->device), "attr");
+        H->stream = reinterpret_cast<cudaStream_t>(stream);
+        ck(cudaMallocHost(&H->hctrl, sizeof(Ctrl)), "cudaMallocHost");
+    });
+    if (st != SVDSC_OK) {
+        delete H;
+        return st;
+    }
+    *h = H;
+    return SVDSC_OK;
+}
+
+svdsc_status svdsc_set_stream(svdsc_handle *h, void *stream) {
+    if (!h) return SVDSC_EINVAL;
+    h->stream = reinterpret_cast<cudaStream_t>(stream);
+    return SVDSC_OK;
+}
+
+void svdsc_destroy(svdsc_handle *h) {
+    if (!h) return;
+    if (h->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm);
+    if (h->hctrl) cudaFreeHost(h->hctrl);
+    if (h->scratch) cudaFree(h->scratch);
+    delete h;
+}
+
+const char *svdsc_last_error(const svdsc_handle *h) { return h ? h->err.c_str() : "null handle"; }
+
+svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_ptr,
+                              const int32_t *col_idx, const double *values, int64_t row_offset, int64_t m_global,
+                              svdsc_matrix **Mout) {
+    if (!h || !Mout) return SVDSC_EINVAL;
+    *Mout = nullptr;
+    svdsc_matrix *M = new svdsc_matrix();
+    svdsc_status st = guarded(h, [&] {
+        einval(nrows < 0 || ncols < 1 || nnz < 0, "bad dimensions");
+        einval(!row_ptr || (nnz > 0 && (!col_idx || !values)), "NULL array");
+        einval(nnz >= (int64_t)1 << 31 || nrows >= (int64_t)1 << 31 || ncols >= (int64_t)1 << 31,
+               "nnz, nrows and ncols must be < 2^31 per rank");
+        einval(row_offset < 0 || m_global < row_offset + nrows, "row_offset/m_global inconsistent");
+        M->h = h;
+        M->kind = 0;
+        M->m_local = nrows;
+        M->n = ncols;
+        M->nnz = nnz;
+        M->row_offset = row_offset;
+        M->m_global = m_global;
+        cudaStream_t s = h->stream;
+        int *bad = nullptr;
+        ck(cudaMallocAsync((void **)&bad, sizeof(int), s), "alloc");
+        ck(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+        k_validate_csr<<<148 * 4, 256, 0, s>>>(nrows, ncols, nnz, row_ptr, col_idx, values, bad);
+        int hb = 0;
+        ck(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaFreeAsync(bad, s), "free");
+        ck(cudaStreamSynchronize(s), "sync");
+        einval(hb & 8, "row_ptr[0] != 0 or row_ptr[nrows] != nnz");
+        einval(hb & 1, "row_ptr is not monotone");
+        einval(hb & 2, "column index out of range");
+        einval(hb & 4, "non-finite value");
+        M->A.nrows = nrows;
+        M->A.ncols = ncols;
+        M->A.nnz = nnz;
+        M->A.row_ptr = row_ptr;
+        M->A.col = col_idx;
+        M->A.val = values;
+        csr_analyze(M->A, s);
+        csr_transpose(M->A, M->At, s);
+    });
+    if (st != SVDSC_OK) {
+        csr_free(M->A);
+        csr_free(M->At);
+        delete M;
+        return st;
+    }
+    *Mout = M;
+    return SVDSC_OK;
+}
+
+svdsc_status svdsc_matrix_dense(svdsc_handle *h, int64_t nrows, int64_t ncols, int64_t ld, const double *data,
+                                int64_t row_offset, int64_t m_global, svdsc_matrix **Mout) {
+    if (!h || !Mout) return SVDSC_EINVAL;
+    *Mout = nullptr;
+    svdsc_matrix *M = new svdsc_matrix();
+    svdsc_status st = guarded(h, [&] {
+        einval(nrows < 1 || ncols < 1 || ld < nrows, "bad dimensions");
+        einval(!data, "NULL data");
+        einval(row_offset < 0 || m_global < row_offset + nrows, "row_offset/m_global inconsistent");
+        M->h = h;
+        M->kind = 1;
+        M->m_local = nrows;
+        M->n = ncols;
+        M->row_offset = row_offset;
+        M->m_global = m_global;
+        M->nnz = nrows * ncols;
+        cudaStream_t s = h->stream;
+        int *bad = nullptr;
+        ck(cudaMallocAsync((void **)&bad, sizeof(int), s), "alloc");
+        ck(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+        k_validate_dense<<<148 * 4, 256, 0, s>>>(nrows, ncols, ld, data, bad);
+        int hb = 0;
+        ck(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaFreeAsync(bad, s), "free");
+        ck(cudaStreamSynchronize(s), "sync");
+        einval(hb & 4, "non-finite value");
+        M->D.nrows = nrows;
+        M->D.ncols = ncols;
+        M->D.ld = ld;
+        M->D.data = data;
+        matrix_common_dense_setup(M);
+    });
+    if (st != SVDSC_OK) {
+        if (M->dense_partial) cudaFree(M->dense_partial);
+        delete M;
+        return st;
+    }
+    *Mout = M;
+    return SVDSC_OK;
+}
+
+void svdsc_matrix_destroy(svdsc_matrix *M) {
+    if (!M) return;
+    csr_free(M->A);
+    csr_free(M->At);
+    if (M->dense_partial) cudaFree(M->dense_partial);
+    delete M;
+}
+
+svdsc_status svdsc_workspace_size(svdsc_matrix *M, const svdsc_opts *o, size_t *bytes) {
+    if (!M || !bytes) return SVDSC_EINVAL;
+    return guarded(M->h, [&] {
+        check_opts(M, o);
+        Ws w;
+        *bytes = carve(w, nullptr, M->m_local, M->n, resolve_t(o, M->m_global, M->n), o->k, M->h->nranks);
+    });
+}
+
+svdsc_status svdsc_solve(svdsc_matrix *M, const svdsc_opts *o, void *workspace, size_t ws_bytes, double *S, double *U,
+                         int64_t ldu, double *V, int64_t ldv, double *resid, svdsc_info *info) {
+    if (!M) return SVDSC_EINVAL;
+    return run_solver(M, o, workspace, ws_bytes, S, U, ldu, V, ldv, resid, info, false, 0, nullptr);
+}
+
+svdsc_status svdsc_op_lbp(svdsc_matrix *M, const svdsc_opts *o, int32_t t, const double *v0, double *U, int64_t ldu,
+                          double *V, int64_t ldv, double *T, svdsc_info *info) {
+    if (!M || !o) return SVDSC_EINVAL;
+    if (M->h->nranks != 1 || t < 1 || t + 1 > std::min(M->m_global, M->n) || t > 1023 || !U || !V || !T ||
+        ldu < M->m_local || ldv < M->n) {
+        M->h->err = "op_lbp: single rank, 1 <= t <= 1023, t+1 <= min(m,n), non-NULL U, V, T";
+        return SVDSC_EINVAL;
+    }
+    svdsc_opts oo = *o;
+    oo.v0 = v0;
+    oo.k = 1;
+    oo.tol = oo.tol > 0 ? oo.tol : 1e-10;
+    return run_solver(M, &oo, nullptr, 0, nullptr, U, ldu, V, ldv, nullptr, info, true, t, T);
+}
+
+svdsc_status svdsc_solve_host_csr(svdsc_handle *h, int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr,
+                                  const int32_t *col_idx, const double *values, const svdsc_opts *o, double *S,
+                                  double *U, double *V, double *resid, svdsc_info *info) {
+    if (!h || !o) return SVDSC_EINVAL;
+    std::vector<void *> bufs;
+    svdsc_matrix *M = nullptr;
+    svdsc_status ret = SVDSC_OK;
+    svdsc_status st = guarded(h, [&] {
+        einval(m < 1 || n < 1 || nnz < 0 || !row_ptr || !S || !U || !V, "bad arguments");
+        cudaStream_t s = h->stream;
+        auto dalloc = [&](size_t b) {
+            void *p = nullptr;
+            ck(cudaMallocAsync(&p, std::max<size_t>(b, 8), s), "cudaMallocAsync");
+            bufs.push_back(p);
+            return p;
+        };
+        int64_t *drp = (int64_t *)dalloc((m + 1) * 8);
+        int32_t *dci = (int32_t *)dalloc(nnz * 4);
+        double *dva = (double *)dalloc(nnz * 8);
+        ck(cudaMemcpyAsync(drp, row_ptr, (m + 1) * 8, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(dci, col_idx, nnz * 4, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(dva, values, nnz * 8, cudaMemcpyHostToDevice, s), "H2D");
+        svdsc_opts oo = *o;
+        if (o->v0) {
+            double *dv0 = (double *)dalloc(n * 8);
+            ck(cudaMemcpyAsync(dv0, o->v0, n * 8, cudaMemcpyHostToDevice, s), "H2D");
+            oo.v0 = dv0;
+        }
+        const int k = o->k;
+        double *dS = (double *)dalloc(k * 8), *dU = (double *)dalloc(m * k * 8), *dV = (double *)dalloc(n * k * 8),
+               *dr = (double *)dalloc(k * 8);
+        svdsc_status s1 = svdsc_matrix_csr(h, m, n, nnz, drp, dci, dva, 0, m, &M);
+        if (s1 != SVDSC_OK) throw SvdscError(s1, h->err);
+        ret = svdsc_solve(M, &oo, nullptr, 0, dS, dU, m, dV, n, dr, info);
+        if (ret < 0) throw SvdscError(ret, h->err);
+        ck(cudaMemcpyAsync(S, dS, k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(U, dU, m * k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(V, dV, n * k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (resid) ck(cudaMemcpyAsync(resid, dr, k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+    svdsc_matrix_destroy(M);
+    for (void *p : bufs) cudaFreeAsync(p, h->stream);
+    cudaStreamSynchronize(h->stream);
+    return st != SVDSC_OK ? st : ret;
+}
+
+svdsc_status svdsc_solve_host_dense(svdsc_handle *h, int64_t m, int64_t n, const double *data, const svdsc_opts *o,
+                                    double *S, double *U, double *V, double *resid, svdsc_info *info) {
+    if (!h || !o) return SVDSC_EINVAL;
+    std::vector<void *> bufs;
+    svdsc_matrix *M = nullptr;
+    svdsc_status ret = SVDSC_OK;
+    svdsc_status st = guarded(h, [&] {
+        einval(m < 1 || n < 1 || !data || !S || !U || !V, "bad arguments");
+        cudaStream_t s = h->stream;
+        auto dalloc = [&](size_t b) {
+            void *p = nullptr;
+            ck(cudaMallocAsync(&p, std::max<size_t>(b, 8), s), "cudaMallocAsync");
+            bufs.push_back(p);
+            return p;
+        };
+        double *dA = (double *)dalloc((size_t)m * n * 8);
+        ck(cudaMemcpyAsync(dA, data, (size_t)m * n * 8, cudaMemcpyHostToDevice, s), "H2D");
+        svdsc_opts oo = *o;
+        if (o->v0) {
+            double *dv0 = (double *)dalloc(n * 8);
+            ck(cudaMemcpyAsync(dv0, o->v0, n * 8, cudaMemcpyHostToDevice, s), "H2D");
+            oo.v0 = dv0;
+        }
+        const int k = o->k;
+        double *dS = (double *)dalloc(k * 8), *dU = (double *)dalloc(m * k * 8), *dV = (double *)dalloc(n * k * 8),
+               *dr = (double *)dalloc(k * 8);
+        svdsc_status s1 = svdsc_matrix_dense(h, m, n, m, dA, 0, m, &M);
+        if (s1 != SVDSC_OK) throw SvdscError(s1, h->err);
+        ret = svdsc_solve(M, &oo, nullptr, 0, dS, dU, m, dV, n, dr, info);
+        if (ret < 0) throw SvdscError(ret, h->err);
+        ck(cudaMemcpyAsync(S, dS, k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(U, dU, m * k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(V, dV, n * k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (resid) ck(cudaMemcpyAsync(resid, dr, k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+    svdsc_matrix_destroy(M);
+    for (void *p : bufs) cudaFreeAsync(p, h->stream);
+    cudaStreamSynchronize(h->stream);
+    return st != SVDSC_OK ? st : ret;
+}
+
+// ---- step-level ops -----------------------------------------------------------
+svdsc_status svdsc_op_matvec(svdsc_matrix *M, int trans, const double *x, double *y, const double *c_dev,
+                             const double *yprev) {
+    if (!M) return SVDSC_EINVAL;
+    return guarded(M->h, [&] {
+        einval(!x || !y || (c_dev && !yprev), "NULL vector");
+        cudaStream_t s = M->h->stream;
+        if (M->kind == 0) spmv_csr(trans ? M->At : M->A, x, y, c_dev, yprev, nullptr, s);
+        else if (trans) gemv_t(M->D, x, y, c_dev, yprev, nullptr, s);
+        else gemv_n(M->D, x, y, c_dev, yprev, nullptr, s);
+        ck(cudaGetLastError(), "matvec launch");
+    });
+}
+
+namespace {
+// op-level scratch: ctrl + partials + reductions + Jacobi work arrays
+struct OpScratch {
+    Ctrl *ctrl;
+    double *partial, *h1, *h2, *nrm, *W, *Vw;
+};
+OpScratch op_scratch(svdsc_handle *h, int maxcols, int p) {
+    Carver c{nullptr};
+    c.take<Ctrl>(1);
+    c.take<double>((size_t)(maxcols + 2) * kMaxBlocks);
+    c.take<double>(maxcols + 2);
+    c.take<double>(maxcols + 2);
+    c.take<double>(4);
+    c.take<double>((size_t)p * p);
+    c.take<double>((size_t)p * p);
+    const size_t need = c.off + 256;
+    if (need > h->scratch_bytes) {
+        if (h->scratch) cudaFree(h->scratch);
+        h->scratch = nullptr;
+        ck(cudaMalloc(&h->scratch, need), "cudaMalloc scratch");
+        h->scratch_bytes = need;
+    }
+    Carver d{reinterpret_cast<char *>(h->scratch)};
+    OpScratch o;
+    o.ctrl = d.take<Ctrl>(1);
+    o.partial = d.take<double>((size_t)(maxcols + 2) * kMaxBlocks);
+    o.h1 = d.take<double>(maxcols + 2);
+    o.h2 = d.take<double>(maxcols + 2);
+    o.nrm = d.take<double>(4);
+    o.W = d.take<double>((size_t)p * p);
+    o.Vw = d.take<double>((size_t)p * p);
+    ck(cudaMemsetAsync(o.ctrl, 0, sizeof(Ctrl), h->stream), "memset");
+    return o;
+}
+}  // namespace
+
+svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const double *Q, int64_t ldq, double *w,
+                           double *norm_dev) {
+    if (!h) return SVDSC_EINVAL;
+    return guarded(h, [&] {
+        einval(N < 1 || ncols < 0 || ncols > 1023 || (ncols > 0 && (!Q || ldq < N)) || !w, "bad arguments");
+        OpScratch sc = op_scratch(h, (int)ncols, 1);
+        RedBuf rb{sc.partial, kMaxBlocks, sc.h1, sc.h2, sc.nrm, sc.ctrl->cnt};
+        cudaStream_t s = h->stream;
+        if (ncols > 0) {
+            cgs_p1(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
+            cgs_p2(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
+            cgs_p3(N, (int)ncols, Q, ldq, w, sc.h2, rb, nullptr, h->nsm, s);
+        } else {
+            cgs_p3(N, 0, Q, ldq, w, nullptr, rb, nullptr, h->nsm, s);
+        }
+        if (norm_dev) {
+            // norm = sqrt(nrm2) via a 1-element normalize-free copy
+            double hv = 0.0;
+            ck(cudaMemcpyAsync(&hv, sc.nrm, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaStreamSynchronize(s), "sync");
+            hv = std::sqrt(hv);
+            ck(cudaMemcpyAsync(norm_dev, &hv, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+        }
+        ck(cudaStreamSynchronize(s), "sync");
+        ck(cudaGetLastError(), "cgs2");
+    });
+}
+
+svdsc_status svdsc_op_small_svd(svdsc_handle *h, int32_t p, const double *Tm, double *U, double *S, double *V,
+                                int32_t *sweeps) {
+    if (!h) return SVDSC_EINVAL;
+    svdsc_status ret = SVDSC_OK;
+    svdsc_status st = guarded(h, [&] {
+        einval(p < 1 || p > 1023 || !Tm || !U || !S || !V, "bad arguments");
+        OpScratch sc = op_scratch(h, 0, p);
+        cudaStream_t s = h->stream;
+        small_svd(p, Tm, p, sc.W, sc.Vw, U, S, V, p, sc.ctrl, nullptr, s);
+        Ctrl c;
+        ck(cudaMemcpyAsync(&c, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+        ck(cudaGetLastError(), "small_svd");
+        if (sweeps) *sweeps = c.svd_sweeps;
+        if (c.svd_status != 0) ret = SVDSC_ESVD_NOCONV;
+    });
+    return st != SVDSC_OK ? st : ret;
+}
+
+svdsc_status svdsc_op_recombine(svdsc_handle *h, int64_t N, int32_t t, int32_t k, const double *Q, int64_t ldq,
+                                const double *W, int32_t ldw, double *Qout, int64_t ldo) {
+    if (!h) return SVDSC_EINVAL;
+    return guarded(h, [&] {
+        einval(N < 1 || t < 1 || t > 1023 || k < 1 || k > t || !Q || !W || !Qout || ldq < N || ldw < t || ldo < N,
+               "bad arguments");
+        recombine(N, t, k, Q, ldq, W, ldw, Qout, ldo, h->nsm, h->stream);
+        ck(cudaGetLastError(), "recombine");
+    });
+}
+
+svdsc_status svdsc_comm_unique_id(unsigned char id[128]) {
+    if (!id) return SVDSC_EINVAL;
+    if (!nccl_load()) return SVDSC_ENCCL;
+    ncclUniqueId u;
+    if (g_nccl.GetUniqueId(&u) != 0) return SVDSC_ENCCL;
+    std::memcpy(id, u.internal, 128);
+    return SVDSC_OK;
+}
+
+svdsc_status svdsc_comm_init(svdsc_handle *h, int nranks, int rank, const unsigned char id[128]) {
+    if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks) return SVDSC_EINVAL;
+    if (nranks == 1) {
+        h->nranks = 1;
+        h->rank = 0;
+        return SVDSC_OK;
+    }
+    return guarded(h, [&] {
+        if (!nccl_load()) throw SvdscError(SVDSC_ENCCL, "libnccl.so.2 not loadable");
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, 128);
+        ckn(g_nccl.CommInitRank(&h->comm, nranks, u, rank), "ncclCommInitRank");
+        h->nranks = nranks;
+        h->rank = rank;
+    });
+}
+
+svdsc_status svdsc_partition_rows(int64_t m, const int64_t *row_ptr, int64_t basis_cols, int nparts, int64_t *bounds) {
+    if (m < 0 || !row_ptr || nparts < 1 || !bounds || basis_cols < 0) return SVDSC_EINVAL;
+    // cost(r) = 24 nnz_r + 24 basis_cols  (A read twice at 12 B/nnz; three U sweeps)
+    const long double total = 24.0L * (long double)row_ptr[m] + 24.0L * basis_cols * (long double)m;
+    bounds[0] = 0;
+    int64_t r = 0;
+    long double acc = 0.0L;
+    for (int q = 1; q < nparts; q++) {
+        const long double target = total * q / nparts;
+        while (r < m) {
+            const long double c = 24.0L * (row_ptr[r + 1] - row_ptr[r]) + 24.0L * basis_cols;
+            if (acc + c / 2 > target) break;
+            acc += c;
+            r++;
+        }
+        bounds[q] = r;
+    }
+    bounds[nparts] = m;
+    for (int q = 1; q <= nparts; q++)
+        if (bounds[q] < bounds[q - 1]) return SVDSC_EINVAL;
+    return SVDSC_OK;
+}
+
+}  // extern "C"

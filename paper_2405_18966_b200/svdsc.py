@@ -1,0 +1,333 @@
+"""Thin Python binding of libsvdsc.so (C ABI in include/svdsc.h).
+
+Argument marshalling only: torch CUDA tensors are passed as raw device
+pointers with the current CUDA stream; every step of the method runs in the
+library's sm_100a kernels.  There is no CPU fallback: if the shared library is
+missing this module raises at import of the first call.
+
+Layouts: dense matrices and bases are column-major, i.e. a torch tensor of
+shape (m, n) with stride (1, ld) (``colmajor(...)`` makes one).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libsvdsc.so")
+_lib = None
+
+OK, NOT_CONVERGED = 0, 1
+STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL",
+          -5: "ESVD_NOCONV", -6: "ERANKDEF"}
+
+
+class SvdscError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"svdsc {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("tol", ctypes.c_double), ("t", ctypes.c_int32),
+                ("maxit", ctypes.c_int32), ("seed", ctypes.c_uint64), ("v0", ctypes.c_void_p),
+                ("fixed_passes", ctypes.c_int32), ("reorth", ctypes.c_int32)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("passes", ctypes.c_int32), ("restarts", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("t_used", ctypes.c_int32),
+                ("steps", ctypes.c_int64), ("matvecs", ctypes.c_int64),
+                ("breakdowns", ctypes.c_int64), ("max_resid", ctypes.c_double),
+                ("seconds_total", ctypes.c_double), ("launches", ctypes.c_int64),
+                ("bytes_model", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_error", "svdsc_version",
+           "svdsc_matrix_csr", "svdsc_matrix_dense", "svdsc_matrix_destroy", "svdsc_workspace_size",
+           "svdsc_solve", "svdsc_solve_host_csr", "svdsc_solve_host_dense", "svdsc_op_matvec",
+           "svdsc_op_cgs2", "svdsc_op_small_svd", "svdsc_op_recombine", "svdsc_op_lbp",
+           "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows"]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise ImportError(f"{_SO} is missing: build it with `python -m paper_2405_18966_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(_SO)
+        P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        L.svdsc_create.argtypes = [ctypes.POINTER(P), P]
+        L.svdsc_set_stream.argtypes = [P, P]
+        L.svdsc_destroy.argtypes = [P]
+        L.svdsc_destroy.restype = None
+        L.svdsc_last_error.argtypes = [P]
+        L.svdsc_last_error.restype = ctypes.c_char_p
+        L.svdsc_version.restype = ctypes.c_char_p
+        L.svdsc_matrix_csr.argtypes = [P, I64, I64, I64, P, P, P, I64, I64, ctypes.POINTER(P)]
+        L.svdsc_matrix_dense.argtypes = [P, I64, I64, I64, P, I64, I64, ctypes.POINTER(P)]
+        L.svdsc_matrix_destroy.argtypes = [P]
+        L.svdsc_matrix_destroy.restype = None
+        L.svdsc_workspace_size.argtypes = [P, ctypes.POINTER(Opts), ctypes.POINTER(ctypes.c_size_t)]
+        L.svdsc_solve.argtypes = [P, ctypes.POINTER(Opts), P, ctypes.c_size_t, P, P, I64, P, I64, P,
+                                  ctypes.POINTER(Info)]
+        L.svdsc_solve_host_csr.argtypes = [P, I64, I64, I64, P, P, P, ctypes.POINTER(Opts), P, P, P, P,
+                                           ctypes.POINTER(Info)]
+        L.svdsc_solve_host_dense.argtypes = [P, I64, I64, P, ctypes.POINTER(Opts), P, P, P, P,
+                                             ctypes.POINTER(Info)]
+        L.svdsc_op_matvec.argtypes = [P, ctypes.c_int, P, P, P, P]
+        L.svdsc_op_cgs2.argtypes = [P, I64, I64, P, I64, P, P]
+        L.svdsc_op_small_svd.argtypes = [P, I32, P, P, P, P, ctypes.POINTER(I32)]
+        L.svdsc_op_recombine.argtypes = [P, I64, I32, I32, P, I64, P, I32, P, I64]
+        L.svdsc_op_lbp.argtypes = [P, ctypes.POINTER(Opts), I32, P, P, I64, P, I64, P,
+                                   ctypes.POINTER(Info)]
+        L.svdsc_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.svdsc_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+        L.svdsc_partition_rows.argtypes = [I64, P, I64, ctypes.c_int, P]
+        for name in EXPORTS:
+            f = getattr(L, name)
+            if f.restype is ctypes.c_int:  # default
+                f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def colmajor(rows, cols, device="cuda", dtype=torch.float64):
+    """Empty (rows, cols) tensor with column-major strides (1, rows)."""
+    return torch.empty((cols, rows), device=device, dtype=dtype).t()
+
+
+def _ld(t):
+    assert t.dim() == 2 and t.stride(0) == 1, "expected a column-major 2-D tensor (stride(0) == 1)"
+    return max(t.stride(1), t.shape[0])
+
+
+class Handle:
+    """svdsc_create on the current device and CUDA stream."""
+
+    def __init__(self, stream=None):
+        self.ptr = ctypes.c_void_p()
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        self._check(lib().svdsc_create(ctypes.byref(self.ptr), ctypes.c_void_p(s)))
+        self.nranks, self.rank = 1, 0
+
+    def _check(self, st):
+        if st < 0:
+            msg = lib().svdsc_last_error(self.ptr).decode() if self.ptr else ""
+            raise SvdscError(st, msg)
+        return st
+
+    def set_stream(self, stream):
+        self._check(lib().svdsc_set_stream(self.ptr, ctypes.c_void_p(stream.cuda_stream)))
+
+    def comm_init(self, nranks, rank, uid: bytes):
+        self._check(lib().svdsc_comm_init(self.ptr, nranks, rank, uid))
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.ptr:
+            lib().svdsc_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = lib().svdsc_comm_unique_id(buf)
+    if st < 0:
+        raise SvdscError(st, "ncclGetUniqueId")
+    return buf.raw
+
+
+def partition_rows(row_ptr: np.ndarray, basis_cols: int, nparts: int) -> np.ndarray:
+    """Host partitioner (svdsc_partition_rows): contiguous balanced row blocks."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    b = np.zeros(nparts + 1, dtype=np.int64)
+    st = lib().svdsc_partition_rows(rp.size - 1, rp.ctypes.data, basis_cols, nparts, b.ctypes.data)
+    if st < 0:
+        raise SvdscError(st, "partition_rows")
+    return b
+
+
+class Matrix:
+    """svdsc_matrix over caller-owned device arrays (kept alive here)."""
+
+    def __init__(self, h: Handle, kind, m, n, keep, ptr, row_offset=0, m_global=None):
+        self.h, self.kind, self.m, self.n, self._keep, self.ptr = h, kind, m, n, keep, ptr
+        self.row_offset = row_offset
+        self.m_global = m if m_global is None else m_global
+
+    @classmethod
+    def csr(cls, h: Handle, row_ptr, col_idx, values, ncols, row_offset=0, m_global=None):
+        assert row_ptr.dtype == torch.int64 and col_idx.dtype == torch.int32 and values.dtype == torch.float64
+        assert row_ptr.is_cuda and col_idx.is_cuda and values.is_cuda
+        row_ptr, col_idx, values = row_ptr.contiguous(), col_idx.contiguous(), values.contiguous()
+        m = row_ptr.numel() - 1
+        mg = m if m_global is None else m_global
+        p = ctypes.c_void_p()
+        h._check(lib().svdsc_matrix_csr(h.ptr, m, ncols, values.numel(), _ptr(row_ptr), _ptr(col_idx),
+                                        _ptr(values), row_offset, mg, ctypes.byref(p)))
+        return cls(h, "csr", m, ncols, (row_ptr, col_idx, values), p, row_offset, mg)
+
+    @classmethod
+    def dense(cls, h: Handle, A, row_offset=0, m_global=None):
+        assert A.dtype == torch.float64 and A.is_cuda
+        m, n = A.shape
+        mg = m if m_global is None else m_global
+        p = ctypes.c_void_p()
+        h._check(lib().svdsc_matrix_dense(h.ptr, m, n, _ld(A), _ptr(A), row_offset, mg, ctypes.byref(p)))
+        return cls(h, "dense", m, n, (A,), p, row_offset, mg)
+
+    @classmethod
+    def from_host(cls, h: Handle, A, device="cuda", row_offset=0, m_global=None):
+        """From a workloads.Matrix (host numpy) -> device copy + analysis."""
+        if A.kind == "csr":
+            rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, np.int64)).to(device)
+            ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, np.int32)).to(device)
+            va = torch.from_numpy(np.ascontiguousarray(A.values, np.float64)).to(device)
+            return cls.csr(h, rp, ci, va, A.n, row_offset, m_global)
+        D = torch.from_numpy(np.asfortranarray(A.dense, np.float64).T.copy()).to(device).t()
+        return cls.dense(h, D, row_offset, m_global)
+
+    def close(self):
+        if self.ptr:
+            lib().svdsc_matrix_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _opts(k, tol, t, maxit, seed, v0, fixed_passes, reorth):
+    return Opts(k=k, tol=tol, t=t or 0, maxit=maxit, seed=seed,
+                v0=None if v0 is None else v0.data_ptr(), fixed_passes=fixed_passes, reorth=reorth)
+
+
+@dataclass
+class Result:
+    S: torch.Tensor
+    U: torch.Tensor
+    V: torch.Tensor
+    resid: torch.Tensor
+    status: int
+    info: dict
+
+
+def svds_c(M: Matrix, k, tol=1e-10, maxit=100, t=None, seed=0, v0=None, fixed_passes=0, reorth=2,
+           workspace=None) -> Result:
+    """Alg. 2 of the paper: k largest singular triplets of M (svdsc_solve)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if v0 is not None:
+        v0 = v0.to(device=dev, dtype=torch.float64).contiguous()
+    o = _opts(k, tol, t, maxit, seed, v0, fixed_passes, reorth)
+    S = torch.empty(k, device=dev, dtype=torch.float64)
+    U = colmajor(M.m, k, dev)
+    V = colmajor(M.n, k, dev)
+    R = torch.empty(k, device=dev, dtype=torch.float64)
+    info = Info()
+    ws, wsb = (None, 0) if workspace is None else (workspace, workspace.numel() * workspace.element_size())
+    st = M.h._check(lib().svdsc_solve(M.ptr, ctypes.byref(o), _ptr(ws), wsb, _ptr(S), _ptr(U), max(M.m, 1),
+                                      _ptr(V), M.n, _ptr(R), ctypes.byref(info)))
+    return Result(S, U, V, R, st, info.as_dict())
+
+
+def workspace_size(M: Matrix, k, t=None, tol=1e-10, maxit=100) -> int:
+    o = _opts(k, tol, t, maxit, 0, None, 0, 2)
+    n = ctypes.c_size_t()
+    M.h._check(lib().svdsc_workspace_size(M.ptr, ctypes.byref(o), ctypes.byref(n)))
+    return n.value
+
+
+def svds_c_host(h: Handle, A, k, tol=1e-10, maxit=100, t=None, seed=0, v0=None, fixed_passes=0,
+                reorth=2):
+    """End-to-end with HOST buffers (svdsc_solve_host_*): numpy in, numpy out."""
+    m, n = A.m, A.n
+    S, U, V, R = (np.zeros(k), np.zeros((k, m)), np.zeros((k, n)), np.zeros(k))
+    v0h = None if v0 is None else np.ascontiguousarray(v0, np.float64)
+    o = Opts(k=k, tol=tol, t=t or 0, maxit=maxit, seed=seed,
+             v0=None if v0h is None else v0h.ctypes.data, fixed_passes=fixed_passes, reorth=reorth)
+    info = Info()
+    if A.kind == "csr":
+        rp = np.ascontiguousarray(A.row_ptr, np.int64)
+        ci = np.ascontiguousarray(A.col_idx, np.int32)
+        va = np.ascontiguousarray(A.values, np.float64)
+        st = lib().svdsc_solve_host_csr(h.ptr, m, n, va.size, rp.ctypes.data, ci.ctypes.data,
+                                        va.ctypes.data, ctypes.byref(o), S.ctypes.data, U.ctypes.data,
+                                        V.ctypes.data, R.ctypes.data, ctypes.byref(info))
+    else:
+        D = np.asfortranarray(A.dense, np.float64)
+        st = lib().svdsc_solve_host_dense(h.ptr, m, n, D.ctypes.data, ctypes.byref(o), S.ctypes.data,
+                                          U.ctypes.data, V.ctypes.data, R.ctypes.data, ctypes.byref(info))
+    h._check(st)
+    return S, U.T, V.T, R, st, info.as_dict()
+
+
+# ---- step-level ops ----------------------------------------
+def matvec(M: Matrix, x, trans=False, c=None, yprev=None):
+    """a1/a5: y = op(A) x - c * yprev (c: 1-element device tensor)."""
+    dev = x.device
+    y = torch.empty(M.n if trans else M.m, device=dev, dtype=torch.float64)
+    M.h._check(lib().svdsc_op_matvec(M.ptr, int(trans), _ptr(x), _ptr(y), _ptr(c), _ptr(yprev)))
+    return y
+
+
+def cgs2(h: Handle, Q, w):
+    """a2-a4/a6: w <- (I - QQ^T)^2 w in place on a copy; returns (w, ||w||)."""
+    w = w.clone()
+    N = w.numel()
+    ncols = 0 if Q is None else Q.shape[1]
+    nrm = torch.empty(1, device=w.device, dtype=torch.float64)
+    ldq = _ld(Q) if ncols else N
+    h._check(lib().svdsc_op_cgs2(h.ptr, N, ncols, _ptr(Q) if ncols else None, ldq, _ptr(w), _ptr(nrm)))
+    return w, nrm
+
+
+def small_svd(h: Handle, T):
+    """a7: device one-sided Jacobi SVD of a p x p column-major matrix."""
+    p = T.shape[0]
+    U, V = colmajor(p, p, T.device), colmajor(p, p, T.device)
+    S = torch.empty(p, device=T.device, dtype=torch.float64)
+    sw = ctypes.c_int32()
+    h._check(lib().svdsc_op_small_svd(h.ptr, p, _ptr(T), _ptr(U), _ptr(S), _ptr(V), ctypes.byref(sw)))
+    return U, S, V, sw.value
+
+
+def recombine(h: Handle, Q, W, k, out=None):
+    """a8/a9: out(:, :k) = Q(:, :t) W(:, :k); out may be Q (in place)."""
+    N, t = Q.shape[0], W.shape[0]
+    if out is None:
+        out = colmajor(N, k, Q.device)
+    h._check(lib().svdsc_op_recombine(h.ptr, N, t, k, _ptr(Q), _ld(Q), _ptr(W), _ld(W), _ptr(out),
+                                      _ld(out)))
+    return out
+
+
+def lbp(M: Matrix, t, v0, seed=0, reorth=2):
+    """One first pass LBP(A, t+1): U (m x t+1), V (n x t+1), T (t+1 x t+1), info."""
+    dev = v0.device
+    U, V, T = colmajor(M.m, t + 1, dev), colmajor(M.n, t + 1, dev), colmajor(t + 1, t + 1, dev)
+    o = _opts(1, 1e-10, 0, 1, seed, None, 0, reorth)
+    info = Info()
+    M.h._check(lib().svdsc_op_lbp(M.ptr, ctypes.byref(o), t, _ptr(v0.contiguous()), _ptr(U), _ld(U),
+                                  _ptr(V), _ld(V), _ptr(T), ctypes.byref(info)))
+    return U, V, T, info.as_dict()

@@ -1,0 +1,281 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, row by row
+of SURVEY.md 8(a), on seeded synthetic inputs.  -m gpu (B200 via gpurun).
+
+Tolerances:
+  * products a1/a5: per element |y - y_or| <= 2 gamma_{L+2} sum_j |a_rj x_j|
+    (both sides are valid reduction orders; gamma_n = n u / (1 - n u)).
+  * CGS2 / norms: |w - w_or| <= 1e-12 ||w_in||, |nrm - nrm_or| <= 1e-12 ||w_in||.
+  * small SVD: |s - s_or| <= 1e-13 s_1; singular vectors (distinct s, sign rule)
+    within 1e-9.
+  * end to end (BASELINE north_star): |s_i - s_i^or| <= 1e-10 s_1, principal
+    angles (from sines) <= 1e-8, same pass count (reading Q18).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as W
+from helpers import certificates, gamma, orth_error, sin_max_angle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2405_18966_b200 import build, svdsc
+    build.build()
+    return svdsc
+
+
+@pytest.fixture(scope="module")
+def H(S):
+    return S.Handle()
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def product_budget(A, x, trans):
+    D = np.abs(A.to_dense()) if (A.kind == "dense" or A.m * A.n < 4e7) else None
+    if D is not None:
+        absprod = (D.T if trans else D) @ np.abs(x)
+        lens = (D.T if trans else D).astype(bool).sum(1) if A.kind == "csr" else np.full(absprod.size, A.m if trans else A.n)
+    else:
+        Aa = W.Matrix("csr", A.m, A.n, row_ptr=A.row_ptr, col_idx=A.col_idx, values=np.abs(A.values))
+        absprod = O.spmv_t(Aa, np.abs(x)) if trans else O.spmv(Aa, np.abs(x))
+        if trans:
+            lens = np.bincount(A.col_idx, minlength=A.n)
+        else:
+            lens = np.diff(A.row_ptr)
+    return 2 * gamma(lens + 2) * absprod
+
+
+def check_products(S, H, A, seed=0):
+    M = S.Matrix.from_host(H, A)
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(A.n)
+    u = rng.standard_normal(A.m)
+    y = S.matvec(M, dev(x)).cpu().numpy()
+    yt = S.matvec(M, dev(u), trans=True).cpu().numpy()
+    y_or, yt_or = O.spmv(A, x), O.spmv_t(A, u)
+    assert np.all(np.abs(y - y_or) <= product_budget(A, x, False) + 1e-300)
+    assert np.all(np.abs(yt - yt_or) <= product_budget(A, u, True) + 1e-300)
+    # epilogue: y = A x - c * yprev
+    c = torch.tensor([0.75], dtype=torch.float64, device="cuda")
+    yp = rng.standard_normal(A.m)
+    y2 = S.matvec(M, dev(x), c=c, yprev=dev(yp)).cpu().numpy()
+    assert np.all(np.abs(y2 - (y_or - 0.75 * yp)) <= product_budget(A, x, False) + 4 * gamma(2) * np.abs(yp) + 1e-300)
+    M.close()
+
+
+# ---------------------------------------------------------------- a1 / a5
+@pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000)])
+def test_products_configs(S, H, cid, scale):
+    wl = W.config(cid, scale=scale)
+    check_products(S, H, wl.A)
+
+
+def test_products_edge_cases(S, H):
+    rng = np.random.default_rng(7)
+    m, n = 3001, 777
+    rows = []
+    # empty rows, single-entry rows, a 70k-long row (chunked path), a 3k row (CTA path)
+    lens = rng.integers(0, 40, m)
+    lens[::17] = 0
+    lens[5] = n  # dense row
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int32)
+    val = rng.standard_normal(rp[-1])
+    A = W.Matrix("csr", m, n, row_ptr=rp, col_idx=col, values=val)
+    check_products(S, H, A)
+    # a very long row (> 65536 nnz) with duplicates (duplicates act as their sum)
+    m2, n2 = 40, 50000
+    lens2 = np.full(m2, 3)
+    lens2[7] = 150000
+    rp2 = np.zeros(m2 + 1, np.int64)
+    rp2[1:] = np.cumsum(lens2)
+    col2 = rng.integers(0, n2, rp2[-1]).astype(np.int32)
+    A2 = W.Matrix("csr", m2, n2, row_ptr=rp2, col_idx=col2, values=rng.standard_normal(rp2[-1]))
+    M = S.Matrix.from_host(H, A2)
+    x = rng.standard_normal(n2)
+    u = rng.standard_normal(m2)
+    y = S.matvec(M, dev(x)).cpu().numpy()
+    yt = S.matvec(M, dev(u), trans=True).cpu().numpy()
+    assert np.all(np.abs(y - O.spmv(A2, x)) <= product_budget(A2, x, False) + 1e-300)
+    # the transposed product sums duplicates; bound by the same per-column budget
+    Aa = W.Matrix("csr", m2, n2, row_ptr=rp2, col_idx=col2, values=np.abs(A2.values))
+    bud = 2 * gamma(np.bincount(col2, minlength=n2) + 2) * O.spmv_t(Aa, np.abs(u))
+    assert np.all(np.abs(yt - O.spmv_t(A2, u)) <= bud + 1e-300)
+
+
+@pytest.mark.parametrize("m,n", [(5000, 1250), (1001, 333), (20000, 5000)])
+def test_products_dense(S, H, m, n):
+    rng = np.random.default_rng(m)
+    A = W.dense_matrix(rng.standard_normal((m, n)))
+    check_products(S, H, A, seed=n)
+
+
+# ---------------------------------------------------------------- a2-a4 / a6
+@pytest.mark.parametrize("N,c", [(10007, 37), (200000, 300), (3, 1), (50000, 0), (4096, 600)])
+def test_cgs2(S, H, N, c):
+    rng = np.random.default_rng(N + c)
+    Q = np.linalg.qr(rng.standard_normal((N, max(c, 1))))[0][:, :c]
+    w = rng.standard_normal(N)
+    if c:
+        w += Q @ rng.standard_normal(c) * 10  # mostly inside span(Q)
+    Qd = S.colmajor(N, max(c, 1))
+    if c:
+        Qd.copy_(dev(np.asfortranarray(Q)))
+    wg, nrm = S.cgs2(H, Qd if c else None, dev(w))
+    w_or = O.cgs2(Q, w) if c else w.copy()
+    scale = np.linalg.norm(w)
+    assert np.abs(wg.cpu().numpy() - w_or).max() <= 1e-12 * scale
+    assert abs(nrm.item() - O.norm2(w_or)) <= 1e-12 * scale
+
+
+# ---------------------------------------------------------------- a7
+def _bidiag(rng, p):
+    T = np.diag(rng.uniform(0.5, 2, p)) + np.diag(rng.uniform(0.1, 1, p - 1), 1)
+    return T
+
+
+def _arrow(rng, p, k):
+    T = np.zeros((p, p))
+    T[np.arange(k), np.arange(k)] = np.sort(rng.uniform(1, 3, k))[::-1]
+    T[:k, k] = rng.uniform(-0.1, 0.1, k)
+    T[k:, k:] = _bidiag(rng, p - k)
+    return T
+
+
+@pytest.mark.parametrize("p,kind", [(30, "bidiag"), (150, "arrow"), (300, "arrow"), (31, "bidiag"), (1, "bidiag")])
+def test_small_svd(S, H, p, kind):
+    rng = np.random.default_rng(p)
+    T = _bidiag(rng, p) if kind == "bidiag" or p < 3 else _arrow(rng, p, p // 3)
+    Td = S.colmajor(p, p)
+    Td.copy_(dev(np.asfortranarray(T)))
+    U, s, V, sw = S.small_svd(H, Td)
+    Uo, so, Vo, _ = O.jacobi_svd(T)
+    s = s.cpu().numpy()
+    assert np.abs(s - so).max() <= 1e-13 * so[0]
+    gaps = np.minimum(np.abs(np.diff(so, prepend=np.inf)), np.abs(np.diff(so, append=-np.inf)))
+    ok = gaps > 1e-6 * so[0]
+    assert np.abs(U.cpu().numpy()[:, ok] - Uo[:, ok]).max() <= 1e-9
+    assert np.abs(V.cpu().numpy()[:, ok] - Vo[:, ok]).max() <= 1e-9
+    assert orth_error(U.cpu().numpy()) <= 1e-13 * p and orth_error(V.cpu().numpy()) <= 1e-13 * p
+
+
+# ---------------------------------------------------------------- a8 / a9
+@pytest.mark.parametrize("N,t,k", [(10007, 30, 10), (200000, 300, 100), (77, 600, 200)])
+def test_recombine(S, H, N, t, k):
+    rng = np.random.default_rng(t)
+    Q = rng.standard_normal((N, t + 1))
+    Wm = rng.standard_normal((t, t))
+    Qd = S.colmajor(N, t + 1)
+    Qd.copy_(dev(np.asfortranarray(Q)))
+    Wd = S.colmajor(t, t)
+    Wd.copy_(dev(np.asfortranarray(Wm)))
+    out = S.recombine(H, Qd, Wd, k).cpu().numpy()
+    ref = Q[:, :t] @ Wm[:, :k]
+    bud = 2 * gamma(t + 2) * (np.abs(Q[:, :t]) @ np.abs(Wm[:, :k]))
+    assert np.all(np.abs(out - ref) <= bud)
+    # in place
+    S.recombine(H, Qd, Wd, k, out=Qd)
+    got = Qd.cpu().numpy()
+    assert np.all(np.abs(got[:, :k] - ref) <= bud)
+    assert np.array_equal(got[:, k:], Q[:, k:])
+
+
+# ---------------------------------------------------------------- one pass
+@pytest.mark.parametrize("cid,scale,t", [(1, 1, 30), (3, 20, 60), (2, 4, 40), (4, 100, 40)])
+def test_lbp_first_pass(S, H, cid, scale, t):
+    wl = W.config(cid, scale=scale)
+    M = S.Matrix.from_host(H, wl.A)
+    U, V, T, info = S.lbp(M, t, dev(wl.v0))
+    Uo, Vo, To, _ = O.lbp(wl.A, t, wl.v0)
+    T = T.cpu().numpy()
+    al, be = np.diag(T)[:t], np.diag(T, 1)[:t]
+    alo, beo = np.diag(To)[:t], np.diag(To, 1)[:t]
+    scale_ = max(alo.max(), beo.max())
+    assert np.abs(al - alo).max() <= 1e-10 * scale_
+    assert np.abs(be - beo).max() <= 1e-10 * scale_
+    assert orth_error(U.cpu().numpy()[:, :t]) <= 1e-12
+    assert orth_error(V.cpu().numpy()) <= 1e-12
+    assert sin_max_angle(U.cpu().numpy()[:, :t], Uo[:, :t]) <= 1e-8
+    assert sin_max_angle(V.cpu().numpy(), Vo) <= 1e-8
+    assert info["matvecs"] == 2 * t  # u_{t+1} is not formed on the GPU (reading Q2)
+    M.close()
+
+
+# ---------------------------------------------------------------- end to end
+def _e2e(S, H, wl, fixed=True, **kw):
+    r_or = O.svds(wl.A, wl.k, wl.v0, tol=wl.tol, t=wl.t, maxit=wl.maxit, **kw)
+    M = S.Matrix.from_host(H, wl.A)
+    r = S.svds_c(M, wl.k, tol=wl.tol, t=wl.t, maxit=wl.maxit, v0=dev(wl.v0),
+                 fixed_passes=r_or.passes if fixed else 0, **kw)
+    s = r.S.cpu().numpy()
+    assert np.abs(s - r_or.S).max() <= 1e-10 * r_or.S[0]
+    U, V = r.U.cpu().numpy(), r.V.cpu().numpy()
+    assert r.info["passes"] == r_or.passes
+    M.close()
+    return r, r_or, U, V, s
+
+
+@pytest.mark.parametrize("cid,scale", [(1, 1), (2, 4), (3, 20), (4, 100)])
+def test_svds_parity(S, H, cid, scale):
+    wl = W.config(cid, scale=scale)
+    r, r_or, U, V, s = _e2e(S, H, wl)
+    k = wl.k
+    assert sin_max_angle(U, r_or.U) <= 1e-8
+    assert sin_max_angle(V, r_or.V) <= 1e-8
+    assert bool(r.info["converged"]) == r_or.converged
+    assert orth_error(U) <= 1e-10 and orth_error(V) <= 1e-10
+    r1, r2 = certificates(wl.A, s, U, V)
+    assert np.all(r1 <= 1e-10 * s[0])
+    assert np.all(np.abs(r2 - r.resid.cpu().numpy()) <= 1e-8 * max(1.0, r2.max()))
+    # free-running GPU stops on the same pass as the oracle here
+    M = S.Matrix.from_host(H, wl.A)
+    rf = S.svds_c(M, k, tol=wl.tol, t=wl.t, maxit=wl.maxit, v0=dev(wl.v0))
+    assert rf.info["passes"] == r_or.passes
+
+
+def test_svds_forced_restarts_and_breakdown(S, H):
+    # t = k + 3 forces restarts (Eqs. 5-7)
+    A = W.dense_with_spectrum(500, 400, W.spectrum("decay1", 400), seed=5)
+    wl = W.Workload("decay1", A, W.start_vector(400, 5), 10, 13, 1e-10, 500)
+    r, r_or, U, V, s = _e2e(S, H, wl)
+    assert r.info["restarts"] >= 1 and r.info["steps"] == r_or.steps
+    # exactly rank-3 matrix, k = 5: breakdown replacements (reading Q7)
+    rng = np.random.default_rng(3)
+    D = rng.standard_normal((60, 3)) @ rng.standard_normal((3, 40))
+    wl2 = W.Workload("rank3", W.dense_matrix(D), rng.standard_normal(40), 5, 15, 1e-10, 20)
+    r_or = O.svds(wl2.A, 5, wl2.v0, t=15, maxit=20)
+    M = S.Matrix.from_host(H, wl2.A)
+    r = S.svds_c(M, 5, t=15, maxit=20, v0=dev(wl2.v0), fixed_passes=r_or.passes)
+    assert r_or.breakdowns >= 1 and r.info["breakdowns"] == r_or.breakdowns
+    assert np.abs(r.S.cpu().numpy()[:3] - r_or.S[:3]).max() <= 1e-10 * r_or.S[0]
+
+
+def test_svds_contract_errors(S, H):
+    wl = W.config(1, scale=10)
+    M = S.Matrix.from_host(H, wl.A)
+    for kw in (dict(k=0), dict(k=5, tol=0.0), dict(k=298), dict(k=5, reorth=1)):
+        with pytest.raises(S.SvdscError) as e:
+            S.svds_c(M, **kw)
+        assert e.value.status == -1
+    r = S.svds_c(M, 5, maxit=1, v0=dev(wl.v0), tol=1e-14)
+    assert r.status == 1 and r.info["passes"] == 1  # NOT_CONVERGED, outputs filled
+    assert np.all(np.isfinite(r.S.cpu().numpy()))
+
+
+def test_deterministic_and_host_path(S, H):
+    wl = W.config(1, scale=2)
+    M = S.Matrix.from_host(H, wl.A)
+    a = S.svds_c(M, wl.k, t=wl.t, v0=dev(wl.v0))
+    b = S.svds_c(M, wl.k, t=wl.t, v0=dev(wl.v0))
+    assert torch.equal(a.S, b.S) and torch.equal(a.U, b.U) and torch.equal(a.V, b.V)
+    Sh, Uh, Vh, Rh, st, info = S.svds_c_host(H, wl.A, wl.k, t=wl.t, v0=wl.v0)
+    assert np.array_equal(Sh, a.S.cpu().numpy()) and np.array_equal(Uh, a.U.cpu().numpy())
+    assert np.array_equal(Vh, a.V.cpu().numpy())
