@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the svds-C hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C] [--impl ours|reference]
+
+A "step" is one full svds-C solve (Alg. 2: every SURVEY.md 8(a) row -- the
+Lanczos steps, the small SVD, the restarts and the final assembly) on the
+workload's synthetic input, which is resident in HBM before timing starts.
+  value        Lanczos steps per second of the whole job (steps of all timed
+               solves / max-over-ranks device time)
+  ms_per_step  time-to-k-triplets of one solve (ms)
+  roofline     dominant kernel family (the A / A^T products for dense and
+               sparse inputs), algorithmic bytes per launch
+               over its CUDA-event-timed average duration inside the timed
+               region, against MEASURED_PEAKS.json hbm_gbs
+  e2e          same metric through the C-ABI host-buffer entry point
+               (svdsc_solve_host_*), H2D of A and v0 and D2H of S, U, V, resid
+               inside the timed region
+  cpu_baseline the CPU oracle (oracle/oracle.c, 1 thread) on a bounded sample
+The default workload is BASELINE.json configs[1] (dense 20,000 x 5,000,
+sigma_i = exp(-i/40), k = 50).  A is 800 MB, larger than the 126 MB L2, so no
+L2 flush is needed between timed solves.
+
+--impl reference times the CPU oracle as it stands (the reference arm of this
+tier): each step is a bounded sample (the first Lanczos steps of LBP on the
+same workload), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Lanczos steps/s & time-to-k triplets; HBM GB/s vs 8 TB/s peak, 1/2/4/8 GPUs"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc, self.th = index, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.th:
+            self.th.join(timeout=5)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def cpu_sample(wl, seconds_target=15.0):
+    """Time the oracle as it stands (1 thread) on the first s Lanczos steps of
+    this workload: returns (steps/s, s, seconds)."""
+    import oracle as O
+    # calibrate s with a 2-step probe, then run a bounded sample
+    t0 = time.perf_counter()
+    O.lbp(wl.A, 2, wl.v0)
+    probe = time.perf_counter() - t0
+    per = max(probe / 2.5, 1e-4)
+    s = int(max(2, min(wl.t, seconds_target / per)))
+    t0 = time.perf_counter()
+    O.lbp(wl.A, s, wl.v0)
+    dt = time.perf_counter() - t0
+    return s / dt, s, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", type=int, default=2, help="BASELINE.json config id (1-based)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import numpy as np
+    import workloads as W
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        wl = W.config(args.workload)
+        # reference arm = the CPU oracle as it stands, bounded sample per step
+        import oracle as O
+        O.lib()
+        _, s, _ = cpu_sample(wl, seconds_target=6.0)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.lbp(wl.A, s, wl.v0)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+        val = s * len(times) / sum(times)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": wl.name, "m": wl.A.m, "n": wl.A.n, "nnz": wl.A.nnz, "k": wl.k, "t": wl.t,
+                       "tol": wl.tol, "l2": "inputs larger than L2 (A is %d MB)" % (wl.A.bytes_one_pass() >> 20)},
+            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {s} Lanczos steps (Alg. 1 + CGS2) of {wl.name}, plain C, 1 thread"},
+            "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_18966_b200 import build as B
+    from paper_2405_18966_b200 import svdsc as S
+
+    B.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- workload: rank-local rows of A (row partition) ----
+    wl_full = W.config(args.workload)
+    A = wl_full.A
+    if world > 1:
+        if A.kind == "csr":
+            bounds = S.partition_rows(A.row_ptr, (wl_full.k + wl_full.t) // 2, world)
+        else:
+            bounds = np.linspace(0, A.m, world + 1).astype(np.int64)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        if A.kind == "csr":
+            rp = A.row_ptr[r0:r1 + 1] - A.row_ptr[r0]
+            Al = W.Matrix("csr", r1 - r0, A.n, row_ptr=rp, col_idx=A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]],
+                          values=A.values[A.row_ptr[r0]:A.row_ptr[r1]])
+        else:
+            Al = W.dense_matrix(A.dense[r0:r1])
+    else:
+        r0, r1, Al = 0, A.m, A
+
+    stream = torch.cuda.current_stream()
+    H = S.Handle(stream)
+    if world > 1:
+        uid = [S.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        H.comm_init(world, rank, uid[0])
+    M = S.Matrix.from_host(H, Al, device=dev, row_offset=r0, m_global=A.m)
+    v0 = torch.from_numpy(wl_full.v0).to(dev)
+    k, t = wl_full.k, wl_full.t
+    ws = torch.empty(S.workspace_size(M, k, t=t), dtype=torch.uint8, device=dev)
+
+    def solve():
+        return S.svds_c(M, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0, workspace=ws)
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+
+    # ---- timed region ----
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    H.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    steps_total, launches, passes, res = 0, 0, [], None
+    for _ in range(args.steps):
+        res = solve()
+        steps_total += res.info["steps"]
+        launches += res.info["launches"]
+        passes.append(res.info["passes"])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    prof = H.profile_read()
+    H.profile(False)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = steps_total / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel family ----
+    peak, peak_src = load_peaks()
+    fam = max(("Av", "ATu"), key=lambda f: prof[f][0])
+    bytes_per_launch = Al.bytes_one_pass() if Al.kind == "dense" else (
+        12 * Al.nnz + 4 * (Al.m + 1) if fam == "Av" else 12 * Al.nnz + 4 * (Al.n + 1))
+    f_ms, f_calls = prof[fam]
+    achieved = bytes_per_launch / (f_ms / f_calls / 1e3) / 1e9 if f_calls else None
+    step_bytes = res.info["bytes_model"] / max(res.info["steps"], 1)
+    total_prof = sum(v[0] for v in prof.values())
+
+    # ---- end to end through the host-buffer C-ABI entry point ----
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e_steps, e2e_ms, h2d, d2h = 0, 0.0, 0, 0
+        if Al.kind == "dense":
+            hostA = torch.empty((Al.n, Al.m), dtype=torch.float64).pin_memory()
+            hostA.copy_(torch.from_numpy(np.asfortranarray(Al.dense).T))
+            Ahost = W.Matrix("dense", Al.m, Al.n, dense=hostA.numpy().T)
+            h2d = 8 * Al.m * Al.n + 8 * Al.n
+        else:
+            Ahost = W.Matrix("csr", Al.m, Al.n,
+                             row_ptr=torch.from_numpy(Al.row_ptr).pin_memory().numpy(),
+                             col_idx=torch.from_numpy(Al.col_idx).pin_memory().numpy(),
+                             values=torch.from_numpy(Al.values).pin_memory().numpy())
+            h2d = 8 * (Al.m + 1) + 12 * Al.nnz + 8 * Al.n
+        d2h = 8 * (k + Al.m * k + Al.n * k + k)
+        v0h = torch.from_numpy(wl_full.v0).pin_memory().numpy()
+        S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h)  # warm
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+            e2e_steps += out[5]["steps"]
+        e2e = {"value": e2e_steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.e2e_steps,
+               "note": "includes per-solve matrix analysis (validation" + (", CSC build" if Al.kind == "csr" else "") + ")"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        sps, s, dt = cpu_sample(wl_full, seconds_target=15.0)
+        cpu = {"value": sps, "unit": "steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {s} Lanczos steps (Alg. 1 + CGS2, LBP first pass) of {wl_full.name}, "
+                         f"{dt:.1f} s, plain C -O2, 1 thread"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl_full.name, "m": A.m, "n": A.n, "nnz": A.nnz, "k": k, "t": t,
+                       "tol": wl_full.tol, "maxit": wl_full.maxit, "passes_per_solve": passes,
+                       "lanczos_steps_per_solve": steps_total // args.steps,
+                       "time_to_k_ms": ms / args.steps,
+                       "l2": f"inputs larger than L2 (A = {A.bytes_one_pass() >> 20} MB per pass)",
+                       "parallelism": f"rows{world}" if world > 1 else "single",
+                       "step_hbm_gb_per_s": step_bytes * (steps_total / (ms / 1e3)) / 1e9,
+                       "step_bytes_model": step_bytes},
+            "roofline": {"bound": "hbm", "kernel": f"{fam} product ({'gemv' if A.kind == 'dense' else 'spmv'})",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "bytes_per_launch": bytes_per_launch, "avg_launch_us": 1e3 * f_ms / max(f_calls, 1),
+                         "share_of_step": f_ms / ms if ms else None, "peak_source": peak_src},
+            "breakdown_ms": {f: round(v[0], 3) for f, v in prof.items() if v[1]},
+            "breakdown_share": {f: round(v[0] / total_prof, 4) for f, v in prof.items() if v[1] and total_prof},
+            "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

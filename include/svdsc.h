@@ -171,6 +171,17 @@ SVDSC_API svdsc_status svdsc_op_lbp(svdsc_matrix *M, const svdsc_opts *o, int32_
                           double *U, int64_t ldu, double *V, int64_t ldv, double *T,
                           svdsc_info *info);
 
+/* ---- profiling ----------------------------------------------------------------
+ * When enabled, svdsc_solve brackets each operation family with CUDA events on
+ * the handle's stream and accumulates device milliseconds per family (read
+ * after the solve).  Families: 0 A v products (a5), 1 A^T u products (a1),
+ * 2 CGS sweep p1, 3 p2, 4 p3, 5 normalize, 6 small SVD (a7), 7 residuals,
+ * 8 recombination (a8/a9), 9 restart misc, 10 collectives.  enable resets the
+ * counters.  ms / calls: host arrays of 16 entries. */
+#define SVDSC_PROF_FAMILIES 16
+SVDSC_API svdsc_status svdsc_profile_enable(svdsc_handle *h, int enable);
+SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int64_t *calls);
+
 /* ---- multi-GPU (row-partitioned A) -------------------------- */
 /* Rank 0 creates an NCCL unique id (128 bytes, host) that the caller
  * broadcasts (e.g. torch.distributed.broadcast); every rank then calls

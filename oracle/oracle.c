@@ -180,6 +180,12 @@ int or_jacobi_svd(int64_t p, int64_t q, const double *M, double *U, double *S,
      * orthogonal to working precision is never rotated again and the sweep
      * loop terminates (reading Q10a). */
     const double ctol = 2.0 * (double)p * 2.220446049250313e-16;
+    /* numerically zero columns (reading Q10b): a column whose norm is
+     * <= p eps ||M||_F carries only rounding noise; it is never rotated and its
+     * singular value is reported as exactly 0 (U completed orthonormally). */
+    double normF = 0.0;
+    for (int64_t i = 0; i < p * q; i++) normF += M[i] * M[i];
+    const double tiny = (double)p * 2.220446049250313e-16 * sqrt(normF);
     int sweeps = 0, converged = 0;
     for (sweeps = 1; sweeps <= max_sweeps; sweeps++) {
         int rotated = 0;
@@ -191,7 +197,7 @@ int or_jacobi_svd(int64_t p, int64_t q, const double *M, double *U, double *S,
                     beta += W[r + b * p] * W[r + b * p];
                     gamma += W[r + a * p] * W[r + b * p];
                 }
-                if (alpha == 0.0 || beta == 0.0) continue;
+                if (!(sqrt(alpha) > tiny) || !(sqrt(beta) > tiny)) continue;
                 if (fabs(gamma) <= ctol * sqrt(alpha) * sqrt(beta)) continue;
                 rotated = 1;
                 double zeta = (beta - alpha) / (2.0 * gamma);
@@ -217,7 +223,11 @@ int or_jacobi_svd(int64_t p, int64_t q, const double *M, double *U, double *S,
         free(W); free(Vw); free(Sw); free(perm);
         return OR_ESVD_NOCONV;
     }
-    for (int64_t j = 0; j < q; j++) { Sw[j] = or_norm2(p, W + j * p); perm[j] = j; }
+    for (int64_t j = 0; j < q; j++) {
+        Sw[j] = or_norm2(p, W + j * p);
+        if (!(Sw[j] > tiny)) Sw[j] = 0.0;
+        perm[j] = j;
+    }
     /* stable descending sort of the singular values (ties keep natural order) */
     for (int64_t i = 1; i < q; i++) {
         int64_t pj = perm[i];

@@ -32,6 +32,7 @@ struct Ctrl {
     int converged;
     int rankdef;
     double max_resid;
+    double svd_tiny;      // p eps ||T||_F: numerically zero column norm (reading Q10b)
     unsigned int cnt[16]; // last-block counters (one per reduction site)
 };
 
@@ -103,12 +104,25 @@ void random_start(int64_t N, int64_t row_offset, double *w, uint64_t seed, cudaS
 void axpy_dev(int64_t N, double *y, const double *c_dev, const double *x, const int *abort,
               cudaStream_t s);  // y -= c x
 
+// Fused single-kernel CGS2 + norm + normalize (single GPU, cooperative launch).
+struct FusedScratch {
+    double *partial;      // >= 2*nsm x (ncols+2)
+    double *h1, *h2, *h3; // >= ncols+2
+    unsigned int *bar;    // 2 zero-initialized words (grid barrier)
+};
+// false: the fused path is not applicable (caller uses cgs_p1/p2/p3 + normalize)
+bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
+                const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s);
+
 // ---- small SVD / restart ---------------------------------------------------------
 // Jacobi SVD of the p x p matrix stored (ld p) in W; outputs Uh, Sh, Vh (ld p),
 // writes ctrl->svd_status / svd_sweeps.  Vw is scratch (p x p).  kneed: number
 // of leading columns whose zero-sigma completion is required.
+// tlog: rotation log of small_svd_log_doubles(p) doubles (NULL: one-CTA
+// global-memory Jacobi without the cluster/log path)
+size_t small_svd_log_doubles(int p);
 void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double *Uh, double *Sh,
-               double *Vh, int kneed, Ctrl *ctrl, const int *abort, cudaStream_t s);
+               double *Vh, int kneed, Ctrl *ctrl, const int *abort, double *tlog, cudaStream_t s);
 // Eq. (4) residuals, convergence flag (Alg. 2 step 5)
 void residuals(int t, int k, const double *T, int ldt, const double *Uh, const double *Sh,
                double tol, double *resid, Ctrl *ctrl, const int *abort, cudaStream_t s);

@@ -10,12 +10,15 @@
 // pair ordering (t/2 independent rotations per round, one warp each), the
 // rotation rule and threshold of the oracle, descending sort, and the sign
 // rule of SPEC.md:158.  No CPU fallback.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace svdsc {
 namespace {
@@ -32,12 +35,27 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__global__ void k_copy_T(int p, const double *__restrict__ T, int ldt, double *W, double *V, const int *abort) {
+// W = T(1:p,1:p), V = I, ctrl->svd_tiny = p eps ||T||_F (reading Q10b); one CTA,
+// fixed-order reduction
+__global__ void __launch_bounds__(1024) k_copy_T(int p, const double *__restrict__ T, int ldt, double *W, double *V,
+                                                 Ctrl *ctrl, const int *abort) {
     if (aborted(abort)) return;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < p * p; idx += gridDim.x * blockDim.x) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) {
         const int r = idx % p, c = idx / p;
-        W[idx] = T[r + (int64_t)c * ldt];
+        const double x = T[r + (int64_t)c * ldt];
+        W[idx] = x;
         V[idx] = (r == c) ? 1.0 : 0.0;
+        s = fma(x, x, s);
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += sh[i];
+        ctrl->svd_tiny = (double)p * 2.220446049250313e-16 * sqrt(tot);
     }
 }
 
@@ -63,6 +81,7 @@ __global__ void __launch_bounds__(1024) k_jacobi(int p, double *W, double *V, Ct
     if (aborted(abort)) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int pe = p + (p & 1);
+    const double tiny = *(volatile double *)&ctrl->svd_tiny;
     __shared__ int rotated;
     int sweep;
     bool conv = false;
@@ -85,7 +104,7 @@ __global__ void __launch_bounds__(1024) k_jacobi(int p, double *W, double *V, Ct
                 al = warp_sum(al);
                 be = warp_sum(be);
                 ga = warp_sum(ga);
-                if (al == 0.0 || be == 0.0) continue;
+                if (!(sqrt(al) > tiny) || !(sqrt(be) > tiny)) continue;
                 if (fabs(ga) <= ctol * sqrt(al) * sqrt(be)) continue;
                 if (lane == 0) rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
@@ -119,11 +138,174 @@ __global__ void __launch_bounds__(1024) k_jacobi(int p, double *W, double *V, Ct
     }
 }
 
+// rotation parameters from t = tan(theta), pinned rounding (no contraction) so
+// that the W kernel and the V (log-apply) kernel produce bitwise equal c, s
+__device__ __forceinline__ void rot_cs(double t, double &c, double &s) {
+    c = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(t, t))));
+    s = __dmul_rn(c, t);
+}
+
+// One-sided Jacobi with W = T(1:p,1:p) resident in the shared memory of a
+// thread-block cluster (C CTAs own ceil(p/C) columns each; pairs whose columns
+// live in another CTA are reached through distributed shared memory).  The
+// tangent of every rotation is logged (0 = no rotation) so that V = J_1 J_2 ...
+// can be formed afterwards by k_apply_log, row-parallel, off the critical path.
+__global__ void __launch_bounds__(1024) k_jacobi_cluster(int p, int ncc, const double *__restrict__ W0, double *Wout,
+                                                         double *tlog, int max_sweeps, Ctrl *ctrl, const int *abort,
+                                                         double ctol) {
+    if (aborted(abort)) return;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+    extern __shared__ double Wl[];
+    __shared__ int rot_flag[2];  // by sweep parity: the flag of sweep s+1 is cleared during sweep s
+    const double tiny = *(volatile double *)&ctrl->svd_tiny;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int c0 = me * ncc;
+    for (int idx = threadIdx.x; idx < ncc * p; idx += blockDim.x) {
+        const int col = c0 + idx / p, r = idx % p;
+        Wl[idx] = (col < p) ? W0[r + (int64_t)col * p] : 0.0;
+    }
+    if (threadIdx.x == 0) rot_flag[0] = rot_flag[1] = 0;
+    cl.sync();
+    const int pe = p + (p & 1), npairs = pe / 2;
+    int sweep;
+    bool conv = false;
+    for (sweep = 1; sweep <= max_sweeps; sweep++) {
+        int *flag = &rot_flag[sweep & 1];
+        for (int rnd = 0; rnd < pe - 1; rnd++) {
+            double *logr = tlog + ((int64_t)(sweep - 1) * (pe - 1) + rnd) * npairs;
+            for (int q = me * nw + wid; q < npairs; q += C * nw) {
+                int a, b;
+                rr_pair(pe, rnd, q, a, b);
+                double t = 0.0;
+                if (b < p) {
+                    const int oa = a / ncc, ob = b / ncc;
+                    double *wa = Wl + (a - oa * ncc) * p, *wb = Wl + (b - ob * ncc) * p;
+                    if (oa != me) wa = cl.map_shared_rank(wa, oa);
+                    if (ob != me) wb = cl.map_shared_rank(wb, ob);
+                    double al = 0.0, be = 0.0, ga = 0.0;
+                    for (int r = lane; r < p; r += 32) {
+                        const double x = wa[r], y = wb[r];
+                        al = fma(x, x, al);
+                        be = fma(y, y, be);
+                        ga = fma(x, y, ga);
+                    }
+                    al = warp_sum(al);
+                    be = warp_sum(be);
+                    ga = warp_sum(ga);
+                    if (sqrt(al) > tiny && sqrt(be) > tiny && fabs(ga) > ctol * sqrt(al) * sqrt(be)) {
+                        const double zeta = (be - al) / (2.0 * ga);
+                        t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                        double c, s;
+                        rot_cs(t, c, s);
+                        for (int r = lane; r < p; r += 32) {
+                            const double x = wa[r], y = wb[r];
+                            wa[r] = c * x - s * y;
+                            wb[r] = s * x + c * y;
+                        }
+                        if (lane == 0) *flag = 1;
+                    }
+                }
+                if (lane == 0) logr[q] = t;
+            }
+            cl.sync();
+            // every CTA has read the previous sweep's flags by now: recycle that slot
+            if (rnd == 0 && threadIdx.x == 0) rot_flag[(sweep + 1) & 1] = 0;
+        }
+        int any = 0;
+        for (int r = 0; r < C; r++) any |= *cl.map_shared_rank(flag, r);
+        if (!any) {
+            conv = true;
+            break;
+        }
+    }
+    for (int idx = threadIdx.x; idx < ncc * p; idx += blockDim.x) {
+        const int col = c0 + idx / p, r = idx % p;
+        if (col < p) Wout[r + (int64_t)col * p] = Wl[idx];
+    }
+    if (me == 0 && threadIdx.x == 0) {
+        ctrl->svd_sweeps = conv ? sweep : max_sweeps;
+        ctrl->svd_status = conv ? 0 : (int)SVDSC_ESVD_NOCONV;
+    }
+    cl.sync();
+}
+
+// V = J_1 J_2 ... (the logged rotations) for R rows of V per CTA: each row of V
+// evolves independently (row r of V = e_r^T J_1 J_2 ...).  The log is staged
+// through shared memory in chunks of KR rounds with cp.async double buffering.
+constexpr int kLogRounds = 16;
+__global__ void k_apply_log(int p, const double *__restrict__ tlog, const Ctrl *ctrl, double *V, int R,
+                            const int *abort) {
+    if (aborted(abort)) return;
+    extern __shared__ double sm[];
+    const int pe = p + (p & 1), npairs = pe / 2;
+    const int nsweeps = ctrl->svd_sweeps;
+    const int64_t total_rounds = (int64_t)nsweeps * (pe - 1);
+    double *rows = sm;                           // R x p
+    double *buf = rows + (int64_t)R * p;         // 2 x kLogRounds x npairs
+    const int chunk = kLogRounds * npairs;
+    const int r0 = blockIdx.x * R;
+    for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
+        const int i = idx / p, j = idx % p;
+        rows[idx] = (r0 + i == j) ? 1.0 : 0.0;
+    }
+    auto load_chunk = [&](int64_t first_round, double *dst) {
+        const int64_t nrem = total_rounds - first_round;
+        const int n = (int)min((int64_t)kLogRounds, max((int64_t)0, nrem)) * npairs;
+        const double *src = tlog + first_round * npairs;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(src + i));
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    if (total_rounds > 0) load_chunk(0, buf);
+    int cur = 0;
+    for (int64_t base = 0; base < total_rounds; base += kLogRounds) {
+        if (base + kLogRounds < total_rounds) {
+            load_chunk(base + kLogRounds, buf + (cur ^ 1) * chunk);
+            asm volatile("cp.async.wait_group 1;");
+        } else {
+            asm volatile("cp.async.wait_group 0;");
+        }
+        __syncthreads();
+        const double *lg = buf + cur * chunk;
+        const int nr = (int)min((int64_t)kLogRounds, total_rounds - base);
+        for (int k = 0; k < nr; k++) {
+            const int rnd = (int)((base + k) % (pe - 1));
+            const int q = threadIdx.x;
+            if (q < npairs) {
+                int a, b;
+                rr_pair(pe, rnd, q, a, b);
+                const double t = lg[k * npairs + q];
+                if (b < p && t != 0.0) {
+                    double c, s;
+                    rot_cs(t, c, s);
+                    for (int i = 0; i < R; i++) {
+                        double *row = rows + i * p;
+                        const double x = row[a], y = row[b];
+                        row[a] = c * x - s * y;
+                        row[b] = s * x + c * y;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        cur ^= 1;
+    }
+    for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
+        const int i = idx / p, j = idx % p;
+        if (r0 + i < p) V[(r0 + i) + (int64_t)j * p] = rows[idx];
+    }
+}
+
 // norms, descending sort (ties: natural order), U = W / sigma, zero-sigma
 // completion of the first kneed columns, sign rule.
 __global__ void __launch_bounds__(1024) k_svd_finish(int p, const double *__restrict__ W, const double *__restrict__ V,
-                                                     double *Uh, double *Sh, double *Vh, int kneed, const int *abort) {
+                                                     double *Uh, double *Sh, double *Vh, int kneed, const Ctrl *ctrl,
+                                                     const int *abort) {
     if (aborted(abort)) return;
+    const double tiny = ctrl->svd_tiny;
     __shared__ double sig[kMaxP];
     __shared__ int dest[kMaxP];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -134,7 +316,7 @@ __global__ void __launch_bounds__(1024) k_svd_finish(int p, const double *__rest
             s = fma(x, x, s);
         }
         s = warp_sum(s);
-        if (lane == 0) sig[j] = sqrt(s);
+        if (lane == 0) sig[j] = (sqrt(s) > tiny) ? sqrt(s) : 0.0;
     }
     __syncthreads();
     for (int j = threadIdx.x; j < p; j += blockDim.x) {
@@ -305,14 +487,59 @@ __global__ void __launch_bounds__(256) k_recombine(int64_t N, int t, int k, cons
 
 }  // namespace
 
+size_t small_svd_log_doubles(int p) {
+    const int64_t pe = p + (p & 1);
+    return (size_t)(50 * (pe - 1) * (pe / 2));
+}
+
 void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double *Uh, double *Sh, double *Vh,
-               int kneed, Ctrl *ctrl, const int *abort, cudaStream_t s) {
-    k_copy_T<<<std::max(1, std::min(148, (p * p + 255) / 256)), 256, 0, s>>>(p, Tsrc, ldt, W, Vw, abort);
+               int kneed, Ctrl *ctrl, const int *abort, double *tlog, cudaStream_t s) {
+    k_copy_T<<<1, 1024, 0, s>>>(p, Tsrc, ldt, W, Vw, ctrl, abort);
+    count_launch();
     const double ctol = 2.0 * (double)p * 2.220446049250313e-16;  // reading Q10a
-    k_jacobi<<<1, 1024, 0, s>>>(p, W, Vw, ctrl, abort, ctol, 50);
-    k_svd_finish<<<1, 1024, 0, s>>>(p, W, Vw, Uh, Sh, Vh, kneed, abort);
-    count_launch();
-    count_launch();
+    bool done = false;
+    if (tlog) {
+        // smallest cluster whose shared memory holds W
+        int C = 1;
+        while (C <= 16 && (size_t)((p + C - 1) / C) * p * 8 > 200 * 1024) C <<= 1;
+        if (C <= 16) {
+            const int ncc = (p + C - 1) / C;
+            const size_t smem = (size_t)ncc * p * 8;
+            cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            if (C > 8) cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(C);
+            cfg.blockDim = dim3(1024);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = C;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, k_jacobi_cluster, p, ncc, (const double *)W, W, tlog, 50, ctrl, abort, ctol) ==
+                cudaSuccess) {
+                count_launch();
+                const int pe = p + (p & 1), npairs = pe / 2;
+                const int R = 4;
+                const int threads = std::max(32, ((npairs + 31) / 32) * 32);
+                const size_t smem2 = ((size_t)R * p + 2 * (size_t)kLogRounds * npairs) * 8;
+                cudaFuncSetAttribute(k_apply_log, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                k_apply_log<<<(p + R - 1) / R, threads, smem2, s>>>(p, tlog, ctrl, Vw, R, abort);
+                count_launch();
+                done = true;
+            } else {
+                cudaGetLastError();  // clear and fall back
+            }
+        }
+    }
+    if (!done) {
+        k_jacobi<<<1, 1024, 0, s>>>(p, W, Vw, ctrl, abort, ctol, 50);
+        count_launch();
+    }
+    k_svd_finish<<<1, 1024, 0, s>>>(p, W, Vw, Uh, Sh, Vh, kneed, ctrl, abort);
     count_launch();
 }
 

@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -88,7 +90,64 @@ inline void einval(bool bad, const std::string &m) {
 }
 }  // namespace
 
+// per-family CUDA-event timing (svdsc_profile_enable)
+struct Prof {
+    bool on = false;
+    double ms[SVDSC_PROF_FAMILIES] = {0};
+    int64_t calls[SVDSC_PROF_FAMILIES] = {0};
+    struct Pair {
+        cudaEvent_t a, b;
+        int fam;
+    };
+    std::vector<Pair> pending, pool;
+    int open_fam = -1;
+    cudaEvent_t open_ev = nullptr;
+    cudaEvent_t take() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back().a;
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void begin(int fam, cudaStream_t s) {
+        if (!on) return;
+        open_fam = fam;
+        open_ev = take();
+        cudaEventRecord(open_ev, s);
+    }
+    void end(cudaStream_t s) {
+        if (!on || open_fam < 0) return;
+        cudaEvent_t e = take();
+        cudaEventRecord(e, s);
+        pending.push_back({open_ev, e, open_fam});
+        open_fam = -1;
+    }
+    void harvest() {  // after a stream sync
+        for (auto &p : pending) {
+            float t = 0.f;
+            if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+                ms[p.fam] += t;
+                calls[p.fam]++;
+            }
+            pool.push_back({p.a, nullptr, 0});
+            pool.push_back({p.b, nullptr, 0});
+        }
+        pending.clear();
+    }
+    ~Prof() {
+        for (auto &p : pending) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+        for (auto &p : pool) cudaEventDestroy(p.a);
+    }
+};
+
 struct svdsc_handle {
+    Prof prof;
     int device = 0, nsm = 148;
     cudaStream_t stream = nullptr;
     std::string err;
@@ -166,6 +225,7 @@ struct Ws {
     double *W = nullptr, *Vw = nullptr, *Uh = nullptr, *Vh = nullptr, *Sh = nullptr;
     double *partial = nullptr, *h1 = nullptr, *h2 = nullptr, *nrm = nullptr, *rho = nullptr, *resid = nullptr;
     double *yfull = nullptr, *vfull = nullptr, *vtmp = nullptr;
+    double *tlog = nullptr;
     Ctrl *ctrl = nullptr;
     int64_t ldu = 0, ldv = 0, nv = 0, n_pad = 0;
     int ldt = 0;
@@ -205,6 +265,7 @@ size_t carve(Ws &w, void *base, int64_t m, int64_t n, int t, int k, int P) {
     w.nrm = c.take<double>(4);
     w.rho = c.take<double>(k);
     w.resid = c.take<double>(k);
+    w.tlog = c.take<double>(small_svd_log_doubles(t));
     if (P > 1) {
         w.yfull = c.take<double>(w.n_pad);
         w.vfull = c.take<double>(w.n_pad);
@@ -258,15 +319,19 @@ struct Solver {
             ckn(g_nccl.AllGather(vcol, w.vfull, (size_t)nv, kNcclFloat64, H->comm, s), "ncclAllGather");
             x = w.vfull;
         }
+        H->prof.begin(0, s);
         if (M->kind == 0) spmv_csr(M->A, x, z, c_dev, zprev, abort, s);
         else gemv_n(M->D, x, z, c_dev, zprev, abort, s);
+        H->prof.end(s);
         matvecs++;
     }
     // wslice = (A^T u)_slice - c wprev
     void Atu(const double *u, double *wcol, const double *c_dev, const double *wprev) {
         if (P == 1) {
+            H->prof.begin(1, s);
             if (M->kind == 0) spmv_csr(M->At, u, wcol, c_dev, wprev, abort, s);
             else gemv_t(M->D, u, wcol, c_dev, wprev, abort, s);
+            H->prof.end(s);
         } else {
             if (M->kind == 0) spmv_csr(M->At, u, w.yfull, nullptr, nullptr, abort, s);
             else gemv_t(M->D, u, w.yfull, nullptr, nullptr, abort, s);
@@ -279,15 +344,43 @@ struct Solver {
     // two-pass CGS against Q(:, 0:ncols) then ||w||^2 in rb.nrm
     void cgs2(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, bool force_reorth) {
         if (ncols > 0 && (o->reorth != 0 || force_reorth)) {
+            H->prof.begin(2, s);
             cgs_p1(N, ncols, Q, ldq, wv, rb, abort, nsm, s);
+            H->prof.end(s);
             allreduce(rb.h1, ncols);
+            H->prof.begin(3, s);
             cgs_p2(N, ncols, Q, ldq, wv, rb, abort, nsm, s);
+            H->prof.end(s);
             allreduce(rb.h2, ncols + 1);
+            H->prof.begin(4, s);
             cgs_p3(N, ncols, Q, ldq, wv, rb.h2, rb, abort, nsm, s);
+            H->prof.end(s);
         } else {
+            H->prof.begin(4, s);
             cgs_p3(N, 0, Q, ldq, wv, nullptr, rb, abort, nsm, s);
+            H->prof.end(s);
         }
         allreduce(rb.nrm, 1);
+    }
+
+    bool fused_ok = true;
+    // re-orthogonalize wv against Q(:, 0:ncols) (optionally after wv -= Q pre_h),
+    // then beta = ||wv||, breakdown test, T entry, wv /= beta.
+    void orth_norm(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, double *t_entry, int chk,
+                   const double *pre_h) {
+        if (P == 1 && o->reorth != 0 && fused_ok) {
+            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, &w.ctrl->cnt[14]};
+            H->prof.begin(11, s);
+            const bool ok = cgs2_fused(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s);
+            H->prof.end(s);
+            if (ok) return;
+            fused_ok = false;
+        }
+        if (pre_h) cgs_p3(N, ncols, Q, ldq, wv, pre_h, rb, abort, nsm, s);
+        cgs2(N, ncols, Q, ldq, wv, false);
+        H->prof.begin(5, s);
+        normalize(N, wv, rb, w.ctrl, t_entry, chk, 0, nsm, s);
+        H->prof.end(s);
     }
 
     double *Ucol(int j) { return w.U + (int64_t)j * w.ldu; }
@@ -303,15 +396,13 @@ struct Solver {
         switch (h.kind) {
             case 0:  // Alg. 1 lines 2-3
                 Av(Vcol(0), Ucol(0), nullptr, nullptr);
-                cgs2(m, 0, w.U, w.ldu, Ucol(0), false);
-                normalize(m, Ucol(0), rb, w.ctrl, Tm(0, 0), chk, 0, nsm, s);
+                orth_norm(m, 0, w.U, w.ldu, Ucol(0), Tm(0, 0), chk, nullptr);
                 bytes_model += bytesA + 8 * m * 5;
                 break;
-            case 1: {  // Alg. 1 lines 5-6 + re-orthogonalization
+            case 1: {  // Alg. 1 lines 5-6 + re-orthogonalization (PAPER.md:121)
                 const int i = h.i;
                 Atu(Ucol(i - 1), Vcol(i), Tm(i - 1, i - 1), Vcol(i - 1));
-                cgs2(nv, i, w.V, w.ldv, Vcol(i), false);
-                normalize(nv, Vcol(i), rb, w.ctrl, Tm(i - 1, i), chk, 0, nsm, s);
+                orth_norm(nv, i, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk, nullptr);
                 steps++;
                 bytes_model += bytesA + 8 * nv * (3 * (int64_t)i + 5);
                 break;
@@ -319,16 +410,13 @@ struct Solver {
             case 2: {  // Alg. 1 lines 7-8 + re-orthogonalization
                 const int i = h.i;
                 Av(Vcol(i), Ucol(i), Tm(i - 1, i), Ucol(i - 1));
-                cgs2(m, i, w.U, w.ldu, Ucol(i), false);
-                normalize(m, Ucol(i), rb, w.ctrl, Tm(i, i), chk, 0, nsm, s);
+                orth_norm(m, i, w.U, w.ldu, Ucol(i), Tm(i, i), chk, nullptr);
                 bytes_model += bytesA + 8 * m * (3 * (int64_t)i + 5);
                 break;
             }
             case 3: {  // Alg. 2 steps 10-11: u_{k+1} = A v_{k+1} - Uk rho, re-orth
                 Av(Vcol(k), Ucol(k), nullptr, nullptr);
-                cgs_p3(m, k, w.U, w.ldu, Ucol(k), w.rho, rb, abort, nsm, s);
-                cgs2(m, k, w.U, w.ldu, Ucol(k), false);
-                normalize(m, Ucol(k), rb, w.ctrl, Tm(k, k), chk, 0, nsm, s);
+                orth_norm(m, k, w.U, w.ldu, Ucol(k), Tm(k, k), chk, w.rho);
                 break;
             }
         }
@@ -358,6 +446,7 @@ struct Solver {
         ck(cudaMemcpyAsync(H->hctrl, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H ctrl");
         ck(cudaStreamSynchronize(s), "sync");
         ck(cudaGetLastError(), "kernels");
+        H->prof.harvest();
         return *H->hctrl;
     }
 
@@ -367,10 +456,22 @@ struct Solver {
         for (;;) {
             for (size_t idx = pos; idx < plan.size(); idx++) run_half(plan[idx], c0 + (int)idx);
             if (with_svd) {
-                small_svd(t, w.T, w.ldt, w.W, w.Vw, w.Uh, w.Sh, w.Vh, k, w.ctrl, abort, s);
+                H->prof.begin(6, s);
+                small_svd(t, w.T, w.ldt, w.W, w.Vw, w.Uh, w.Sh, w.Vh, k, w.ctrl, abort, w.tlog, s);
+                H->prof.end(s);
+                H->prof.begin(7, s);
                 residuals(t, k, w.T, w.ldt, w.Uh, w.Sh, o->tol, w.resid, w.ctrl, abort, s);
+                H->prof.end(s);
             }
             Ctrl c = read_ctrl();
+            if (const char *dump = getenv("SVDSC_DEBUG_DUMP")) {  // debugging aid: append T per pass
+                std::vector<double> hT((size_t)(t + 1) * (t + 1));
+                ck(cudaMemcpy(hT.data(), w.T, hT.size() * sizeof(double), cudaMemcpyDeviceToHost), "dump");
+                if (FILE *f = fopen(dump, "ab")) {
+                    fwrite(hT.data(), sizeof(double), hT.size(), f);
+                    fclose(f);
+                }
+            }
             if (!c.abort) return;
             const int idx = c.abort_check - c0;
             if (idx < 0 || idx >= (int)plan.size()) throw SvdscError(SVDSC_ECUDA, "breakdown bookkeeping");
@@ -387,6 +488,10 @@ struct Solver {
         carve(w, ws_base, m, n, t, k, P);
         nv = w.nv;
         rb = RedBuf{w.partial, kMaxBlocks, w.h1, w.h2, w.nrm, w.ctrl->cnt};
+        {
+            const char *e = getenv("SVDSC_NO_FUSED");
+            fused_ok = !(e && e[0] == '1');
+        }
         abort = &w.ctrl->abort;
         bytesA = M->kind == 0 ? 12 * M->nnz + 4 * (m + 1) : 8 * m * n;
         ck(cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s), "memset");
@@ -440,10 +545,14 @@ struct Solver {
                 const bool stop = o->fixed_passes > 0 ? passes >= o->fixed_passes : (c.converged || passes >= maxit);
                 if (stop) break;
                 // augmented restart, Alg. 2 steps 8-12
+                H->prof.begin(8, s);
                 recombine(m, t, k, w.U, w.ldu, w.Uh, t, w.U, w.ldu, nsm, s);
                 recombine(nv, t, k, w.V, w.ldv, w.Vh, t, w.V, w.ldv, nsm, s);
+                H->prof.end(s);
+                H->prof.begin(9, s);
                 copy_col(nv, Vcol(t), Vcol(k), s);  // v_{k+1} = v_{t+1}
                 restart_T(t, k, w.T, w.ldt, w.Uh, w.Sh, w.rho, s);
+                H->prof.end(s);
                 matvecs += 0;
                 c0 += (int)plan.size();
                 plan.clear();
@@ -456,7 +565,9 @@ struct Solver {
             // Alg. 2 steps 15-16: S, U_k = U(:,1:t) Uh(:,1:k), V_k likewise
             ck(cudaMemcpyAsync(S, w.Sh, k * sizeof(double), cudaMemcpyDeviceToDevice, s), "S");
             if (resid) ck(cudaMemcpyAsync(resid, w.resid, k * sizeof(double), cudaMemcpyDeviceToDevice, s), "resid");
+            H->prof.begin(8, s);
             recombine(m, t, k, w.U, w.ldu, w.Uh, t, Uout, ldu_out, nsm, s);
+            H->prof.end(s);
             if (P == 1) {
                 recombine(nv, t, k, w.V, w.ldv, w.Vh, t, Vout, ldv_out, nsm, s);
             } else {
@@ -833,7 +944,7 @@ namespace {
 // op-level scratch: ctrl + partials + reductions + Jacobi work arrays
 struct OpScratch {
     Ctrl *ctrl;
-    double *partial, *h1, *h2, *nrm, *W, *Vw;
+    double *partial, *h1, *h2, *nrm, *W, *Vw, *tlog;
 };
 OpScratch op_scratch(svdsc_handle *h, int maxcols, int p) {
     Carver c{nullptr};
@@ -844,6 +955,7 @@ OpScratch op_scratch(svdsc_handle *h, int maxcols, int p) {
     c.take<double>(4);
     c.take<double>((size_t)p * p);
     c.take<double>((size_t)p * p);
+    c.take<double>(small_svd_log_doubles(p));
     const size_t need = c.off + 256;
     if (need > h->scratch_bytes) {
         if (h->scratch) cudaFree(h->scratch);
@@ -860,6 +972,7 @@ OpScratch op_scratch(svdsc_handle *h, int maxcols, int p) {
     o.nrm = d.take<double>(4);
     o.W = d.take<double>((size_t)p * p);
     o.Vw = d.take<double>((size_t)p * p);
+    o.tlog = d.take<double>(small_svd_log_doubles(p));
     ck(cudaMemsetAsync(o.ctrl, 0, sizeof(Ctrl), h->stream), "memset");
     return o;
 }
@@ -901,7 +1014,7 @@ svdsc_status svdsc_op_small_svd(svdsc_handle *h, int32_t p, const double *Tm, do
         einval(p < 1 || p > 1023 || !Tm || !U || !S || !V, "bad arguments");
         OpScratch sc = op_scratch(h, 0, p);
         cudaStream_t s = h->stream;
-        small_svd(p, Tm, p, sc.W, sc.Vw, U, S, V, p, sc.ctrl, nullptr, s);
+        small_svd(p, Tm, p, sc.W, sc.Vw, U, S, V, p, sc.ctrl, nullptr, getenv("SVDSC_NO_CLUSTER_SVD") ? nullptr : sc.tlog, s);
         Ctrl c;
         ck(cudaMemcpyAsync(&c, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H");
         ck(cudaStreamSynchronize(s), "sync");
@@ -921,6 +1034,27 @@ svdsc_status svdsc_op_recombine(svdsc_handle *h, int64_t N, int32_t t, int32_t k
         recombine(N, t, k, Q, ldq, W, ldw, Qout, ldo, h->nsm, h->stream);
         ck(cudaGetLastError(), "recombine");
     });
+}
+
+svdsc_status svdsc_profile_enable(svdsc_handle *h, int enable) {
+    if (!h) return SVDSC_EINVAL;
+    cudaStreamSynchronize(h->stream);
+    h->prof.harvest();
+    h->prof.on = enable != 0;
+    for (int i = 0; i < SVDSC_PROF_FAMILIES; i++) {
+        h->prof.ms[i] = 0.0;
+        h->prof.calls[i] = 0;
+    }
+    return SVDSC_OK;
+}
+
+svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int64_t *calls) {
+    if (!h || !ms || !calls) return SVDSC_EINVAL;
+    for (int i = 0; i < SVDSC_PROF_FAMILIES; i++) {
+        ms[i] = h->prof.ms[i];
+        calls[i] = h->prof.calls[i];
+    }
+    return SVDSC_OK;
 }
 
 svdsc_status svdsc_comm_unique_id(unsigned char id[128]) {

@@ -54,7 +54,10 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
            "svdsc_matrix_csr", "svdsc_matrix_dense", "svdsc_matrix_destroy", "svdsc_workspace_size",
            "svdsc_solve", "svdsc_solve_host_csr", "svdsc_solve_host_dense", "svdsc_op_matvec",
            "svdsc_op_cgs2", "svdsc_op_small_svd", "svdsc_op_recombine", "svdsc_op_lbp",
-           "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows"]
+           "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows",
+           "svdsc_profile_enable", "svdsc_profile_read"]
+PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",
+                 "recombine", "restart_misc", "collectives", "cgs2_fused"]
 
 
 def lib():
@@ -92,6 +95,8 @@ def lib():
         L.svdsc_comm_unique_id.argtypes = [ctypes.c_char_p]
         L.svdsc_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
         L.svdsc_partition_rows.argtypes = [I64, P, I64, ctypes.c_int, P]
+        L.svdsc_profile_enable.argtypes = [P, ctypes.c_int]
+        L.svdsc_profile_read.argtypes = [P, P, P]
         for name in EXPORTS:
             f = getattr(L, name)
             if f.restype is ctypes.c_int:  # default
@@ -135,6 +140,15 @@ class Handle:
     def comm_init(self, nranks, rank, uid: bytes):
         self._check(lib().svdsc_comm_init(self.ptr, nranks, rank, uid))
         self.nranks, self.rank = nranks, rank
+
+    def profile(self, enable=True):
+        self._check(lib().svdsc_profile_enable(self.ptr, int(enable)))
+
+    def profile_read(self):
+        ms = np.zeros(16)
+        calls = np.zeros(16, dtype=np.int64)
+        self._check(lib().svdsc_profile_read(self.ptr, ms.ctypes.data, calls.ctypes.data))
+        return {name: (float(ms[i]), int(calls[i])) for i, name in enumerate(PROF_FAMILIES)}
 
     def close(self):
         if self.ptr:
