@@ -138,124 +138,291 @@ __global__ void __launch_bounds__(1024) k_jacobi(int p, double *W, double *V, Ct
     }
 }
 
-// rotation parameters from t = tan(theta), pinned rounding (no contraction) so
-// that the W kernel and the V (log-apply) kernel produce bitwise equal c, s
+__device__ __forceinline__ double rcp_approx(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ double rsqrt_approx(double x) {
+    double y;
+    asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
+// rotation parameters from t = tan(theta): c = (1 + t^2)^(-1/2) to ~1 ulp
+// (hardware rsqrt approximation + two Newton steps), s = c t.  Pinned
+// rounding (explicit _rn intrinsics, no contraction choices left to the
+// compiler) so that the W kernel and the V (log-apply) kernel produce bitwise
+// equal c, s from the logged t.
 __device__ __forceinline__ void rot_cs(double t, double &c, double &s) {
-    c = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(t, t))));
+    const double x = __fma_rn(t, t, 1.0);
+    const double hx = __dmul_rn(0.5, x);
+    double y = rsqrt_approx(x);
+    y = __dmul_rn(y, __fma_rn(-hx, __dmul_rn(y, y), 1.5));
+    y = __dmul_rn(y, __fma_rn(-hx, __dmul_rn(y, y), 1.5));
+    c = y;
     s = __dmul_rn(c, t);
 }
 
-// One-sided Jacobi with W = T(1:p,1:p) resident in the shared memory of a
-// thread-block cluster (C CTAs own ceil(p/C) columns each; pairs whose columns
-// live in another CTA are reached through distributed shared memory).  The
-// tangent of every rotation is logged (0 = no rotation) so that V = J_1 J_2 ...
-// can be formed afterwards by k_apply_log, row-parallel, off the critical path.
-__global__ void __launch_bounds__(1024) k_jacobi_cluster(int p, int ncc, const double *__restrict__ W0, double *Wout,
-                                                         double *tlog, int max_sweeps, Ctrl *ctrl, const int *abort,
-                                                         double ctol) {
+// tangent of the Jacobi angle for the pair (alpha, beta, gamma): only the
+// convergence rate depends on its accuracy (the rotation built from it by
+// rot_cs is orthogonal to working precision), so fast approximate reciprocal /
+// rsqrt are used: zeta = (beta - alpha) / (2 gamma), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)).
+__device__ __forceinline__ double jacobi_tan(double al, double be, double gam) {
+    const double zeta = (be - al) * 0.5 * rcp_approx(gam);
+    const double az = fabs(zeta);
+    double t;
+    if (az > 1e100) {
+        t = 0.5 * rcp_approx(az);
+    } else {
+        const double r = fma(az, az, 1.0);
+        t = rcp_approx(az + r * rsqrt_approx(r));
+    }
+    return zeta >= 0.0 ? t : -t;
+}
+
+// ---------------------------------------------------------------------------
+// Block one-sided Jacobi on a thread-block cluster (B200: up to 16 CTAs,
+// distributed shared memory).  The pe = p + (p odd) columns are cut into 2C
+// half-blocks of h columns; CTA c holds two half-blocks in its shared memory
+// and, per block round, runs a full local round-robin sweep over its 2h
+// columns (all pairs, LDS only, __syncthreads between local rounds).  Between
+// block rounds the half-blocks move along the circle-method tournament (one
+// DSMEM pull into registers, cluster barrier, store), so every pair of
+// half-blocks meets once per block sweep.  Every rotation is logged as
+// (t = tan theta, a, b) for k_apply_log; rotations of one local round (all
+// CTAs) touch disjoint columns, so replaying them round by round is exact.
+struct RotLog {
+    double t;
+    int32_t a, b;
+};
+
+// circle-method tournament over 2C players (player 0 fixed, m = 2C - 1)
+__device__ __forceinline__ int hb_at(int C, int r, int c, int slot) {
+    const int m = 2 * C - 1;
+    if (slot == 0) return c == 0 ? 0 : ((c - 1 - r) % m + m) % m + 1;
+    return ((m - 1 - c - r) % m + m) % m + 1;
+}
+// where (cta, slot) is player P in round r
+__device__ __forceinline__ void hb_loc(int C, int r, int P, int &cta, int &slot) {
+    if (P == 0) {
+        cta = 0;
+        slot = 0;
+        return;
+    }
+    const int m = 2 * C - 1;
+    const int k = (P - 1 + r) % m;
+    if (k < C - 1) {
+        cta = k + 1;
+        slot = 0;
+    } else {
+        cta = m - 1 - k;
+        slot = 1;
+    }
+}
+
+constexpr int kExR = 20;  // registers per thread per slot for the half-block exchange (h*p <= 20*640)
+
+constexpr int kMaxRPL = 20;   // rows per lane held in registers: p <= 32 * kMaxRPL
+constexpr int kJThreads = 640; // 20 warps: one warp per pair, <= 20 pairs per CTA
+constexpr int kMaxPairs = kJThreads / 32;
+
+template <bool CL, int kRPL>
+__global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const double *__restrict__ W0, double *Wout,
+                                                       RotLog *rlog, int max_sweeps, Ctrl *ctrl, const int *abort,
+                                                       double ctol) {
     if (aborted(abort)) return;
     cg::cluster_group cl = cg::this_cluster();
-    const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
-    extern __shared__ double Wl[];
-    __shared__ int rot_flag[2];  // by sweep parity: the flag of sweep s+1 is cleared during sweep s
+    const int C = CL ? (int)cl.num_blocks() : 1;
+    const int me = CL ? (int)cl.block_rank() : 0;
+    extern __shared__ double Wl[];  // slot s, local column i: Wl + (s*h + i)*p
+    __shared__ int rot_flag[2];
+    __shared__ int src_cta[2], src_slot[2];
     const double tiny = *(volatile double *)&ctrl->svd_tiny;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int c0 = me * ncc;
-    for (int idx = threadIdx.x; idx < ncc * p; idx += blockDim.x) {
-        const int col = c0 + idx / p, r = idx % p;
+    const double tiny2 = tiny * tiny;
+    const double ctol2 = ctol * ctol;
+    constexpr int kG = 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, gl = lane;
+    const int ngrp = blockDim.x / kG;
+    const int m = 2 * C - 1;
+    const int H2 = 2 * h;
+    __shared__ unsigned short pair_tab[2 * kMaxPairs * 2 * kMaxPairs];  // [lr][q] = i | j << 8
+    __shared__ int gcol[2 * kMaxPairs];                                  // local column -> global
+    int hb[2] = {hb_at(C, 0, me, 0), hb_at(C, 0, me, 1)};
+    for (int idx = threadIdx.x; idx < (H2 - 1) * h; idx += blockDim.x) {
+        int i, j;
+        rr_pair(H2, idx / h, idx % h, i, j);
+        pair_tab[idx] = (unsigned short)(i | (j << 8));
+    }
+    for (int lc = threadIdx.x; lc < H2; lc += blockDim.x) gcol[lc] = hb[lc / h] * h + (lc % h);
+    for (int idx = threadIdx.x; idx < H2 * p; idx += blockDim.x) {
+        const int lc = idx / p, r = idx % p;
+        const int col = hb[lc / h] * h + (lc % h);
         Wl[idx] = (col < p) ? W0[r + (int64_t)col * p] : 0.0;
     }
     if (threadIdx.x == 0) rot_flag[0] = rot_flag[1] = 0;
-    cl.sync();
-    const int pe = p + (p & 1), npairs = pe / 2;
+    if (CL) cl.sync(); else __syncthreads();
+    const int64_t per_round = (int64_t)C * h;
+    const int lrounds = H2 - 1;
     int sweep;
     bool conv = false;
     for (sweep = 1; sweep <= max_sweeps; sweep++) {
         int *flag = &rot_flag[sweep & 1];
-        for (int rnd = 0; rnd < pe - 1; rnd++) {
-            double *logr = tlog + ((int64_t)(sweep - 1) * (pe - 1) + rnd) * npairs;
-            for (int q = me * nw + wid; q < npairs; q += C * nw) {
-                int a, b;
-                rr_pair(pe, rnd, q, a, b);
-                double t = 0.0;
-                if (b < p) {
-                    const int oa = a / ncc, ob = b / ncc;
-                    double *wa = Wl + (a - oa * ncc) * p, *wb = Wl + (b - ob * ncc) * p;
-                    if (oa != me) wa = cl.map_shared_rank(wa, oa);
-                    if (ob != me) wb = cl.map_shared_rank(wb, ob);
-                    double al = 0.0, be = 0.0, ga = 0.0;
-                    for (int r = lane; r < p; r += 32) {
-                        const double x = wa[r], y = wb[r];
-                        al = fma(x, x, al);
-                        be = fma(y, y, be);
-                        ga = fma(x, y, ga);
+        for (int br = 0; br < m; br++) {
+            for (int lr = 0; lr < lrounds; lr++) {
+                RotLog *logr = rlog + (((int64_t)(sweep - 1) * m + br) * lrounds + lr) * per_round + (int64_t)me * h;
+                for (int qb = wid * (32 / kG); qb < h; qb += ngrp) {
+                    const int q = qb + lane / kG;
+                    int i = 0, j = 0;
+                    if (q < h) {
+                        const unsigned pr = pair_tab[lr * h + q];
+                        i = pr & 0xff;
+                        j = pr >> 8;
                     }
-                    al = warp_sum(al);
-                    be = warp_sum(be);
-                    ga = warp_sum(ga);
-                    if (sqrt(al) > tiny && sqrt(be) > tiny && fabs(ga) > ctol * sqrt(al) * sqrt(be)) {
-                        const double zeta = (be - al) / (2.0 * ga);
-                        t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const int ga = gcol[i], gb = gcol[j];
+                    const bool live = (q < h) && ga < p && gb < p;
+                    // the pair's columns, oriented (lower global index, higher) as in the oracle
+                    double *pa = Wl + (int64_t)(ga < gb ? i : j) * p, *pb = Wl + (int64_t)(ga < gb ? j : i) * p;
+                    double xr[kRPL], yr[kRPL];
+                    double al = 0.0, be = 0.0, gam = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+#pragma unroll
+                    for (int u = 0; u < kRPL; u++) {
+                        const int r = gl + kG * u;
+                        const bool ok = live && r < p;
+                        xr[u] = ok ? pa[r] : 0.0;
+                        yr[u] = ok ? pb[r] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kRPL; u += 2) {
+                        al = fma(xr[u], xr[u], al);
+                        be = fma(yr[u], yr[u], be);
+                        gam = fma(xr[u], yr[u], gam);
+                        if (u + 1 < kRPL) {
+                            al1 = fma(xr[u + 1], xr[u + 1], al1);
+                            be1 = fma(yr[u + 1], yr[u + 1], be1);
+                            ga1 = fma(xr[u + 1], yr[u + 1], ga1);
+                        }
+                    }
+                    al += al1;
+                    be += be1;
+                    gam += ga1;
+#pragma unroll
+                    for (int off = kG / 2; off > 0; off >>= 1) {
+                        al += __shfl_xor_sync(0xffffffffu, al, off, kG);
+                        be += __shfl_xor_sync(0xffffffffu, be, off, kG);
+                        gam += __shfl_xor_sync(0xffffffffu, gam, off, kG);
+                    }
+                    double t = 0.0;
+                    if (live && al > tiny2 && be > tiny2 && gam * gam > ctol2 * (al * be)) {
+                        t = jacobi_tan(al, be, gam);
                         double c, s;
                         rot_cs(t, c, s);
-                        for (int r = lane; r < p; r += 32) {
-                            const double x = wa[r], y = wb[r];
-                            wa[r] = c * x - s * y;
-                            wb[r] = s * x + c * y;
+#pragma unroll
+                        for (int u = 0; u < kRPL; u++) {
+                            const int r = gl + kG * u;
+                            if (r < p) {
+                                pa[r] = c * xr[u] - s * yr[u];
+                                pb[r] = s * xr[u] + c * yr[u];
+                            }
                         }
-                        if (lane == 0) *flag = 1;
+                        if (gl == 0) *flag = 1;
+                    }
+                    if (gl == 0 && q < h) {
+                        RotLog e;
+                        e.t = t;
+                        e.a = min(ga, gb);
+                        e.b = max(ga, gb);
+                        logr[q] = e;
                     }
                 }
-                if (lane == 0) logr[q] = t;
+                __syncthreads();
             }
-            cl.sync();
-            // every CTA has read the previous sweep's flags by now: recycle that slot
-            if (rnd == 0 && threadIdx.x == 0) rot_flag[(sweep + 1) & 1] = 0;
+            if (CL && m > 1) {
+                // move to round br+1 (after the last block round the circle is back at round 0)
+                const int rn = (br + 1) % m;
+                if (threadIdx.x < 2) {
+                    int ct, sl;
+                    hb_loc(C, br, hb_at(C, rn, me, threadIdx.x), ct, sl);
+                    src_cta[threadIdx.x] = ct;
+                    src_slot[threadIdx.x] = sl;
+                }
+                cl.sync();  // local sweeps done everywhere; sources known
+                double reg[2][kExR];
+                const int n = h * p;
+#pragma unroll
+                for (int sl = 0; sl < 2; sl++) {
+                    const double *src = Wl + (int64_t)src_slot[sl] * n;
+                    if (src_cta[sl] != me) src = cl.map_shared_rank(src, src_cta[sl]);
+#pragma unroll
+                    for (int u = 0; u < kExR; u++) {
+                        const int idx = threadIdx.x + u * blockDim.x;
+                        reg[sl][u] = (idx < n) ? src[idx] : 0.0;
+                    }
+                }
+                cl.sync();  // every CTA has pulled its new half-blocks
+#pragma unroll
+                for (int sl = 0; sl < 2; sl++)
+#pragma unroll
+                    for (int u = 0; u < kExR; u++) {
+                        const int idx = threadIdx.x + u * blockDim.x;
+                        if (idx < n) Wl[(int64_t)sl * n + idx] = reg[sl][u];
+                    }
+                hb[0] = hb_at(C, rn, me, 0);
+                hb[1] = hb_at(C, rn, me, 1);
+                for (int lc = threadIdx.x; lc < H2; lc += blockDim.x) gcol[lc] = hb[lc / h] * h + (lc % h);
+                __syncthreads();
+            }
         }
+        if (CL) cl.sync(); else __syncthreads();
         int any = 0;
-        for (int r = 0; r < C; r++) any |= *cl.map_shared_rank(flag, r);
+        if (CL) {
+            for (int r = 0; r < C; r++) any |= *cl.map_shared_rank(flag, r);
+        } else {
+            any = *flag;
+        }
+        if (CL) cl.sync(); else __syncthreads();
+        if (threadIdx.x == 0) rot_flag[(sweep + 1) & 1] = 0;
         if (!any) {
             conv = true;
             break;
         }
     }
-    for (int idx = threadIdx.x; idx < ncc * p; idx += blockDim.x) {
-        const int col = c0 + idx / p, r = idx % p;
+    for (int idx = threadIdx.x; idx < H2 * p; idx += blockDim.x) {
+        const int lc = idx / p, r = idx % p;
+        const int col = hb[lc / h] * h + (lc % h);
         if (col < p) Wout[r + (int64_t)col * p] = Wl[idx];
     }
     if (me == 0 && threadIdx.x == 0) {
         ctrl->svd_sweeps = conv ? sweep : max_sweeps;
         ctrl->svd_status = conv ? 0 : (int)SVDSC_ESVD_NOCONV;
     }
-    cl.sync();
+    if (CL) cl.sync();
 }
 
-// V = J_1 J_2 ... (the logged rotations) for R rows of V per CTA: each row of V
-// evolves independently (row r of V = e_r^T J_1 J_2 ...).  The log is staged
-// through shared memory in chunks of KR rounds with cp.async double buffering.
+// V = J_1 J_2 ... (the logged rotations) for R rows of V per CTA: row r of V is
+// e_r^T J_1 J_2 ..., independent of the other rows.  The log is staged through
+// shared memory in chunks of kLogRounds rounds with cp.async double buffering.
 constexpr int kLogRounds = 16;
-__global__ void k_apply_log(int p, const double *__restrict__ tlog, const Ctrl *ctrl, double *V, int R,
-                            const int *abort) {
+__global__ void k_apply_log(int p, int per_round, int rounds_per_sweep, const RotLog *__restrict__ rlog,
+                            const Ctrl *ctrl, double *V, int R, const int *abort) {
     if (aborted(abort)) return;
     extern __shared__ double sm[];
-    const int pe = p + (p & 1), npairs = pe / 2;
-    const int nsweeps = ctrl->svd_sweeps;
-    const int64_t total_rounds = (int64_t)nsweeps * (pe - 1);
-    double *rows = sm;                           // R x p
-    double *buf = rows + (int64_t)R * p;         // 2 x kLogRounds x npairs
-    const int chunk = kLogRounds * npairs;
+    const int64_t total_rounds = (int64_t)ctrl->svd_sweeps * rounds_per_sweep;
+    double *rows = sm;                                        // R x p
+    RotLog *buf = reinterpret_cast<RotLog *>(rows + (int64_t)R * p);  // 2 x kLogRounds x per_round
+    const int chunk = kLogRounds * per_round;
     const int r0 = blockIdx.x * R;
     for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
         const int i = idx / p, j = idx % p;
         rows[idx] = (r0 + i == j) ? 1.0 : 0.0;
     }
-    auto load_chunk = [&](int64_t first_round, double *dst) {
+    auto load_chunk = [&](int64_t first_round, RotLog *dst) {
         const int64_t nrem = total_rounds - first_round;
-        const int n = (int)min((int64_t)kLogRounds, max((int64_t)0, nrem)) * npairs;
-        const double *src = tlog + first_round * npairs;
+        const int n = (int)min((int64_t)kLogRounds, max((int64_t)0, nrem)) * per_round;
+        const RotLog *src = rlog + first_round * per_round;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst + i);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(src + i));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + i));
         }
         asm volatile("cp.async.commit_group;");
     };
@@ -269,28 +436,25 @@ __global__ void k_apply_log(int p, const double *__restrict__ tlog, const Ctrl *
             asm volatile("cp.async.wait_group 0;");
         }
         __syncthreads();
-        const double *lg = buf + cur * chunk;
+        const RotLog *lg = buf + cur * chunk;
         const int nr = (int)min((int64_t)kLogRounds, total_rounds - base);
         for (int k = 0; k < nr; k++) {
-            const int rnd = (int)((base + k) % (pe - 1));
-            const int q = threadIdx.x;
-            if (q < npairs) {
-                int a, b;
-                rr_pair(pe, rnd, q, a, b);
-                const double t = lg[k * npairs + q];
-                if (b < p && t != 0.0) {
+            for (int q = threadIdx.x; q < per_round; q += blockDim.x) {
+                const RotLog e = lg[k * per_round + q];
+                if (e.t != 0.0) {
                     double c, s;
-                    rot_cs(t, c, s);
+                    rot_cs(e.t, c, s);
                     for (int i = 0; i < R; i++) {
                         double *row = rows + i * p;
-                        const double x = row[a], y = row[b];
-                        row[a] = c * x - s * y;
-                        row[b] = s * x + c * y;
+                        const double x = row[e.a], y = row[e.b];
+                        row[e.a] = c * x - s * y;
+                        row[e.b] = s * x + c * y;
                     }
                 }
             }
             __syncthreads();
         }
+        __syncthreads();
         cur ^= 1;
     }
     for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
@@ -487,9 +651,53 @@ __global__ void __launch_bounds__(256) k_recombine(int64_t N, int t, int k, cons
 
 }  // namespace
 
+namespace {
+// cluster size and half-block width for p columns (0 if W does not fit)
+void jacobi_geometry(int p, int &C, int &h) {
+    // <= 20 pairs (one warp each) per CTA, W half-blocks resident in shared memory
+    const int pe = p + (p & 1);
+    for (C = 1; C <= 16; C <<= 1) {
+        h = (pe + 2 * C - 1) / (2 * C);
+        if (h <= kJThreads / 32 && (size_t)2 * h * p * 8 <= 210 * 1024 && h * p <= kExR * kJThreads &&
+            p <= 32 * kMaxRPL)
+            return;
+    }
+    C = 0;
+    h = 0;
+}
+}  // namespace
+
+template <int R>
+cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *rlog, Ctrl *ctrl, const int *abort,
+                          double ctol, cudaStream_t s) {
+    if (C == 1) {
+        cudaFuncSetAttribute(k_jacobi_block<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol);
+        return cudaGetLastError();
+    }
+    cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (C > 8) cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kJThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort, ctol);
+}
+
 size_t small_svd_log_doubles(int p) {
-    const int64_t pe = p + (p & 1);
-    return (size_t)(50 * (pe - 1) * (pe / 2));
+    int C, h;
+    jacobi_geometry(p, C, h);
+    if (!C) return 1;
+    const int64_t per_sweep = (int64_t)(2 * C - 1) * (2 * h - 1) * C * h;
+    return (size_t)(50 * per_sweep * (sizeof(RotLog) / sizeof(double)));
 }
 
 void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double *Uh, double *Sh, double *Vh,
@@ -498,41 +706,34 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
     count_launch();
     const double ctol = 2.0 * (double)p * 2.220446049250313e-16;  // reading Q10a
     bool done = false;
-    if (tlog) {
-        // smallest cluster whose shared memory holds W
-        int C = 1;
-        while (C <= 16 && (size_t)((p + C - 1) / C) * p * 8 > 200 * 1024) C <<= 1;
-        if (C <= 16) {
-            const int ncc = (p + C - 1) / C;
-            const size_t smem = (size_t)ncc * p * 8;
-            cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            if (C > 8) cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(C);
-            cfg.blockDim = dim3(1024);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = s;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = C;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            if (cudaLaunchKernelEx(&cfg, k_jacobi_cluster, p, ncc, (const double *)W, W, tlog, 50, ctrl, abort, ctol) ==
-                cudaSuccess) {
-                count_launch();
-                const int pe = p + (p & 1), npairs = pe / 2;
-                const int R = 4;
-                const int threads = std::max(32, ((npairs + 31) / 32) * 32);
-                const size_t smem2 = ((size_t)R * p + 2 * (size_t)kLogRounds * npairs) * 8;
-                cudaFuncSetAttribute(k_apply_log, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-                k_apply_log<<<(p + R - 1) / R, threads, smem2, s>>>(p, tlog, ctrl, Vw, R, abort);
-                count_launch();
-                done = true;
-            } else {
-                cudaGetLastError();  // clear and fall back
-            }
+    int C, h;
+    jacobi_geometry(p, C, h);
+    if (tlog && C) {
+        RotLog *rlog = reinterpret_cast<RotLog *>(tlog);
+        const size_t smem = (size_t)2 * h * p * 8;
+        cudaError_t e;
+        const int rpl = (p + 31) / 32;
+        e = rpl <= 1 ? launch_jacobi<1>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 2 ? launch_jacobi<2>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 4 ? launch_jacobi<4>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 6 ? launch_jacobi<6>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 8 ? launch_jacobi<8>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 12 ? launch_jacobi<12>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 16 ? launch_jacobi<16>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+                      : launch_jacobi<20>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s);
+        if (e == cudaSuccess) {
+            count_launch();
+            const int per_round = C * h;
+            const int rps = (2 * C - 1) * (2 * h - 1);
+            const int R = 4;
+            const int threads = std::min(1024, std::max(32, ((per_round + 31) / 32) * 32));
+            const size_t smem2 = (size_t)R * p * 8 + 2 * (size_t)kLogRounds * per_round * sizeof(RotLog);
+            cudaFuncSetAttribute(k_apply_log, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            k_apply_log<<<(p + R - 1) / R, threads, smem2, s>>>(p, per_round, rps, rlog, ctrl, Vw, R, abort);
+            count_launch();
+            done = true;
+        } else {
+            cudaGetLastError();  // clear and fall back
         }
     }
     if (!done) {
