@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -328,6 +329,319 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     for (int i = tid; i < nr; i += blockDim.x) a.w[r0 + i] = wv[i] / beta;
 }
 
+// ---------------------------------------------------------------------------
+// Streaming variant for tall bases (Q does not fit on chip): each CTA owns a
+// contiguous range of rows and streams it through shared memory in row tiles
+// of RT rows x ncols, loaded with cp.async (16-byte chunks, double-buffered,
+// zero-filled tails) into an XOR-swizzled layout so that both access patterns
+// -- lane per row (row updates) and thread per column (column dots) -- are
+// bank-conflict free.  Three sweeps over Q (the CGS2 minimum), one grid
+// barrier pair per global reduction.
+struct SArgs {
+    int64_t N;
+    int ncols;
+    const double *Q;
+    int64_t ldq;
+    double *w;
+    double *partial;
+    int PS;
+    double *h1, *h2, *h3;
+    unsigned int *bar;
+    Ctrl *ctrl;
+    double *t_entry;
+    int check;
+    const double *pre_h;
+    int64_t rpb;  // rows per CTA, multiple of RT
+};
+
+template <int RT>
+struct Tiles {
+    static constexpr int kCh = RT / 2;  // 16-byte chunks per column per tile
+    __device__ static __forceinline__ int swz(int j, int c) { return j * RT + ((c ^ (j & (kCh - 1))) << 1); }
+};
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, int bytes) {
+    const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kSThr = 512;  // threads per CTA of the streaming kernel
+
+// issue the loads of one row tile (Q rows [r, r+nr) of all columns, and w rows).
+// Thread t always moves chunk c = t % kCh of columns j = t / kCh + u (kSThr/kCh),
+// so addresses advance by constant strides (no per-chunk index arithmetic).
+template <int RT>
+__device__ __forceinline__ void issue_tile(const SArgs &a, double *buf, double *wt, int64_t r, int nr) {
+    constexpr int kCh = RT / 2;
+    constexpr int CPI = kSThr / kCh;  // columns per iteration
+    const int c = threadIdx.x % kCh, j0 = threadIdx.x / kCh;
+    const double *src = a.Q + r + 2 * c + (int64_t)j0 * a.ldq;
+    const int64_t sstep = (int64_t)CPI * a.ldq;
+    double *dst = buf + j0 * RT + ((c ^ (j0 & (kCh - 1))) << 1);  // (j0 + CPI u) & (kCh-1) == j0 & (kCh-1)
+    constexpr int dstep = CPI * RT;
+    if (nr == RT) {
+        for (int j = j0; j < a.ncols; j += CPI, src += sstep, dst += dstep) cp_async16(dst, src, 16);
+    } else {
+        const int bytes = min(16, max(0, (nr - 2 * c) * 8));
+        for (int j = j0; j < a.ncols; j += CPI, src += sstep, dst += dstep) cp_async16(dst, bytes ? src : a.Q, bytes);
+    }
+    if (threadIdx.x < kCh) {
+        const int bytes = min(16, max(0, (nr - 2 * c) * 8));
+        cp_async16(wt + 2 * c, bytes ? a.w + r + 2 * c : a.w, bytes);
+    }
+    cp_commit();
+}
+
+// per-row s = sum_j T(rr, j) h[j] for the RT rows of a tile: threads as (row,
+// part), P = kSThr/RT parts (a warp = one part, consecutive rows); returns (on
+// threads < RT) the full sum, parts added in fixed order.
+template <int RT>
+__device__ __forceinline__ double tile_rowdot(const double *T, const double *hs, int ncols, double *red) {
+    constexpr int P = kSThr / RT, kCh = RT / 2;
+    const int rr = threadIdx.x % RT, part = threadIdx.x / RT;
+    const int c = rr >> 1, o = rr & 1;
+    // the swizzle of column j depends on j & (kCh-1); with stride P it cycles with period kCh/gcd
+    double s0 = 0.0, s1 = 0.0;
+    int j = part;
+    const double *tp = T + o;
+    for (; j + P < ncols; j += 2 * P) {
+        const int j1 = j + P;
+        s0 = fma(tp[j * RT + ((c ^ (j & (kCh - 1))) << 1)], hs[j], s0);
+        s1 = fma(tp[j1 * RT + ((c ^ (j1 & (kCh - 1))) << 1)], hs[j1], s1);
+    }
+    if (j < ncols) s0 = fma(tp[j * RT + ((c ^ (j & (kCh - 1))) << 1)], hs[j], s0);
+    red[part * RT + rr] = s0 + s1;
+    __syncthreads();
+    double tot = 0.0;
+    if (threadIdx.x < RT)
+        for (int q = 0; q < P; q++) tot += red[q * RT + threadIdx.x];
+    return tot;
+}
+
+// acc[q] += sum_rr T(rr, j) x[rr] for columns j = tid + kSThr q
+template <int RT>
+__device__ __forceinline__ void tile_coldot(const double *T, const double *x, int ncols, double (&acc)[2]) {
+    constexpr int kCh = RT / 2;
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        const int j = threadIdx.x + kSThr * q;
+        if (j < ncols) {
+            const double *tj = T + j * RT;
+            const int sw = j & (kCh - 1);
+            double s0 = acc[q], s1 = 0.0;
+#pragma unroll
+            for (int c = 0; c < kCh; c++) {
+                const double2 v = *reinterpret_cast<const double2 *>(tj + ((c ^ sw) << 1));
+                s0 = fma(v.x, x[2 * c], s0);
+                s1 = fma(v.y, x[2 * c + 1], s1);
+            }
+            acc[q] = s0 + s1;
+        }
+    }
+}
+
+__device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double *sh) {
+    const int nb = gridDim.x;
+    for (int j = blockIdx.x; j < ncols_tot; j += nb) {
+        double s = 0.0;
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
+        s = block_sum_all(s, sh);
+        if (threadIdx.x == 0) out[j] = s;
+    }
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
+    if (*(volatile int *)&a.ctrl->abort) return;
+    extern __shared__ __align__(16) double smem_s[];
+    __shared__ double sh[32];
+    const int tid = threadIdx.x;
+    const int ncols = a.ncols;
+    const int tile_d = ncols * RT;
+    double *buf = smem_s;                    // 2 x ncols x RT (swizzled)
+    double *wt = buf + 2 * tile_d;           // 2 x RT
+    double *hs = wt + 2 * RT;                // ncols + 2
+    double *red = hs + ncols + 2;            // kSThr
+    double *wpt = red + kSThr;               // RT
+    const int64_t rb = (int64_t)blockIdx.x * a.rpb;
+    const int64_t re = min(a.N, rb + a.rpb);
+    const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
+
+    // generic tile loop: body(k, T, W) on tile k (rows rb + k RT ...)
+    auto run_tiles = [&](auto &&body) {
+        if (ntiles == 0) return;
+        issue_tile<RT>(a, buf, wt, rb, (int)min((int64_t)RT, re - rb));
+        for (int k = 0; k < ntiles; k++) {
+            if (k + 1 < ntiles) {
+                const int64_t r1 = rb + (int64_t)(k + 1) * RT;
+                issue_tile<RT>(a, buf + ((k + 1) & 1) * tile_d, wt + ((k + 1) & 1) * RT, r1,
+                               (int)min((int64_t)RT, re - r1));
+                cp_wait<1>();
+            } else {
+                cp_wait<0>();
+            }
+            __syncthreads();
+            body(k, buf + (k & 1) * tile_d, wt + (k & 1) * RT);
+            __syncthreads();
+        }
+    };
+
+    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7)), an extra sweep (once per pass)
+        for (int j = tid; j < ncols; j += blockDim.x) hs[j] = a.pre_h[j];
+        __syncthreads();
+        run_tiles([&](int k, const double *T, const double *W) {
+            const double s = tile_rowdot<RT>(T, hs, ncols, red);
+            const int64_t r = rb + (int64_t)k * RT + tid;
+            if (tid < RT && r < re) a.w[r] = W[tid] - s;
+        });
+        grid_barrier(a.bar);  // make the updated w visible to the cp.async reads below
+    }
+
+    double nrm_wp = 0.0;
+    if (ncols > 0) {
+        // phase A: partial h1 = Q_b^T w_b
+        double acc[2] = {0.0, 0.0};
+        run_tiles([&](int, const double *T, const double *W) { tile_coldot<RT>(T, W, ncols, acc); });
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const int j = tid + kSThr * q;
+            if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc[q];
+        }
+        grid_barrier(a.bar);
+        sreduce_cols(a, ncols, a.h1, sh);
+        grid_barrier(a.bar);
+        for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
+        __syncthreads();
+        // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
+        double acc2[2] = {0.0, 0.0};
+        run_tiles([&](int k, const double *T, const double *W) {
+            const double s = tile_rowdot<RT>(T, hs, ncols, red);
+            const int64_t r = rb + (int64_t)k * RT + tid;
+            if (tid < RT) {
+                double v = 0.0;
+                if (r < re) {
+                    v = W[tid] - s;
+                    a.w[r] = v;
+                    nrm_wp = fma(v, v, nrm_wp);
+                }
+                wpt[tid] = v;
+            }
+            __syncthreads();
+            tile_coldot<RT>(T, wpt, ncols, acc2);
+        });
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const int j = tid + kSThr * q;
+            if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc2[q];
+        }
+    } else {
+        run_tiles([&](int k, const double *, const double *W) {
+            const int64_t r = rb + (int64_t)k * RT + tid;
+            if (tid < RT && r < re) nrm_wp = fma(W[tid], W[tid], nrm_wp);
+        });
+    }
+    {
+        const double bn = block_sum_all(nrm_wp, sh);
+        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+    }
+    grid_barrier(a.bar);
+    sreduce_cols(a, ncols + 1, a.h2, sh);
+    grid_barrier(a.bar);
+    for (int j = tid; j <= ncols; j += blockDim.x) hs[j] = __ldcg(a.h2 + j);
+    __syncthreads();
+
+    // phase C: w'' = w' - Q h2, beta, breakdown, normalize
+    const double nrmp = hs[ncols];
+    double hh = 0.0;
+    for (int j = tid; j < ncols; j += blockDim.x) hh = fma(hs[j], hs[j], hh);
+    hh = block_sum_all(hh, sh);
+    double beta2 = nrmp - hh;
+    const bool pyth = beta2 > 0.5 * nrmp;
+    const double amax = a.ctrl->amax[a.check & 1];
+    const double thr = 1e-14 * fmax(amax, 1.0);
+    bool bd = false;
+    double beta = 0.0;
+    if (pyth) {
+        beta = sqrt(beta2);
+        bd = !(beta > thr);
+        if (!bd && ncols > 0) {
+            run_tiles([&](int k, const double *T, const double *W) {
+                const double s = tile_rowdot<RT>(T, hs, ncols, red);
+                const int64_t r = rb + (int64_t)k * RT + tid;
+                if (tid < RT && r < re) a.w[r] = (W[tid] - s) / beta;
+            });
+        } else if (!bd) {
+            for (int64_t r = rb + tid; r < re; r += blockDim.x) a.w[r] = a.w[r] / beta;
+        }
+    } else {
+        double nrm2 = 0.0;
+        if (ncols > 0) {
+            run_tiles([&](int k, const double *T, const double *W) {
+                const double s = tile_rowdot<RT>(T, hs, ncols, red);
+                const int64_t r = rb + (int64_t)k * RT + tid;
+                if (tid < RT && r < re) {
+                    const double v = W[tid] - s;
+                    a.w[r] = v;
+                    nrm2 = fma(v, v, nrm2);
+                }
+            });
+        } else {
+            for (int64_t r = rb + tid; r < re; r += blockDim.x) nrm2 = fma(a.w[r], a.w[r], nrm2);
+        }
+        const double bn = block_sum_all(nrm2, sh);
+        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
+        grid_barrier(a.bar);
+        sreduce_cols(a, 1, a.h3, sh);
+        grid_barrier(a.bar);
+        beta = sqrt(fmax(__ldcg(a.h3), 0.0));
+        bd = !(beta > thr);
+        if (!bd)
+            for (int64_t r = rb + tid; r < re; r += blockDim.x) a.w[r] = a.w[r] / beta;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        if (bd) {
+            *a.t_entry = 0.0;
+            a.ctrl->amax[(a.check + 1) & 1] = amax;
+            a.ctrl->abort_check = a.check;
+            __threadfence();
+            a.ctrl->abort = 1;
+        } else {
+            *a.t_entry = beta;
+            a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
+        }
+    }
+}
+
+template <int RT>
+bool launch_stream(const SArgs &a0, int nsm, cudaStream_t s) {
+    SArgs a = a0;
+    const size_t smem = ((size_t)2 * a.ncols * RT + 2 * RT + a.ncols + 2 + kSThr + RT) * sizeof(double);
+    if (smem > 220 * 1024) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cgs2_stream<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_stream<RT>, kSThr, smem);
+    if (bps < 1) return false;
+    const int nb = nsm;  // one CTA per SM (the tile buffers fill shared memory)
+    int64_t rpb = (a.N + nb - 1) / nb;
+    rpb = (rpb + RT - 1) / RT * RT;
+    a.rpb = rpb;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
+    void *args[] = {&a};
+    if (cudaLaunchCooperativeKernel((void *)k_cgs2_stream<RT>, grid, kSThr, args, smem, s) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    count_launch();
+    return true;
+}
+
 }  // namespace
 
 // returns false if the fused path cannot be used (caller falls back)
@@ -351,8 +665,10 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     a.t_entry = t_entry;
     a.check = check;
     a.pre_h = pre_h;
-    // try Q-resident mode: 2 CTAs per SM, then 1
-    for (int per_sm = 2; per_sm >= 1; per_sm--) {
+    // try Q-resident mode: 2 CTAs per SM, then 1 (SVDSC_FORCE_STREAM=1 skips it: test hook)
+    const char *fse = getenv("SVDSC_FORCE_STREAM");
+    const bool force_stream = fse && fse[0] == '1';
+    for (int per_sm = 2; per_sm >= 1 && !force_stream; per_sm--) {
         const int nb = nsm * per_sm;
         const int64_t rpb = (N + nb - 1) / nb;
         const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1)) * sizeof(double);
@@ -376,38 +692,30 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             return true;
         }
     }
-    // streaming mode
-    int RT = 64;
-    while (RT > 8 && (size_t)ncols * (RT + 1) * 8 > 80 * 1024) RT >>= 1;
-    const int per_sm = 2;
-    const int nb = nsm * per_sm;
-    int64_t rpb = (N + nb - 1) / nb;
-    const int wsmem = rpb <= 2048 ? 1 : 0;
-    const size_t smem = ((size_t)ncols + 2 + (wsmem ? rpb : 0) + (size_t)ncols * (RT + 1) + 256 + RT) * sizeof(double);
-    if (smem > smem_cap || ncols > 1024) return false;
-    a.rpb = (int)rpb;
-    a.RT = RT;
-    a.wsmem = wsmem;
-    static bool attr2 = false;
-    if (!attr2) {
-        cudaFuncSetAttribute(k_cgs2_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr2 = true;
-    }
-    int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_fused<false>, kThreads, smem);
-    if (bps < 1) return false;
-    const int grid = (int)std::min<int64_t>((int64_t)nsm * std::min(bps, per_sm), (N + rpb - 1) / rpb);
-    if ((int64_t)grid * rpb < N) {
-        // fewer CTAs than planned: recompute rows per CTA
-        rpb = (N + grid - 1) / grid;
-        a.rpb = (int)rpb;
-        a.wsmem = 0;
-    }
-    void *args[] = {&a};
-    if (cudaLaunchCooperativeKernel((void *)k_cgs2_fused<false>, grid, kThreads, args, smem, s) != cudaSuccess)
-        return false;
-    count_launch();
-    return true;
+    // streaming mode (tall bases): cp.async row tiles through shared memory
+    const bool aligned = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    if (!aligned || ncols > 1024) return false;
+    SArgs sa{};
+    sa.N = N;
+    sa.ncols = ncols;
+    sa.Q = Q;
+    sa.ldq = ldq;
+    sa.w = w;
+    sa.partial = fs.partial;
+    sa.PS = ncols + 2;
+    sa.h1 = fs.h1;
+    sa.h2 = fs.h2;
+    sa.h3 = fs.h3;
+    sa.bar = fs.bar;
+    sa.ctrl = ctrl;
+    sa.t_entry = t_entry;
+    sa.check = check;
+    sa.pre_h = pre_h;
+    if (ncols * 32 * 16 <= 190 * 1024 && launch_stream<32>(sa, nsm, s)) return true;
+    if (ncols * 16 * 16 <= 190 * 1024 && launch_stream<16>(sa, nsm, s)) return true;
+    if (launch_stream<8>(sa, nsm, s)) return true;
+    return false;
 }
 
 }  // namespace svdsc

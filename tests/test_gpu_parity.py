@@ -233,11 +233,15 @@ def _e2e(S, H, wl, fixed=True, **kw):
     return r, r_or, U, V, s
 
 
-@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("mode", ["fused", "stream", "split"])
 @pytest.mark.parametrize("cid,scale", [(1, 1), (2, 4), (3, 20)])
-def test_svds_parity(S, H, cid, scale, fused, monkeypatch):
-    if not fused:
+def test_svds_parity(S, H, cid, scale, mode, monkeypatch):
+    if mode == "split":
         monkeypatch.setenv("SVDSC_NO_FUSED", "1")
+    if mode == "stream":
+        if cid == 1:
+            pytest.skip("covered by the other configs")
+        monkeypatch.setenv("SVDSC_FORCE_STREAM", "1")
     wl = W.config(cid, scale=scale)
     r, r_or, U, V, s = _e2e(S, H, wl)
     k = wl.k
