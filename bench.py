@@ -241,6 +241,15 @@ def main():
     bytes_per_launch = Al.bytes_one_pass() if Al.kind == "dense" else (
         12 * Al.nnz + 4 * (Al.m + 1) if fam == "Av" else 12 * Al.nnz + 4 * (Al.n + 1))
     f_ms, f_calls = prof[fam]
+    traffic = None
+    try:  # DRAM bytes per launch of this kernel from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        kname = ("k_gemv_t" if fam == "ATu" else "k_gemv_n") if Al.kind == "dense" else None
+        if kname in tj and tj[kname].get("workload") == wl_full.name:
+            traffic = tj[kname]["bytes_per_launch"]
+    except Exception:
+        traffic = None
     achieved = bytes_per_launch / (f_ms / f_calls / 1e3) / 1e9 if f_calls else None
     step_bytes = res.info["bytes_model"] / max(res.info["steps"], 1)
     total_prof = sum(v[0] for v in prof.values())
@@ -299,7 +308,7 @@ def main():
                        "step_bytes_model": step_bytes},
             "roofline": {"bound": "hbm", "kernel": f"{fam} product ({'gemv' if A.kind == 'dense' else 'spmv'})",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "bytes_per_launch": bytes_per_launch, "avg_launch_us": 1e3 * f_ms / max(f_calls, 1),
                          "share_of_step": f_ms / ms if ms else None, "peak_source": peak_src},
             "breakdown_ms": {f: round(v[0], 3) for f, v in prof.items() if v[1]},
