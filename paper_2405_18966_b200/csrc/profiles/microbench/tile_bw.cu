@@ -1,0 +1,119 @@
+// Microbenchmark: achievable HBM read bandwidth when a column-major N x C
+// matrix (ld = N) is streamed in row tiles of RT rows x C columns with
+// cp.async 16-byte copies into shared memory (NS stages), one CTA per SM,
+// each CTA owning a contiguous row range -- the access pattern of the CGS2
+// streaming kernel.  Also: plain coalesced double2 loads (no smem) per column
+// segment, and a contiguous copy reference.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(src) : "memory");
+}
+
+template <int RT, int NS>
+__global__ void __launch_bounds__(512) k_tiles(const double *Q, int64_t N, int C, int64_t rpb, double *sink) {
+    extern __shared__ __align__(16) double sm[];
+    const int64_t rb = blockIdx.x * rpb, re = min(N, rb + rpb);
+    const int ntiles = (int)((re - rb) / RT);
+    constexpr int kCh = RT / 2;
+    const int tile_d = C * RT;
+    auto issue = [&](int k) {
+        const int64_t r = rb + (int64_t)k * RT;
+        double *buf = sm + (k % NS) * tile_d;
+        for (int idx = threadIdx.x; idx < C * kCh; idx += blockDim.x) {
+            const int j = idx / kCh, c = idx % kCh;
+            cp16(buf + j * RT + 2 * c, Q + r + 2 * c + (int64_t)j * N);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc = 0.0;
+    for (int p = 0; p < NS - 1; p++) {
+        if (p < ntiles) issue(p); else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int k = 0; k < ntiles; k++) {
+        if (k + NS - 1 < ntiles) issue(k + NS - 1); else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
+        __syncthreads();
+        acc += sm[(k % NS) * tile_d + threadIdx.x % tile_d];
+        __syncthreads();
+    }
+    if (acc == 123.456) sink[0] = acc;
+}
+
+// direct loads: thread handles rows (2 per lane via double2), loops columns, unroll U
+template <int U>
+__global__ void __launch_bounds__(512) k_direct(const double *Q, int64_t N, int C, int64_t rpb, double *sink) {
+    const int64_t rb = blockIdx.x * rpb, re = min(N, rb + rpb);
+    double acc = 0.0;
+    for (int64_t r = rb + 2 * threadIdx.x; r + 1 < re; r += 2 * blockDim.x) {
+        int j = 0;
+        for (; j + U <= C; j += U) {
+            double2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) v[u] = __ldcs(reinterpret_cast<const double2 *>(Q + r + (int64_t)(j + u) * N));
+#pragma unroll
+            for (int u = 0; u < U; u++) acc += v[u].x + v[u].y;
+        }
+    }
+    if (acc == 123.456) sink[0] = acc;
+}
+
+__global__ void k_copyref(const double2 *a, int64_t n, double *sink) {
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 v = __ldcs(a + i);
+        acc += v.x + v.y;
+    }
+    if (acc == 123.456) sink[0] = acc;
+}
+
+int main() {
+    int nsm;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t N = 200000 * 4;  // tall basis
+    const int C = 250;
+    double *Q, *sink;
+    cudaMalloc(&Q, (size_t)N * C * 8);
+    cudaMalloc(&sink, 8);
+    cudaMemset(Q, 0, (size_t)N * C * 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double bytes = (double)N * C * 8;
+    auto timeit = [&](const char *name, auto launch) {
+        launch();
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0);
+        for (int i = 0; i < 5; i++) launch();
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("%-28s %8.1f GB/s  (%s)\n", name, bytes * 5 / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    };
+    timeit("copyref double2", [&] { k_copyref<<<nsm * 8, 512>>>((const double2 *)Q, N * C / 2, sink); });
+#define TILES(RT, NS)                                                                                   \
+    {                                                                                                  \
+        int64_t rpb = ((N + nsm - 1) / nsm + RT - 1) / RT * RT;                                        \
+        size_t smem = (size_t)NS * C * RT * 8;                                                         \
+        if (smem <= 220 * 1024) {                                                                      \
+            cudaFuncSetAttribute(k_tiles<RT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
+            char nm[64];                                                                               \
+            snprintf(nm, 64, "tiles RT=%d NS=%d", RT, NS);                                             \
+            timeit(nm, [&] { k_tiles<RT, NS><<<nsm, 512, smem>>>(Q, N, C, rpb, sink); });              \
+        }                                                                                              \
+    }
+    TILES(32, 2) TILES(32, 3) TILES(16, 4) TILES(16, 6) TILES(8, 8) TILES(64, 1)
+#define DIRECT(U, G)                                                                          \
+    {                                                                                         \
+        int64_t rpb = ((N + nsm * G - 1) / (nsm * G) + 1) / 2 * 2;                            \
+        char nm[64];                                                                          \
+        snprintf(nm, 64, "direct U=%d ctas/SM=%d", U, G);                                     \
+        timeit(nm, [&] { k_direct<U><<<nsm * G, 512>>>(Q, N, C, rpb, sink); });               \
+    }
+    DIRECT(8, 1) DIRECT(16, 1) DIRECT(8, 2) DIRECT(16, 2) DIRECT(8, 4)
+    return 0;
+}
