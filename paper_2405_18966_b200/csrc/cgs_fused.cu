@@ -368,12 +368,11 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kSThr = 512;  // threads per CTA of the streaming kernel
 
 // issue the loads of one row tile (Q rows [r, r+nr) of all columns, and w rows).
 // Thread t always moves chunk c = t % kCh of columns j = t / kCh + u (kSThr/kCh),
 // so addresses advance by constant strides (no per-chunk index arithmetic).
-template <int RT>
+template <int RT, int kSThr>
 __device__ __forceinline__ void issue_tile(const SArgs &a, double *buf, double *wt, int64_t r, int nr) {
     constexpr int kCh = RT / 2;
     constexpr int CPI = kSThr / kCh;  // columns per iteration
@@ -398,7 +397,7 @@ __device__ __forceinline__ void issue_tile(const SArgs &a, double *buf, double *
 // per-row s = sum_j T(rr, j) h[j] for the RT rows of a tile: threads as (row,
 // part), P = kSThr/RT parts (a warp = one part, consecutive rows); returns (on
 // threads < RT) the full sum, parts added in fixed order.
-template <int RT>
+template <int RT, int kSThr>
 __device__ __forceinline__ double tile_rowdot(const double *T, const double *hs, int ncols, double *red) {
     constexpr int P = kSThr / RT, kCh = RT / 2;
     const int rr = threadIdx.x % RT, part = threadIdx.x / RT;
@@ -422,11 +421,11 @@ __device__ __forceinline__ double tile_rowdot(const double *T, const double *hs,
 }
 
 // acc[q] += sum_rr T(rr, j) x[rr] for columns j = tid + kSThr q
-template <int RT>
-__device__ __forceinline__ void tile_coldot(const double *T, const double *x, int ncols, double (&acc)[2]) {
+template <int RT, int kSThr, int NQ>
+__device__ __forceinline__ void tile_coldot(const double *T, const double *x, int ncols, double (&acc)[NQ]) {
     constexpr int kCh = RT / 2;
 #pragma unroll
-    for (int q = 0; q < 2; q++) {
+    for (int q = 0; q < NQ; q++) {
         const int j = threadIdx.x + kSThr * q;
         if (j < ncols) {
             const double *tj = T + j * RT;
@@ -453,47 +452,60 @@ __device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double 
     }
 }
 
-template <int RT>
+template <int RT, int kSThr, int NS>
 __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
+    constexpr int NQ = 1024 / kSThr;  // columns per thread (ncols <= 1024)
     if (*(volatile int *)&a.ctrl->abort) return;
     extern __shared__ __align__(16) double smem_s[];
     __shared__ double sh[32];
     const int tid = threadIdx.x;
     const int ncols = a.ncols;
     const int tile_d = ncols * RT;
-    double *buf = smem_s;                    // 2 x ncols x RT (swizzled)
-    double *wt = buf + 2 * tile_d;           // 2 x RT
-    double *hs = wt + 2 * RT;                // ncols + 2
+    double *buf = smem_s;                    // NS x ncols x RT (swizzled)
+    double *wt = buf + NS * tile_d;          // NS x RT
+    double *hs = wt + NS * RT;               // ncols + 2
     double *red = hs + ncols + 2;            // kSThr
     double *wpt = red + kSThr;               // RT
     const int64_t rb = (int64_t)blockIdx.x * a.rpb;
     const int64_t re = min(a.N, rb + a.rpb);
     const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
 
-    // generic tile loop: body(k, T, W) on tile k (rows rb + k RT ...)
+    // generic tile loop: body(k, T, W) on tile k (rows rb + k RT ...); NS-stage
+    // cp.async ring (NS-1 tiles in flight while one is consumed); one commit
+    // group per iteration (possibly empty) keeps wait_group<NS-1> exact.
     auto run_tiles = [&](auto &&body) {
         if (ntiles == 0) return;
-        issue_tile<RT>(a, buf, wt, rb, (int)min((int64_t)RT, re - rb));
-        for (int k = 0; k < ntiles; k++) {
-            if (k + 1 < ntiles) {
-                const int64_t r1 = rb + (int64_t)(k + 1) * RT;
-                issue_tile<RT>(a, buf + ((k + 1) & 1) * tile_d, wt + ((k + 1) & 1) * RT, r1,
-                               (int)min((int64_t)RT, re - r1));
-                cp_wait<1>();
+#pragma unroll
+        for (int p = 0; p < NS - 1; p++) {
+            if (p < ntiles) {
+                const int64_t r1 = rb + (int64_t)p * RT;
+                issue_tile<RT, kSThr>(a, buf + p * tile_d, wt + p * RT, r1, (int)min((int64_t)RT, re - r1));
             } else {
-                cp_wait<0>();
+                cp_commit();
             }
+        }
+        for (int k = 0; k < ntiles; k++) {
+            const int kn = k + NS - 1;
+            if (kn < ntiles) {
+                const int64_t r1 = rb + (int64_t)kn * RT;
+                issue_tile<RT, kSThr>(a, buf + (kn % NS) * tile_d, wt + (kn % NS) * RT, r1,
+                                      (int)min((int64_t)RT, re - r1));
+            } else {
+                cp_commit();
+            }
+            cp_wait<NS - 1>();
             __syncthreads();
-            body(k, buf + (k & 1) * tile_d, wt + (k & 1) * RT);
+            body(k, buf + (k % NS) * tile_d, wt + (k % NS) * RT);
             __syncthreads();
         }
+        cp_wait<0>();
     };
 
     if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7)), an extra sweep (once per pass)
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = a.pre_h[j];
         __syncthreads();
         run_tiles([&](int k, const double *T, const double *W) {
-            const double s = tile_rowdot<RT>(T, hs, ncols, red);
+            const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
             const int64_t r = rb + (int64_t)k * RT + tid;
             if (tid < RT && r < re) a.w[r] = W[tid] - s;
         });
@@ -503,10 +515,12 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
     double nrm_wp = 0.0;
     if (ncols > 0) {
         // phase A: partial h1 = Q_b^T w_b
-        double acc[2] = {0.0, 0.0};
-        run_tiles([&](int, const double *T, const double *W) { tile_coldot<RT>(T, W, ncols, acc); });
+        double acc[NQ];
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
+        for (int q = 0; q < NQ; q++) acc[q] = 0.0;
+        run_tiles([&](int, const double *T, const double *W) { tile_coldot<RT, kSThr, NQ>(T, W, ncols, acc); });
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
             const int j = tid + kSThr * q;
             if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc[q];
         }
@@ -516,9 +530,11 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
         __syncthreads();
         // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
-        double acc2[2] = {0.0, 0.0};
+        double acc2[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; q++) acc2[q] = 0.0;
         run_tiles([&](int k, const double *T, const double *W) {
-            const double s = tile_rowdot<RT>(T, hs, ncols, red);
+            const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
             const int64_t r = rb + (int64_t)k * RT + tid;
             if (tid < RT) {
                 double v = 0.0;
@@ -530,10 +546,10 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
                 wpt[tid] = v;
             }
             __syncthreads();
-            tile_coldot<RT>(T, wpt, ncols, acc2);
+            tile_coldot<RT, kSThr, NQ>(T, wpt, ncols, acc2);
         });
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
+        for (int q = 0; q < NQ; q++) {
             const int j = tid + kSThr * q;
             if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc2[q];
         }
@@ -569,7 +585,7 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
         bd = !(beta > thr);
         if (!bd && ncols > 0) {
             run_tiles([&](int k, const double *T, const double *W) {
-                const double s = tile_rowdot<RT>(T, hs, ncols, red);
+                const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
                 const int64_t r = rb + (int64_t)k * RT + tid;
                 if (tid < RT && r < re) a.w[r] = (W[tid] - s) / beta;
             });
@@ -580,7 +596,7 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
         double nrm2 = 0.0;
         if (ncols > 0) {
             run_tiles([&](int k, const double *T, const double *W) {
-                const double s = tile_rowdot<RT>(T, hs, ncols, red);
+                const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
                 const int64_t r = rb + (int64_t)k * RT + tid;
                 if (tid < RT && r < re) {
                     const double v = W[tid] - s;
@@ -615,26 +631,26 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
     }
 }
 
-template <int RT>
+template <int RT, int NT, int NS>
 bool launch_stream(const SArgs &a0, int nsm, cudaStream_t s) {
     SArgs a = a0;
-    const size_t smem = ((size_t)2 * a.ncols * RT + 2 * RT + a.ncols + 2 + kSThr + RT) * sizeof(double);
+    const size_t smem = ((size_t)NS * a.ncols * RT + NS * RT + a.ncols + 2 + NT + RT) * sizeof(double);
     if (smem > 220 * 1024) return false;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_cgs2_stream<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_cgs2_stream<RT, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         attr = true;
     }
     int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_stream<RT>, kSThr, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_stream<RT, NT, NS>, NT, smem);
     if (bps < 1) return false;
-    const int nb = nsm;  // one CTA per SM (the tile buffers fill shared memory)
+    const int nb = nsm;
     int64_t rpb = (a.N + nb - 1) / nb;
     rpb = (rpb + RT - 1) / RT * RT;
     a.rpb = rpb;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
     void *args[] = {&a};
-    if (cudaLaunchCooperativeKernel((void *)k_cgs2_stream<RT>, grid, kSThr, args, smem, s) != cudaSuccess) {
+    if (cudaLaunchCooperativeKernel((void *)k_cgs2_stream<RT, NT, NS>, grid, NT, args, smem, s) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
@@ -712,9 +728,15 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     sa.t_entry = t_entry;
     sa.check = check;
     sa.pre_h = pre_h;
-    if (ncols * 32 * 16 <= 190 * 1024 && launch_stream<32>(sa, nsm, s)) return true;
-    if (ncols * 16 * 16 <= 190 * 1024 && launch_stream<16>(sa, nsm, s)) return true;
-    if (launch_stream<8>(sa, nsm, s)) return true;
+    // deepest pipeline that fits: RT = 32 rows with 4, 3, 2 stages, then 16 and 8 rows
+    const char *sv = getenv("SVDSC_STREAM_VARIANT");
+    const int var = sv ? atoi(sv) : 0;
+    if (var == 1 && launch_stream<16, 512, 4>(sa, nsm, s)) return true;
+    if (launch_stream<32, 512, 4>(sa, nsm, s)) return true;
+    if (launch_stream<32, 512, 3>(sa, nsm, s)) return true;
+    if (launch_stream<32, 512, 2>(sa, nsm, s)) return true;
+    if (launch_stream<16, 512, 2>(sa, nsm, s)) return true;
+    if (launch_stream<8, 512, 2>(sa, nsm, s)) return true;
     return false;
 }
 
