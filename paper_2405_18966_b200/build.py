@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
     link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-            "-o", OUT, *objs, "-ldl", "-lpthread"]
+            "-o", OUT, *objs, "-ldl", "-lpthread", "-Xlinker", "--no-undefined"]
     subprocess.check_call(link)
     return OUT
 

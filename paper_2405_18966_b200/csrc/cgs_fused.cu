@@ -16,15 +16,19 @@
 // Reductions over CTAs: partials [block][column], then CTA b reduces columns
 // b, b + nb, ... in a fixed tree order (deterministic), grid barrier, and
 // every CTA reads the reduced vector.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
 
 namespace svdsc {
+unsigned long long *g_ktbuf = nullptr;
 namespace {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -52,18 +56,25 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
     return v;
 }
 
-// sense-free generation barrier over all CTAs of a cooperative launch
-__device__ __forceinline__ void grid_barrier(unsigned int *bar) {
+__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier over all CTAs of a cooperative launch: arrival counter +
+// generation word (flags[0], flags[1]); the last CTA to arrive resets the
+// counter and bumps the generation.  (A flag-per-CTA barrier with all-to-all
+// polling measured slower on B200: L2 polling contention.)
+__device__ __forceinline__ void grid_sync(unsigned int *flags, unsigned int) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned int gen = ld_acquire(bar + 1);
+        const unsigned int gen = ld_acquire(flags + 1);
         __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
+        if (atomicAdd(flags, 1u) == gridDim.x - 1) {
+            flags[0] = 0;
             __threadfence();
-            atomicAdd(bar + 1, 1u);
+            atomicAdd(flags + 1, 1u);
         } else {
-            while (ld_acquire(bar + 1) == gen) __nanosleep(20);
+            while (ld_acquire(flags + 1) == gen) __nanosleep(20);
         }
         __threadfence();
     }
@@ -95,7 +106,8 @@ struct Args {
     double *partial;  // [nb][PS]
     int PS;
     double *h1, *h2, *h3;
-    unsigned int *bar;
+    unsigned int *flags;  // grid-barrier flags (one per CTA)
+    unsigned int epoch;   // base epoch of this launch
     Ctrl *ctrl;
     double *t_entry;
     int check;
@@ -125,6 +137,7 @@ __device__ __forceinline__ double qval(const Args &a, const double *qsh, int ldq
 template <bool QS>
 __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the grid
+    unsigned int nbar = 0;
     extern __shared__ double sm[];
     __shared__ double sh[32];
     __shared__ double sred[8][kTile];
@@ -197,9 +210,9 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
                 __syncthreads();
             }
         }
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, ncols, a.h1, sh);
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
         __syncthreads();
 
@@ -266,9 +279,9 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
         }
         const double bn = block_sum_all(nrm_wp, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, ncols + 1, a.h2, sh);
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j <= ncols; j += blockDim.x) hs[j] = __ldcg(a.h2 + j);
         __syncthreads();
     } else {
@@ -276,9 +289,9 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
         for (int i = tid; i < nr; i += blockDim.x) nrm_wp = fma(wv[i], wv[i], nrm_wp);
         const double bn = block_sum_all(nrm_wp, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, 1, a.h2, sh);
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         if (tid == 0) hs[0] = __ldcg(a.h2);
         __syncthreads();
     }
@@ -305,9 +318,9 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     if (!pyth) {  // explicit norm (uniform branch: every CTA sees the same hs)
         const double bn = block_sum_all(nrm2, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, 1, a.h3, sh);
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         beta2 = __ldcg(a.h3);
     }
     const double beta = sqrt(fmax(beta2, 0.0));
@@ -346,12 +359,14 @@ struct SArgs {
     double *partial;
     int PS;
     double *h1, *h2, *h3;
-    unsigned int *bar;
+    unsigned int *flags;  // grid-barrier flags (one per CTA)
+    unsigned int epoch;   // base epoch of this launch
     Ctrl *ctrl;
     double *t_entry;
     int check;
     const double *pre_h;
     int64_t rpb;  // rows per CTA, multiple of RT
+    unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
 };
 
 template <int RT>
@@ -456,6 +471,7 @@ template <int RT, int kSThr, int NS>
 __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
     constexpr int NQ = 1024 / kSThr;  // columns per thread (ncols <= 1024)
     if (*(volatile int *)&a.ctrl->abort) return;
+    unsigned int nbar = 0;
     extern __shared__ __align__(16) double smem_s[];
     __shared__ double sh[32];
     const int tid = threadIdx.x;
@@ -509,7 +525,7 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
             const int64_t r = rb + (int64_t)k * RT + tid;
             if (tid < RT && r < re) a.w[r] = W[tid] - s;
         });
-        grid_barrier(a.bar);  // make the updated w visible to the cp.async reads below
+        grid_sync(a.flags, a.epoch + (++nbar));  // make the updated w visible to the cp.async reads below
     }
 
     double nrm_wp = 0.0;
@@ -524,9 +540,9 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
             const int j = tid + kSThr * q;
             if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc[q];
         }
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         sreduce_cols(a, ncols, a.h1, sh);
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
         __syncthreads();
         // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
@@ -563,9 +579,9 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
         const double bn = block_sum_all(nrm_wp, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
     }
-    grid_barrier(a.bar);
+    grid_sync(a.flags, a.epoch + (++nbar));
     sreduce_cols(a, ncols + 1, a.h2, sh);
-    grid_barrier(a.bar);
+    grid_sync(a.flags, a.epoch + (++nbar));
     for (int j = tid; j <= ncols; j += blockDim.x) hs[j] = __ldcg(a.h2 + j);
     __syncthreads();
 
@@ -609,9 +625,9 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
         }
         const double bn = block_sum_all(nrm2, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         sreduce_cols(a, 1, a.h3, sh);
-        grid_barrier(a.bar);
+        grid_sync(a.flags, a.epoch + (++nbar));
         beta = sqrt(fmax(__ldcg(a.h3), 0.0));
         bd = !(beta > thr);
         if (!bd)
@@ -629,6 +645,655 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
             a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming CGS2, register-blocked variant: warp w owns rows w, w+16, ... of
+// every row tile, lane q owns columns q, q+32, ..., q+32(M-1).  Column dots
+// (h1, h2) accumulate in registers across all tiles and are combined across
+// warps once per phase; row dots (w', w'') are one warp reduction per row.
+// The tile body has no __syncthreads (only the cp.async ring's two per tile).
+template <int RT, int NS, int M>
+__global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
+    constexpr int kSThr = 512, NW = 16, RPW = RT / NW, kCh = RT / 2;
+    if (*(volatile int *)&a.ctrl->abort) return;
+    unsigned int nbar = 0;
+    extern __shared__ __align__(16) double smem_s[];
+    __shared__ double sh[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int ncols = a.ncols;
+    const int tile_d = ncols * RT;
+    double *buf = smem_s;               // NS x ncols x RT (swizzled)
+    double *wt = buf + NS * tile_d;     // NS x RT
+    double *red = wt + NS * RT;         // NW x ncols (cross-warp column sums)
+    const int64_t rb = (int64_t)blockIdx.x * a.rpb;
+    const int64_t re = min(a.N, rb + a.rpb);
+    const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
+    const int sw = lane & (kCh - 1);  // swizzle term of every column this lane owns
+
+    // prologue: the first NS-1 tiles of a phase (issued early, e.g. before the
+    // grid barrier of the previous reduction, so the ramp-up hides behind it)
+    auto prefetch = [&]() {
+#pragma unroll
+        for (int p = 0; p < NS - 1; p++) {
+            if (p < ntiles) {
+                const int64_t r1 = rb + (int64_t)p * RT;
+                issue_tile<RT, kSThr>(a, buf + p * tile_d, wt + p * RT, r1, (int)min((int64_t)RT, re - r1));
+            } else {
+                cp_commit();
+            }
+        }
+    };
+    bool prefetched = false;
+    auto run_tiles = [&](auto &&body) {
+        if (ntiles == 0) return;
+        if (!prefetched) prefetch();
+        prefetched = false;
+        for (int k = 0; k < ntiles; k++) {
+            const int kn = k + NS - 1;
+            if (kn < ntiles) {
+                const int64_t r1 = rb + (int64_t)kn * RT;
+                issue_tile<RT, kSThr>(a, buf + (kn % NS) * tile_d, wt + (kn % NS) * RT, r1,
+                                      (int)min((int64_t)RT, re - r1));
+            } else {
+                cp_commit();
+            }
+            cp_wait<NS - 1>();
+            __syncthreads();
+            body(k, buf + (k % NS) * tile_d, wt + (k % NS) * RT);
+            __syncthreads();
+        }
+        cp_wait<0>();
+    };
+    // element (row rr, column lane + 32 m) of a tile
+    auto tval = [&](const double *T, int rr, int m) -> double {
+        return T[(lane + 32 * m) * RT + (((rr >> 1) ^ sw) << 1) + (rr & 1)];
+    };
+    // per-row dot with the lane's coefficients hreg; result on every lane
+    auto rowdot = [&](const double *T, int rr, const double (&hreg)[M]) -> double {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; m += 2) {
+            if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
+            if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+        }
+        return warp_sum(s0 + s1);
+    };
+    // cross-warp column sums of acc -> partial[block][j]
+    auto flush_cols = [&](const double (&acc)[M]) {
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int j = lane + 32 * m;
+            if (j < ncols) red[wid * ncols + j] = acc[m];
+        }
+        __syncthreads();
+        for (int j = tid; j < ncols; j += kSThr) {
+            double s = 0.0;
+            for (int w = 0; w < NW; w++) s += red[w * ncols + j];
+            a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
+        }
+        __syncthreads();
+    };
+    auto load_h = [&](const double *h, double (&hreg)[M]) {
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int j = lane + 32 * m;
+            hreg[m] = j < ncols ? __ldcg(h + j) : 0.0;
+        }
+    };
+
+    double hreg[M];
+    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
+        load_h(a.pre_h, hreg);
+        run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const double s = rowdot(T, rr, hreg);
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                if (lane == 0 && r < re) a.w[r] = W[rr] - s;
+            }
+        });
+        grid_sync(a.flags, a.epoch + (++nbar));
+    }
+
+    double nrm_wp = 0.0;
+    if (ncols > 0) {
+        // phase A: partial h1
+        double acc[M];
+#pragma unroll
+        for (int m = 0; m < M; m++) acc[m] = 0.0;
+        run_tiles([&](int, const double *T, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const double x = W[rr];
+#pragma unroll
+                for (int m = 0; m < M; m++)
+                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
+            }
+        });
+        flush_cols(acc);
+        prefetch();  // phase B re-reads the same tiles: start them under the reduction
+        prefetched = true;
+        grid_sync(a.flags, a.epoch + (++nbar));
+        sreduce_cols(a, ncols, a.h1, sh);
+        grid_sync(a.flags, a.epoch + (++nbar));
+        load_h(a.h1, hreg);
+        // phase B: w' = w - Q h1 (written back), partial h2, ||w'||^2
+#pragma unroll
+        for (int m = 0; m < M; m++) acc[m] = 0.0;
+        run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const double s = rowdot(T, rr, hreg);
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                const double v = (r < re) ? W[rr] - s : 0.0;
+                if (lane == 0 && r < re) {
+                    a.w[r] = v;
+                    nrm_wp = fma(v, v, nrm_wp);
+                }
+#pragma unroll
+                for (int m = 0; m < M; m++)
+                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), v, acc[m]);
+            }
+        });
+        flush_cols(acc);
+    } else {
+        run_tiles([&](int k, const double *, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                if (lane == 0 && r < re) nrm_wp = fma(W[rr], W[rr], nrm_wp);
+            }
+        });
+    }
+    {
+        const double bn = block_sum_all(nrm_wp, sh);
+        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+    }
+    if (ncols > 0) {  // phase C reads w' written above by this CTA
+        __threadfence();
+        __syncthreads();
+        prefetch();
+        prefetched = true;
+    }
+    grid_sync(a.flags, a.epoch + (++nbar));
+    sreduce_cols(a, ncols + 1, a.h2, sh);
+    grid_sync(a.flags, a.epoch + (++nbar));
+    load_h(a.h2, hreg);
+    const double nrmp = __ldcg(a.h2 + ncols);
+    double hh = 0.0;
+    for (int j = tid; j < ncols; j += kSThr) {
+        const double x = __ldcg(a.h2 + j);
+        hh = fma(x, x, hh);
+    }
+    hh = block_sum_all(hh, sh);
+    double beta2 = nrmp - hh;
+    const bool pyth = beta2 > 0.5 * nrmp;
+    const double amax = a.ctrl->amax[a.check & 1];
+    const double thr = 1e-14 * fmax(amax, 1.0);
+    bool bd = false;
+    double beta = 0.0;
+    if (pyth) {
+        beta = sqrt(beta2);
+        bd = !(beta > thr);
+        if (!bd && ncols > 0) {
+            run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const double s = rowdot(T, rr, hreg);
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    if (lane == 0 && r < re) a.w[r] = (W[rr] - s) / beta;
+                }
+            });
+        } else if (!bd) {
+            for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+        }
+    } else {
+        double nrm2 = 0.0;
+        if (ncols > 0) {
+            run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const double s = rowdot(T, rr, hreg);
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    if (lane == 0 && r < re) {
+                        const double v = W[rr] - s;
+                        a.w[r] = v;
+                        nrm2 = fma(v, v, nrm2);
+                    }
+                }
+            });
+        } else {
+            for (int64_t r = rb + tid; r < re; r += kSThr) nrm2 = fma(a.w[r], a.w[r], nrm2);
+        }
+        const double bn = block_sum_all(nrm2, sh);
+        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
+        grid_sync(a.flags, a.epoch + (++nbar));
+        sreduce_cols(a, 1, a.h3, sh);
+        grid_sync(a.flags, a.epoch + (++nbar));
+        beta = sqrt(fmax(__ldcg(a.h3), 0.0));
+        bd = !(beta > thr);
+        if (!bd)
+            for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+    }
+    cp_wait<0>();  // a prefetch may be pending if phase C was skipped
+    if (blockIdx.x == 0 && tid == 0) {
+        if (bd) {
+            *a.t_entry = 0.0;
+            a.ctrl->amax[(a.check + 1) & 1] = amax;
+            a.ctrl->abort_check = a.check;
+            __threadfence();
+            a.ctrl->abort = 1;
+        } else {
+            *a.t_entry = beta;
+            a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
+        }
+    }
+}
+
+template <int RT, int NS, int M>
+bool launch_stream2(const SArgs &a0, int nsm, cudaStream_t s) {
+    SArgs a = a0;
+    const size_t smem = ((size_t)NS * a.ncols * RT + NS * RT + 16 * (size_t)a.ncols) * sizeof(double);
+    if (smem > 220 * 1024 || a.ncols > 32 * M) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cgs2_stream2<RT, NS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_stream2<RT, NS, M>, 512, smem);
+    if (bps < 1) return false;
+    const int nb = nsm;
+    int64_t rpb = (a.N + nb - 1) / nb;
+    rpb = (rpb + RT - 1) / RT * RT;
+    a.rpb = rpb;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
+    void *args[] = {&a};
+    if (cudaLaunchCooperativeKernel((void *)k_cgs2_stream2<RT, NS, M>, grid, 512, args, smem, s) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    count_launch();
+    return true;
+}
+
+bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
+    const int nc = a.ncols;
+    if (nc <= 64) return launch_stream2<32, 4, 2>(a, nsm, s);
+    if (nc <= 128) return launch_stream2<32, 4, 4>(a, nsm, s);
+    if (nc <= 192) return launch_stream2<32, 3, 6>(a, nsm, s);
+    if (nc <= 256) return launch_stream2<32, 3, 8>(a, nsm, s);
+    if (nc <= 320) return launch_stream2<32, 2, 10>(a, nsm, s);
+    if (nc <= 384) return launch_stream2<32, 2, 12>(a, nsm, s);
+    if (nc <= 512) return launch_stream2<16, 2, 16>(a, nsm, s);
+    if (nc <= 768) return launch_stream2<16, 2, 24>(a, nsm, s);
+    return launch_stream2<16, 2, 32>(a, nsm, s);
+}
+
+// ---------------------------------------------------------------------------
+// TMA variant (B200-native): each row tile (32 rows x ncols) arrives as
+// 2 x ceil(ncols/16) TMA boxes of 16 rows x 16 columns (SWIZZLE_128B, so the
+// 128-byte column segments land bank-interleaved) plus one bulk copy of the
+// tile's w rows, all completing on one mbarrier per stage.  A single thread
+// issues the copies, so the load/store pipe is left to the compute warps.
+// Rows beyond N are zero-filled by the TMA unit.  Compute layout as in
+// k_cgs2_stream2 (warp per 2 rows of the tile, lane per 32-strided columns).
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int NS, int M>
+__global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtensorMap tq, SArgs a) {
+    constexpr int RT = 32, NW = 16, RPW = 2, kSThr = 544;  // 16 compute warps + 1 TMA producer warp
+    if (*(volatile int *)&a.ctrl->abort) return;
+    unsigned int nbar = 0;
+    extern __shared__ __align__(1024) double smem_raw[];
+    __shared__ __align__(8) uint64_t full[NS];
+    // SWIZZLE_128B addresses are absolute: align the stage buffers to 1024 B
+    double *smem_t = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023) / 8;
+    __shared__ double sh[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool producer = wid == NW;  // issues the TMA copies, computes nothing
+    const int ptid = NW * 32;         // the producer thread
+    const int ncols = a.ncols;
+    const int nbox = (ncols + 15) >> 4;
+    const int stage_d = 2 * nbox * 256;           // doubles per stage (2 row halves x nbox boxes x 2 KB)
+    double *wt = smem_t + NS * stage_d;           // NS x RT
+    const int64_t rb = (int64_t)blockIdx.x * a.rpb;
+    const int64_t re = min(a.N, rb + a.rpb);
+    const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
+    const unsigned tx_bytes = (unsigned)(2 * nbox * 2048 + RT * 8);
+    if (tid == ptid) {
+        for (int q = 0; q < NS; q++) mbar_init(&full[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int g_issue = 0, g_use = 0;  // tiles issued / consumed so far (ring position and parity)
+    auto issue = [&](int k) {    // thread 0 only
+        const int st = g_issue % NS;
+        const int64_t r0 = rb + (int64_t)k * RT;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], tx_bytes);
+        double *dst = smem_t + st * stage_d;
+        for (int h = 0; h < 2; h++)
+            for (int b = 0; b < nbox; b++)
+                tma_load_2d(dst + (h * nbox + b) * 256, &tq, (int)(r0 + 16 * h), 16 * b, &full[st]);
+        bulk_load(wt + st * RT, a.w + r0, RT * 8, &full[st]);
+        g_issue++;
+    };
+    auto prefetch = [&]() {
+        if (tid == ptid)
+            for (int p = 0; p < NS - 1 && p < ntiles; p++) issue(p);
+    };
+    bool prefetched = false;
+    auto run_tiles = [&](auto &&body) {
+        if (ntiles == 0) return;
+        if (!prefetched) prefetch();
+        prefetched = false;
+        for (int k = 0; k < ntiles; k++) {
+            if (tid == ptid && k + NS - 1 < ntiles) issue(k + NS - 1);
+            const int st = g_use % NS;
+            if (!producer) {
+                mbar_wait(&full[st], (unsigned)((g_use / NS) & 1));
+                body(k, smem_t + st * stage_d, wt + st * RT);
+            }
+            __syncthreads();
+            g_use++;
+        }
+    };
+    // element (row rr, column lane + 32 m) of a stage
+    const int qsw = lane & 7;
+    const int lofs = ((lane >> 4) << 8) + ((lane & 15) << 4);
+    auto tval = [&](const double *T, int rr, int m) -> double {
+        const int h = rr >> 4, c = (rr & 15) >> 1, o = rr & 1;
+        return T[(h * nbox << 8) + (m << 9) + lofs + ((c ^ qsw) << 1) + o];
+    };
+    auto rowdot = [&](const double *T, int rr, const double (&hreg)[M]) -> double {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; m += 2) {
+            if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
+            if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+        }
+        return warp_sum(s0 + s1);
+    };
+    // cross-warp column sums -> partial[block][j] (fixed order).  The stage
+    // buffers are idle here (the tile loop ended with a barrier and the next
+    // prefetch is issued after), so they hold the NW x ncols scratch.
+    auto flush_cols = [&](const double (&acc)[M]) {
+        double *redc = smem_t;
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int j = lane + 32 * m;
+            if (j < ncols && !producer) redc[wid * ncols + j] = acc[m];
+        }
+        __syncthreads();
+        for (int j = tid; j < ncols; j += kSThr) {
+            double s = 0.0;
+            for (int w = 0; w < NW; w++) s += redc[w * ncols + j];
+            a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
+        }
+        __syncthreads();
+    };
+    auto load_h = [&](const double *h, double (&hreg)[M]) {
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int j = lane + 32 * m;
+            hreg[m] = j < ncols ? __ldcg(h + j) : 0.0;
+        }
+    };
+
+    long long tk[8];
+    int ntk = 0;
+    auto stamp = [&]() {
+        if (a.tdbg && ntk < 8) tk[ntk++] = clock64();
+    };
+    stamp();
+    double hreg[M];
+    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
+        load_h(a.pre_h, hreg);
+        run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const double s = rowdot(T, rr, hreg);
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                if (lane == 0 && r < re) a.w[r] = W[rr] - s;
+            }
+        });
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        grid_sync(a.flags, a.epoch + (++nbar));
+    }
+
+    double nrm_wp = 0.0;
+    if (ncols > 0) {
+        double acc[M];
+#pragma unroll
+        for (int m = 0; m < M; m++) acc[m] = 0.0;
+        run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                const double x = r < re ? W[rr] : 0.0;
+#pragma unroll
+                for (int m = 0; m < M; m++)
+                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
+            }
+        });
+        flush_cols(acc);
+        stamp();
+        prefetch();
+        prefetched = true;
+        grid_sync(a.flags, a.epoch + (++nbar));
+        sreduce_cols(a, ncols, a.h1, sh);
+        grid_sync(a.flags, a.epoch + (++nbar));
+        load_h(a.h1, hreg);
+        stamp();
+#pragma unroll
+        for (int m = 0; m < M; m++) acc[m] = 0.0;
+        run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const double s = rowdot(T, rr, hreg);
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                const double v = (r < re) ? W[rr] - s : 0.0;
+                if (lane == 0 && r < re) {
+                    a.w[r] = v;
+                    nrm_wp = fma(v, v, nrm_wp);
+                }
+#pragma unroll
+                for (int m = 0; m < M; m++)
+                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), v, acc[m]);
+            }
+        });
+        flush_cols(acc);
+    } else {
+        run_tiles([&](int k, const double *, const double *W) {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = wid + NW * q;
+                const int64_t r = rb + (int64_t)k * RT + rr;
+                if (lane == 0 && r < re) nrm_wp = fma(W[rr], W[rr], nrm_wp);
+            }
+        });
+    }
+    {
+        const double bn = block_sum_all(nrm_wp, sh);
+        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+    }
+    if (ncols > 0) {  // phase C reads w' written above by this CTA (generic -> async proxy)
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncthreads();
+        prefetch();
+        prefetched = true;
+    }
+    stamp();
+    grid_sync(a.flags, a.epoch + (++nbar));
+    sreduce_cols(a, ncols + 1, a.h2, sh);
+    grid_sync(a.flags, a.epoch + (++nbar));
+    load_h(a.h2, hreg);
+    stamp();
+    const double nrmp = __ldcg(a.h2 + ncols);
+    double hh = 0.0;
+    for (int j = tid; j < ncols; j += kSThr) {
+        const double x = __ldcg(a.h2 + j);
+        hh = fma(x, x, hh);
+    }
+    hh = block_sum_all(hh, sh);
+    double beta2 = nrmp - hh;
+    const bool pyth = beta2 > 0.5 * nrmp;
+    const double amax = a.ctrl->amax[a.check & 1];
+    const double thr = 1e-14 * fmax(amax, 1.0);
+    bool bd = false;
+    double beta = 0.0;
+    if (pyth) {
+        beta = sqrt(beta2);
+        bd = !(beta > thr);
+        if (!bd && ncols > 0) {
+            run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const double s = rowdot(T, rr, hreg);
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    if (lane == 0 && r < re) a.w[r] = (W[rr] - s) / beta;
+                }
+            });
+        } else if (!bd) {
+            for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+        }
+    } else {
+        double nrm2 = 0.0;
+        if (ncols > 0) {
+            run_tiles([&](int k, const double *T, const double *W) {
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const double s = rowdot(T, rr, hreg);
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    if (lane == 0 && r < re) {
+                        const double v = W[rr] - s;
+                        a.w[r] = v;
+                        nrm2 = fma(v, v, nrm2);
+                    }
+                }
+            });
+        } else {
+            for (int64_t r = rb + tid; r < re; r += kSThr) nrm2 = fma(a.w[r], a.w[r], nrm2);
+        }
+        const double bn = block_sum_all(nrm2, sh);
+        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
+        grid_sync(a.flags, a.epoch + (++nbar));
+        sreduce_cols(a, 1, a.h3, sh);
+        grid_sync(a.flags, a.epoch + (++nbar));
+        beta = sqrt(fmax(__ldcg(a.h3), 0.0));
+        bd = !(beta > thr);
+        if (!bd)
+            for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+    }
+    stamp();
+    if (a.tdbg && tid == 0 && ntk == 6)
+        for (int q = 1; q < 6; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
+    if (a.tdbg && tid == 0 && ntk == 6) atomicAdd(a.tdbg + 6, 1ull), atomicAdd(a.tdbg + 7, (unsigned long long)ntiles);
+    // drain a prefetch left pending when phase C was skipped (producer thread)
+    while (g_use < g_issue) {
+        const int st = g_use % NS;
+        mbar_wait(&full[st], (unsigned)((g_use / NS) & 1));
+        g_use++;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        if (bd) {
+            *a.t_entry = 0.0;
+            a.ctrl->amax[(a.check + 1) & 1] = amax;
+            a.ctrl->abort_check = a.check;
+            __threadfence();
+            a.ctrl->abort = 1;
+        } else {
+            *a.t_entry = beta;
+            a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
+        }
+    }
+}
+
+template <int NS, int M>
+bool launch_tma(const CUtensorMap &tq, const SArgs &a0, int nsm, cudaStream_t s) {
+    SArgs a = a0;
+    const int nbox = (a.ncols + 15) / 16;
+    const size_t smem = (size_t)NS * 2 * nbox * 2048 + (NS * 32) * sizeof(double) + 1024;
+    if (smem > 220 * 1024 || a.ncols > 32 * M) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cgs2_tma<NS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_tma<NS, M>, 544, smem);
+    if (bps < 1) return false;
+    const int nb = nsm;
+    int64_t rpb = (a.N + nb - 1) / nb;
+    rpb = (rpb + 31) / 32 * 32;
+    a.rpb = rpb;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
+    CUtensorMap map = tq;
+    void *args[] = {&map, &a};
+    if (cudaLaunchCooperativeKernel((void *)k_cgs2_tma<NS, M>, grid, 544, args, smem, s) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    count_launch();
+    return true;
+}
+
+bool launch_tma_any(const CUtensorMap &tq, const SArgs &a, int nsm, cudaStream_t s) {
+    const int nc = a.ncols;
+    if (nc <= 64) return launch_tma<4, 2>(tq, a, nsm, s);
+    if (nc <= 128) return launch_tma<4, 4>(tq, a, nsm, s);
+    if (nc <= 192) return launch_tma<3, 6>(tq, a, nsm, s);
+    if (nc <= 256) return launch_tma<3, 8>(tq, a, nsm, s);
+    if (nc <= 320) return launch_tma<2, 10>(tq, a, nsm, s);
+    if (nc <= 384) return launch_tma<2, 12>(tq, a, nsm, s);
+    return false;  // wider bases: cp.async variants
 }
 
 template <int RT, int NT, int NS>
@@ -660,9 +1325,46 @@ bool launch_stream(const SArgs &a0, int nsm, cudaStream_t s) {
 
 }  // namespace
 
+bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_total, int64_t ld) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+    }
+    if (!encode || (ld % 2) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)ncols_total};
+    cuuint64_t gstride[1] = {(cuuint64_t)ld * 8};
+    cuuint32_t box[2] = {16, 16};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap *>(map128), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                        const_cast<double *>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// debugging aid (SVDSC_KTIMING=1): per-phase cycle counters of the TMA kernel
+void ktiming_dump() {
+    if (!g_ktbuf) return;
+    unsigned long long h[16];
+    cudaMemcpy(h, g_ktbuf, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaMemset(g_ktbuf, 0, sizeof(h));
+    const double n = h[6] ? (double)h[6] : 1.0;
+    fprintf(stderr,
+            "[ktiming] calls(x CTAs)=%llu avg tiles/CTA=%.1f  phaseA=%.0f red1=%.0f phaseB=%.0f red2=%.0f phaseC=%.0f cycles\n",
+            h[6], h[7] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n);
+}
+
 // returns false if the fused path cannot be used (caller falls back)
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
-                const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s) {
+                const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
+                const void *tmap) {
     constexpr int kThreads = 256;
     const size_t smem_cap = 200 * 1024;
     Args a{};
@@ -676,7 +1378,8 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     a.h1 = fs.h1;
     a.h2 = fs.h2;
     a.h3 = fs.h3;
-    a.bar = fs.bar;
+    a.flags = fs.flags;
+    a.epoch = fs.epoch;
     a.ctrl = ctrl;
     a.t_entry = t_entry;
     a.check = check;
@@ -723,14 +1426,27 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     sa.h1 = fs.h1;
     sa.h2 = fs.h2;
     sa.h3 = fs.h3;
-    sa.bar = fs.bar;
+    sa.flags = fs.flags;
+    sa.epoch = fs.epoch;
     sa.ctrl = ctrl;
     sa.t_entry = t_entry;
     sa.check = check;
     sa.pre_h = pre_h;
+    {
+        const char *kt = getenv("SVDSC_KTIMING");
+        if (kt && kt[0] == '1') {
+            if (!g_ktbuf) {
+                cudaMalloc(&g_ktbuf, 16 * sizeof(unsigned long long));
+                cudaMemset(g_ktbuf, 0, 16 * sizeof(unsigned long long));
+            }
+            sa.tdbg = g_ktbuf;
+        }
+    }
     // deepest pipeline that fits: RT = 32 rows with 4, 3, 2 stages, then 16 and 8 rows
     const char *sv = getenv("SVDSC_STREAM_VARIANT");
     const int var = sv ? atoi(sv) : 0;
+    if (var == 0 && tmap && launch_tma_any(*reinterpret_cast<const CUtensorMap *>(tmap), sa, nsm, s)) return true;
+    if ((var == 0 || var == 2) && launch_stream2_any(sa, nsm, s)) return true;
     if (var == 1 && launch_stream<16, 512, 4>(sa, nsm, s)) return true;
     if (launch_stream<32, 512, 4>(sa, nsm, s)) return true;
     if (launch_stream<32, 512, 3>(sa, nsm, s)) return true;

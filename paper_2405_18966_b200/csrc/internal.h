@@ -34,6 +34,7 @@ struct Ctrl {
     double max_resid;
     double svd_tiny;      // p eps ||T||_F: numerically zero column norm (reading Q10b)
     unsigned int cnt[16]; // last-block counters (one per reduction site)
+    unsigned int gflags[kMaxBlocks];  // grid-barrier flags of the fused kernels
 };
 
 // ---- CSR operand (device) prepared by analysis --------------------------------
@@ -108,11 +109,22 @@ void axpy_dev(int64_t N, double *y, const double *c_dev, const double *x, const 
 struct FusedScratch {
     double *partial;      // >= 2*nsm x (ncols+2)
     double *h1, *h2, *h3; // >= ncols+2
-    unsigned int *bar;    // 2 zero-initialized words (grid barrier)
+    unsigned int *flags;  // >= 2*nsm grid-barrier flags, zeroed once per solve
+    unsigned int epoch;   // unique increasing base per launch (multiple of 16)
 };
 // false: the fused path is not applicable (caller uses cgs_p1/p2/p3 + normalize)
+// tmap: optional CUtensorMap (128 B) of Q for the TMA streaming variant
+// (make_basis_tmap), or NULL
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
-                const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s);
+                const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
+                const void *tmap);
+// TMA descriptor of a column-major basis (N rows, ncols_total columns, ld):
+// 16 x 16 boxes, SWIZZLE_128B, zero fill beyond N.  Returns false if the
+// driver entry point is unavailable.
+bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_total, int64_t ld);
+
+
+void ktiming_dump();  // SVDSC_KTIMING=1 debugging aid
 
 // ---- small SVD / restart ---------------------------------------------------------
 // Jacobi SVD of the p x p matrix stored (ld p) in W; outputs Uh, Sh, Vh (ld p),

@@ -364,14 +364,19 @@ struct Solver {
     }
 
     bool fused_ok = true;
+    unsigned int fused_launches = 0;
+    alignas(64) unsigned char tmapU[128], tmapV[128];
+    bool have_tmap = false;
     // re-orthogonalize wv against Q(:, 0:ncols) (optionally after wv -= Q pre_h),
     // then beta = ||wv||, breakdown test, T entry, wv /= beta.
     void orth_norm(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, double *t_entry, int chk,
                    const double *pre_h) {
         if (P == 1 && o->reorth != 0 && fused_ok) {
-            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, &w.ctrl->cnt[14]};
+            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches)};
             H->prof.begin(11, s);
-            const bool ok = cgs2_fused(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s);
+            const void *tm = have_tmap ? (Q == w.U ? (const void *)tmapU : (Q == w.V ? (const void *)tmapV : nullptr))
+                                       : nullptr;
+            const bool ok = cgs2_fused(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s, tm);
             H->prof.end(s);
             if (ok) return;
             fused_ok = false;
@@ -491,6 +496,9 @@ struct Solver {
         {
             const char *e = getenv("SVDSC_NO_FUSED");
             fused_ok = !(e && e[0] == '1');
+            const char *nt = getenv("SVDSC_NO_TMA");
+            have_tmap = !(nt && nt[0] == '1') && make_basis_tmap(tmapU, w.U, m, t + 1, w.ldu) &&
+                        make_basis_tmap(tmapV, w.V, nv, t + 1, w.ldv);
         }
         abort = &w.ctrl->abort;
         bytesA = M->kind == 0 ? 12 * M->nnz + 4 * (m + 1) : 8 * m * n;
@@ -579,6 +587,7 @@ struct Solver {
             ck(cudaStreamSynchronize(s), "sync");
             ck(cudaGetLastError(), "final");
         }
+        if (getenv("SVDSC_KTIMING")) ktiming_dump();
         if (info) {
             info->passes = passes;
             info->restarts = std::max(0, passes - 1);
@@ -986,6 +995,20 @@ svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const doub
         OpScratch sc = op_scratch(h, (int)ncols, 1);
         RedBuf rb{sc.partial, kMaxBlocks, sc.h1, sc.h2, sc.nrm, sc.ctrl->cnt};
         cudaStream_t s = h->stream;
+        const char *fp = getenv("SVDSC_OPCGS_FUSED");  // test hook: run the solver's fused kernel
+        if (fp && fp[0] == '1') {
+            // fused path normalizes w; norm_dev receives the norm (the T entry)
+            alignas(64) unsigned char tm[128];
+            const bool have = (fp[1] == 't') && ncols > 0 && make_basis_tmap(tm, Q, N, ncols, ldq);
+            FusedScratch fs{sc.partial, sc.h1, sc.h2, sc.nrm, sc.ctrl->gflags, 16u};
+            double *tent = sc.nrm + 2;
+            if (!cgs2_fused(N, (int)ncols, Q, ldq, w, nullptr, fs, sc.ctrl, tent, 0, h->nsm, s, have ? tm : nullptr))
+                throw SvdscError(SVDSC_EINVAL, "fused CGS2 path not applicable");
+            if (norm_dev) ck(cudaMemcpyAsync(norm_dev, tent, sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
+            ck(cudaStreamSynchronize(s), "sync");
+            ck(cudaGetLastError(), "cgs2 fused");
+            return;
+        }
         if (ncols > 0) {
             cgs_p1(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
             cgs_p2(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);

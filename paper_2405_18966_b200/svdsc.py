@@ -307,8 +307,10 @@ def matvec(M: Matrix, x, trans=False, c=None, yprev=None):
 
 def cgs2(h: Handle, Q, w):
     """a2-a4/a6: w <- (I - QQ^T)^2 w in place on a copy; returns (w, ||w||)."""
-    w = w.clone()
     N = w.numel()
+    wp = torch.zeros(-(-N // 32) * 32, device=w.device, dtype=torch.float64)  # padded like a basis column
+    wp[:N] = w
+    w = wp[:N]
     ncols = 0 if Q is None else Q.shape[1]
     nrm = torch.empty(1, device=w.device, dtype=torch.float64)
     ldq = _ld(Q) if ncols else N

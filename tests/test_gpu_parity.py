@@ -136,6 +136,35 @@ def test_cgs2(S, H, N, c):
     assert abs(nrm.item() - O.norm2(w_or)) <= 1e-12 * scale
 
 
+@pytest.mark.parametrize("variant", ["qs", "stream", "stream2", "tma"])
+@pytest.mark.parametrize("N,c", [(10007, 37), (200000, 300), (4096, 150), (1250, 64), (333, 5), (4096, 65),
+                                 (4096, 96), (4096, 128), (4096, 129), (65536, 150)])
+def test_cgs2_fused_variants(S, H, N, c, variant, monkeypatch):
+    """The solver's fused CGS2 + normalize kernels (Q-resident, cp.async
+    streaming, register-blocked streaming, TMA streaming) against the oracle."""
+    env = {"qs": ("1", "0", None), "stream": ("1t", "1", "1"), "stream2": ("1t", "1", "2"),
+           "tma": ("1t", "1", "0")}[variant]
+    monkeypatch.setenv("SVDSC_OPCGS_FUSED", env[0])
+    if env[1] == "1":
+        monkeypatch.setenv("SVDSC_FORCE_STREAM", "1")
+    if env[2] is not None:
+        monkeypatch.setenv("SVDSC_STREAM_VARIANT", env[2])
+    rng = np.random.default_rng(N * 7 + c)
+    Q = np.linalg.qr(rng.standard_normal((N, c)))[0]
+    w = rng.standard_normal(N) + Q @ rng.standard_normal(c) * 3
+    ld = -(-N // 32) * 32
+    Qd = torch.zeros((c + 1, ld), dtype=torch.float64, device="cuda")  # column-major, ld % 32 == 0
+    Qd[:c, :N] = dev(np.ascontiguousarray(Q.T))
+    wd = torch.zeros(ld, dtype=torch.float64, device="cuda")
+    wd[:N] = dev(w)
+    Qv = Qd.t()[:N, :c]
+    wg, nrm = S.cgs2(H, Qv, wd[:N])
+    w_or = O.cgs2(Q, w)
+    nor = O.norm2(w_or)
+    assert abs(nrm.item() - nor) <= 1e-12 * np.linalg.norm(w)
+    assert np.abs(wg.cpu().numpy() - w_or / nor).max() <= 1e-12 * np.linalg.norm(w) / nor
+
+
 # ---------------------------------------------------------------- a7
 def _bidiag(rng, p):
     T = np.diag(rng.uniform(0.5, 2, p)) + np.diag(rng.uniform(0.1, 1, p - 1), 1)

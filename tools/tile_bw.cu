@@ -6,6 +6,7 @@
 // segment, and a contiguous copy reference.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ void cp16(void *dst, const void *src) {
@@ -70,11 +71,12 @@ __global__ void k_copyref(const double2 *a, int64_t n, double *sink) {
     if (acc == 123.456) sink[0] = acc;
 }
 
-int main() {
+int main(int argc, char **argv) {
     int nsm;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t N = 200000 * 4;  // tall basis
-    const int C = 250;
+    const int64_t N = argc > 1 ? atoll(argv[1]) : 800000;  // tall basis
+    const int C = argc > 2 ? atoi(argv[2]) : 250;
+    printf("N=%lld C=%d\n", (long long)N, C);
     double *Q, *sink;
     cudaMalloc(&Q, (size_t)N * C * 8);
     cudaMalloc(&sink, 8);
