@@ -938,13 +938,26 @@ bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA variant (B200-native): each row tile (32 rows x ncols) arrives as
-// 2 x ceil(ncols/16) TMA boxes of 16 rows x 16 columns (SWIZZLE_128B, so the
-// 128-byte column segments land bank-interleaved) plus one bulk copy of the
-// tile's w rows, all completing on one mbarrier per stage.  A single thread
-// issues the copies, so the load/store pipe is left to the compute warps.
-// Rows beyond N are zero-filled by the TMA unit.  Compute layout as in
-// k_cgs2_stream2 (warp per 2 rows of the tile, lane per 32-strided columns).
+// TMA variant (B200-native), warp-specialized producer/consumer pipeline.
+//   * A row tile is 32 rows x ncols: ceil(ncols/16) TMA boxes of 32 rows x 16
+//     columns (column-major, no swizzle: a column segment is 256 contiguous
+//     bytes; 16-row segments measured ~10% less HBM bandwidth, tools/tma_bw.cu)
+//     plus one 256-byte bulk copy of the tile's w rows, completing on the
+//     stage's `full` mbarrier.  One producer thread issues the copies; the 16
+//     consumer warps release a stage by arriving on its `empty` mbarrier, so the
+//     producer runs up to ns stages ahead and consumers never wait for each
+//     other to free a buffer.
+//   * Consumer warp w owns columns [w M, w M + M); lane = row of the tile.
+//     Column dots (Q^T w) accumulate per thread over the CTA's rows and are
+//     reduced over the 32 lanes once per sweep.  Row dots (Q h) are per-thread
+//     partials over the warp's columns, combined over the 16 warps through a
+//     double-buffered shared array and ONE named barrier per tile; every warp
+//     then sums the 16 partials of its rows itself (no shuffles per row).
+//   * Phase B keeps the thread's Q values in registers between the row dot
+//     (w' = w - Q h1) and the column dot (Q^T w'): Q is read from shared
+//     memory once per sweep.
+//   * Sweeps alternate direction so that each sweep starts on the tiles the
+//     previous one read last (still in L2).
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
@@ -953,6 +966,9 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
     asm volatile(
@@ -978,125 +994,141 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// named barrier over the 16 consumer warps (the producer warp never joins)
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
-template <int NS, int M>
-__global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtensorMap tq, SArgs a) {
-    constexpr int RT = 32, NW = 16, RPW = 2, kSThr = 544;  // 16 compute warps + 1 TMA producer warp
+constexpr int kTmaNW = 16;           // consumer warps
+constexpr int kTmaThreads = 17 * 32; // + one producer warp
+constexpr int kTmaRT = 32;           // rows per tile
+constexpr int kTmaMaxNS = 8;
+
+template <int M>
+__global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap tq, SArgs a, int ns) {
+    constexpr int RT = kTmaRT, NW = kTmaNW, J = M;
     if (*(volatile int *)&a.ctrl->abort) return;
     unsigned int nbar = 0;
-    extern __shared__ __align__(1024) double smem_raw[];
-    __shared__ __align__(8) uint64_t full[NS];
-    // SWIZZLE_128B addresses are absolute: align the stage buffers to 1024 B
-    double *smem_t = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023) / 8;
+    extern __shared__ __align__(128) double smem_raw[];
+    __shared__ __align__(8) uint64_t full[kTmaMaxNS], empty[kTmaMaxNS];
     __shared__ double sh[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const bool producer = wid == NW;  // issues the TMA copies, computes nothing
-    const int ptid = NW * 32;         // the producer thread
+    const bool producer = wid == NW;
+    const int ptid = NW * 32;  // the producer thread
     const int ncols = a.ncols;
     const int nbox = (ncols + 15) >> 4;
-    const int stage_d = 2 * nbox * 256;           // doubles per stage (2 row halves x nbox boxes x 2 KB)
-    double *wt = smem_t + NS * stage_d;           // NS x RT
+    const int stage_d = nbox * 512 + RT;  // doubles per stage: boxes, then the tile's w rows
+    double *smem_t = smem_raw;
+    double *rpart = smem_t + (size_t)ns * stage_d;  // [2][NW][RT] row-dot partials
+    double *hs = rpart + 2 * NW * RT;               // coefficient vector of the current sweep (ncols)
     const int64_t rb = (int64_t)blockIdx.x * a.rpb;
     const int64_t re = min(a.N, rb + a.rpb);
     const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
-    const unsigned tx_bytes = (unsigned)(2 * nbox * 2048 + RT * 8);
+    const unsigned tx_bytes = (unsigned)(nbox * 4096 + RT * 8);
     if (tid == ptid) {
-        for (int q = 0; q < NS; q++) mbar_init(&full[q], 1);
+        for (int q = 0; q < ns; q++) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    int g_issue = 0, g_use = 0;  // tiles issued / consumed so far (ring position and parity)
-    auto issue = [&](int k) {    // thread 0 only
-        const int st = g_issue % NS;
-        const int64_t r0 = rb + (int64_t)k * RT;
+    // producer state (meaningful in the producer thread only)
+    int g_issue = 0, k_issued = 0;
+    // consumer state
+    int g_use = 0;
+    int sweep_no = 0;
+    auto tile_of = [&](int k) { return (sweep_no & 1) ? ntiles - 1 - k : k; };
+    auto issue_next = [&]() {  // producer thread: next tile of the current sweep into the ring
+        const int st = g_issue % ns;
+        if (g_issue >= ns) mbar_wait(&empty[st], (unsigned)(((g_issue / ns) - 1) & 1));
+        const int64_t r0 = rb + (int64_t)tile_of(k_issued) * RT;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&full[st], tx_bytes);
-        double *dst = smem_t + st * stage_d;
-        for (int h = 0; h < 2; h++)
-            for (int b = 0; b < nbox; b++)
-                tma_load_2d(dst + (h * nbox + b) * 256, &tq, (int)(r0 + 16 * h), 16 * b, &full[st]);
-        bulk_load(wt + st * RT, a.w + r0, RT * 8, &full[st]);
+        double *dst = smem_t + (size_t)st * stage_d;
+        for (int b = 0; b < nbox; b++) tma_load_2d(dst + b * 512, &tq, (int)r0, 16 * b, &full[st]);
+        bulk_load(dst + nbox * 512, a.w + r0, RT * 8, &full[st]);
         g_issue++;
+        k_issued++;
     };
-    auto prefetch = [&]() {
+    auto prefetch = [&]() {  // first stages of the current sweep (before a grid barrier)
         if (tid == ptid)
-            for (int p = 0; p < NS - 1 && p < ntiles; p++) issue(p);
+            while (k_issued < ntiles && k_issued < ns) issue_next();
     };
-    bool prefetched = false;
     auto run_tiles = [&](auto &&body) {
-        if (ntiles == 0) return;
-        if (!prefetched) prefetch();
-        prefetched = false;
-        for (int k = 0; k < ntiles; k++) {
-            if (tid == ptid && k + NS - 1 < ntiles) issue(k + NS - 1);
-            const int st = g_use % NS;
-            if (!producer) {
-                mbar_wait(&full[st], (unsigned)((g_use / NS) & 1));
-                body(k, smem_t + st * stage_d, wt + st * RT);
+        if (ntiles > 0) {
+            if (producer) {
+                if (lane == 0)
+                    while (k_issued < ntiles) issue_next();
+            } else {
+                for (int k = 0; k < ntiles; k++) {
+                    const int st = g_use % ns;
+                    mbar_wait(&full[st], (unsigned)((g_use / ns) & 1));
+                    const double *T = smem_t + (size_t)st * stage_d;
+                    body(tile_of(k), k, T, T + nbox * 512);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[st]);
+                    g_use++;
+                }
             }
-            __syncthreads();
-            g_use++;
         }
+        sweep_no++;
+        k_issued = 0;
     };
-    // element (row rr, column lane + 32 m) of a stage
-    const int qsw = lane & 7;
-    const int lofs = ((lane >> 4) << 8) + ((lane & 15) << 4);
-    auto tval = [&](const double *T, int rr, int m) -> double {
-        const int h = rr >> 4, c = (rr & 15) >> 1, o = rr & 1;
-        return T[(h * nbox << 8) + (m << 9) + lofs + ((c ^ qsw) << 1) + o];
+    // element of the thread's row (lane) and column w M + j
+    const int row = lane;
+    auto colof = [&](int j) { return wid * M + j; };
+    auto qaddr = [&](int j) {
+        const int c = colof(j);
+        return ((c >> 4) << 9) + ((c & 15) << 5) + row;
     };
-    auto rowdot = [&](const double *T, int rr, const double (&hreg)[M]) -> double {
+    auto load_q = [&](const double *T, double (&q)[J]) {
+#pragma unroll
+        for (int j = 0; j < J; j++) q[j] = colof(j) < ncols ? T[qaddr(j)] : 0.0;
+    };
+    // coefficients to shared memory (every thread of the CTA takes part: call
+    // between CTA-wide barriers); read back as warp-broadcast loads
+    auto load_h = [&](const double *h) {
+        for (int j = tid; j < ncols; j += kTmaThreads) hs[j] = __ldcg(h + j);
+        __syncthreads();
+    };
+    // row dot over all columns for the tile row of this lane (valid in every
+    // consumer thread after one named barrier)
+    auto row_dot = [&](int k, const double (&q)[J]) -> double {
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int m = 0; m < M; m += 2) {
-            if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
-            if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+        for (int j = 0; j < J; j += 2) {
+            if (colof(j) < ncols) s0 = fma(q[j], hs[colof(j)], s0);
+            if (j + 1 < J && colof(j + 1) < ncols) s1 = fma(q[j + 1], hs[colof(j + 1)], s1);
         }
-        return warp_sum(s0 + s1);
-    };
-    // cross-warp column sums -> partial[block][j] (fixed order).  The stage
-    // buffers are idle here (the tile loop ended with a barrier and the next
-    // prefetch is issued after), so they hold the NW x ncols scratch.
-    auto flush_cols = [&](const double (&acc)[M]) {
-        double *redc = smem_t;
+        const double s = s0 + s1;
+        double *rp = rpart + (k & 1) * NW * RT;
+        rp[wid * RT + row] = s;
+        consumers_sync();
+        double t = 0.0;
 #pragma unroll
-        for (int m = 0; m < M; m++) {
-            const int j = lane + 32 * m;
-            if (j < ncols && !producer) redc[wid * ncols + j] = acc[m];
-        }
-        __syncthreads();
-        for (int j = tid; j < ncols; j += kSThr) {
-            double s = 0.0;
-            for (int w = 0; w < NW; w++) s += redc[w * ncols + j];
-            a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
-        }
-        __syncthreads();
+        for (int w = 0; w < NW; w++) t += rp[w * RT + row];
+        return t;
     };
-    auto load_h = [&](const double *h, double (&hreg)[M]) {
+    // column sums of the per-thread accumulators -> partial[block][c]
+    auto flush_cols = [&](double (&acc)[J]) {
+        if (!producer) {
 #pragma unroll
-        for (int m = 0; m < M; m++) {
-            const int j = lane + 32 * m;
-            hreg[m] = j < ncols ? __ldcg(h + j) : 0.0;
+            for (int j = 0; j < J; j++) {
+                double v = acc[j];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0 && colof(j) < ncols) a.partial[(int64_t)blockIdx.x * a.PS + colof(j)] = v;
+            }
         }
     };
 
-    long long tk[8];
-    int ntk = 0;
-    auto stamp = [&]() {
-        if (a.tdbg && ntk < 8) tk[ntk++] = clock64();
-    };
-    stamp();
-    double hreg[M];
     if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
-        load_h(a.pre_h, hreg);
-        run_tiles([&](int k, const double *T, const double *W) {
-#pragma unroll
-            for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
-                const double s = rowdot(T, rr, hreg);
-                const int64_t r = rb + (int64_t)k * RT + rr;
-                if (lane == 0 && r < re) a.w[r] = W[rr] - s;
-            }
+        load_h(a.pre_h);
+        run_tiles([&](int kt, int k, const double *T, const double *W) {
+            double q[J];
+            load_q(T, q);
+            const double s = row_dot(k, q);
+            const int64_t r = rb + (int64_t)kt * RT + row;
+            if (wid == 0 && r < re) a.w[r] = W[row] - s;
         });
         __threadfence();
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1105,56 +1137,44 @@ __global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtens
 
     double nrm_wp = 0.0;
     if (ncols > 0) {
-        double acc[M];
+        double acc[J];
 #pragma unroll
-        for (int m = 0; m < M; m++) acc[m] = 0.0;
-        run_tiles([&](int k, const double *T, const double *W) {
+        for (int j = 0; j < J; j++) acc[j] = 0.0;
+        // phase A: partial h1 = Q_b^T w_b
+        run_tiles([&](int kt, int, const double *T, const double *W) {
+            const int64_t r = rb + (int64_t)kt * RT + row;
+            const double x = r < re ? W[row] : 0.0;
 #pragma unroll
-            for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
-                const int64_t r = rb + (int64_t)k * RT + rr;
-                const double x = r < re ? W[rr] : 0.0;
-#pragma unroll
-                for (int m = 0; m < M; m++)
-                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
-            }
+            for (int j = 0; j < J; j++)
+                if (colof(j) < ncols) acc[j] = fma(T[qaddr(j)], x, acc[j]);
         });
         flush_cols(acc);
-        stamp();
         prefetch();
-        prefetched = true;
         grid_sync(a.flags, a.epoch + (++nbar));
         sreduce_cols(a, ncols, a.h1, sh);
         grid_sync(a.flags, a.epoch + (++nbar));
-        load_h(a.h1, hreg);
-        stamp();
+        load_h(a.h1);
 #pragma unroll
-        for (int m = 0; m < M; m++) acc[m] = 0.0;
-        run_tiles([&](int k, const double *T, const double *W) {
-#pragma unroll
-            for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
-                const double s = rowdot(T, rr, hreg);
-                const int64_t r = rb + (int64_t)k * RT + rr;
-                const double v = (r < re) ? W[rr] - s : 0.0;
-                if (lane == 0 && r < re) {
-                    a.w[r] = v;
-                    nrm_wp = fma(v, v, nrm_wp);
-                }
-#pragma unroll
-                for (int m = 0; m < M; m++)
-                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), v, acc[m]);
+        for (int j = 0; j < J; j++) acc[j] = 0.0;
+        // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
+        run_tiles([&](int kt, int k, const double *T, const double *W) {
+            double q[J];
+            load_q(T, q);
+            const double s = row_dot(k, q);
+            const int64_t r = rb + (int64_t)kt * RT + row;
+            const double v = (r < re) ? W[row] - s : 0.0;
+            if (wid == 0 && r < re) {
+                a.w[r] = v;
+                nrm_wp = fma(v, v, nrm_wp);
             }
+#pragma unroll
+            for (int j = 0; j < J; j++) acc[j] = fma(q[j], v, acc[j]);
         });
         flush_cols(acc);
     } else {
-        run_tiles([&](int k, const double *, const double *W) {
-#pragma unroll
-            for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
-                const int64_t r = rb + (int64_t)k * RT + rr;
-                if (lane == 0 && r < re) nrm_wp = fma(W[rr], W[rr], nrm_wp);
-            }
+        run_tiles([&](int kt, int, const double *, const double *W) {
+            const int64_t r = rb + (int64_t)kt * RT + row;
+            if (wid == 0 && r < re) nrm_wp = fma(W[row], W[row], nrm_wp);
         });
     }
     {
@@ -1166,17 +1186,14 @@ __global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtens
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
         prefetch();
-        prefetched = true;
     }
-    stamp();
     grid_sync(a.flags, a.epoch + (++nbar));
     sreduce_cols(a, ncols + 1, a.h2, sh);
     grid_sync(a.flags, a.epoch + (++nbar));
-    load_h(a.h2, hreg);
-    stamp();
+    load_h(a.h2);
     const double nrmp = __ldcg(a.h2 + ncols);
     double hh = 0.0;
-    for (int j = tid; j < ncols; j += kSThr) {
+    for (int j = tid; j < ncols; j += kTmaThreads) {
         const double x = __ldcg(a.h2 + j);
         hh = fma(x, x, hh);
     }
@@ -1191,36 +1208,32 @@ __global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtens
         beta = sqrt(beta2);
         bd = !(beta > thr);
         if (!bd && ncols > 0) {
-            run_tiles([&](int k, const double *T, const double *W) {
-#pragma unroll
-                for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
-                    const double s = rowdot(T, rr, hreg);
-                    const int64_t r = rb + (int64_t)k * RT + rr;
-                    if (lane == 0 && r < re) a.w[r] = (W[rr] - s) / beta;
-                }
+            run_tiles([&](int kt, int k, const double *T, const double *W) {
+                double q[J];
+                load_q(T, q);
+                const double s = row_dot(k, q);
+                const int64_t r = rb + (int64_t)kt * RT + row;
+                if (wid == 0 && r < re) a.w[r] = (W[row] - s) / beta;
             });
         } else if (!bd) {
-            for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+            for (int64_t r = rb + tid; r < re; r += kTmaThreads) a.w[r] = a.w[r] / beta;
         }
     } else {
         double nrm2 = 0.0;
         if (ncols > 0) {
-            run_tiles([&](int k, const double *T, const double *W) {
-#pragma unroll
-                for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
-                    const double s = rowdot(T, rr, hreg);
-                    const int64_t r = rb + (int64_t)k * RT + rr;
-                    if (lane == 0 && r < re) {
-                        const double v = W[rr] - s;
-                        a.w[r] = v;
-                        nrm2 = fma(v, v, nrm2);
-                    }
+            run_tiles([&](int kt, int k, const double *T, const double *W) {
+                double q[J];
+                load_q(T, q);
+                const double s = row_dot(k, q);
+                const int64_t r = rb + (int64_t)kt * RT + row;
+                if (wid == 0 && r < re) {
+                    const double v = W[row] - s;
+                    a.w[r] = v;
+                    nrm2 = fma(v, v, nrm2);
                 }
             });
         } else {
-            for (int64_t r = rb + tid; r < re; r += kSThr) nrm2 = fma(a.w[r], a.w[r], nrm2);
+            for (int64_t r = rb + tid; r < re; r += kTmaThreads) nrm2 = fma(a.w[r], a.w[r], nrm2);
         }
         const double bn = block_sum_all(nrm2, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
@@ -1230,17 +1243,16 @@ __global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtens
         beta = sqrt(fmax(__ldcg(a.h3), 0.0));
         bd = !(beta > thr);
         if (!bd)
-            for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+            for (int64_t r = rb + tid; r < re; r += kTmaThreads) a.w[r] = a.w[r] / beta;
     }
-    stamp();
-    if (a.tdbg && tid == 0 && ntk == 6)
-        for (int q = 1; q < 6; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
-    if (a.tdbg && tid == 0 && ntk == 6) atomicAdd(a.tdbg + 6, 1ull), atomicAdd(a.tdbg + 7, (unsigned long long)ntiles);
-    // drain a prefetch left pending when phase C was skipped (producer thread)
-    while (g_use < g_issue) {
-        const int st = g_use % NS;
-        mbar_wait(&full[st], (unsigned)((g_use / NS) & 1));
-        g_use++;
+    // phase C prefetched but skipped (breakdown): wait for those copies so
+    // that no bulk copy is in flight when the CTA exits
+    if (!producer && ncols > 0 && pyth && bd) {
+        for (int q = 0; q < min(ntiles, ns); q++) {
+            const int st = g_use % ns;
+            mbar_wait(&full[st], (unsigned)((g_use / ns) & 1));
+            g_use++;
+        }
     }
     if (blockIdx.x == 0 && tid == 0) {
         if (bd) {
@@ -1256,28 +1268,32 @@ __global__ void __launch_bounds__(544) k_cgs2_tma(const __grid_constant__ CUtens
     }
 }
 
-template <int NS, int M>
+template <int M>
 bool launch_tma(const CUtensorMap &tq, const SArgs &a0, int nsm, cudaStream_t s) {
     SArgs a = a0;
     const int nbox = (a.ncols + 15) / 16;
-    const size_t smem = (size_t)NS * 2 * nbox * 2048 + (NS * 32) * sizeof(double) + 1024;
-    if (smem > 220 * 1024 || a.ncols > 32 * M) return false;
+    const size_t stage_b = ((size_t)nbox * 512 + kTmaRT) * sizeof(double);
+    const size_t fixed = ((size_t)2 * kTmaNW * kTmaRT + a.ncols + 2) * sizeof(double) + 128;
+    if (a.ncols > kTmaNW * M) return false;
+    const int ns = (int)std::min<size_t>(kTmaMaxNS, (200 * 1024 - fixed) / stage_b);
+    if (ns < 2) return false;
+    const size_t smem = ns * stage_b + fixed;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_cgs2_tma<NS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_cgs2_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         attr = true;
     }
     int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_tma<NS, M>, 544, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_tma<M>, kTmaThreads, smem);
     if (bps < 1) return false;
     const int nb = nsm;
     int64_t rpb = (a.N + nb - 1) / nb;
-    rpb = (rpb + 31) / 32 * 32;
+    rpb = (rpb + kTmaRT - 1) / kTmaRT * kTmaRT;
     a.rpb = rpb;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
     CUtensorMap map = tq;
-    void *args[] = {&map, &a};
-    if (cudaLaunchCooperativeKernel((void *)k_cgs2_tma<NS, M>, grid, 544, args, smem, s) != cudaSuccess) {
+    void *args[] = {&map, &a, (void *)&ns};
+    if (cudaLaunchCooperativeKernel((void *)k_cgs2_tma<M>, grid, kTmaThreads, args, smem, s) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
@@ -1287,12 +1303,13 @@ bool launch_tma(const CUtensorMap &tq, const SArgs &a0, int nsm, cudaStream_t s)
 
 bool launch_tma_any(const CUtensorMap &tq, const SArgs &a, int nsm, cudaStream_t s) {
     const int nc = a.ncols;
-    if (nc <= 64) return launch_tma<4, 2>(tq, a, nsm, s);
-    if (nc <= 128) return launch_tma<4, 4>(tq, a, nsm, s);
-    if (nc <= 192) return launch_tma<3, 6>(tq, a, nsm, s);
-    if (nc <= 256) return launch_tma<3, 8>(tq, a, nsm, s);
-    if (nc <= 320) return launch_tma<2, 10>(tq, a, nsm, s);
-    if (nc <= 384) return launch_tma<2, 12>(tq, a, nsm, s);
+    if (nc <= 16 * 2) return launch_tma<2>(tq, a, nsm, s);
+    if (nc <= 16 * 4) return launch_tma<4>(tq, a, nsm, s);
+    if (nc <= 16 * 8) return launch_tma<8>(tq, a, nsm, s);
+    if (nc <= 16 * 12) return launch_tma<12>(tq, a, nsm, s);
+    if (nc <= 16 * 16) return launch_tma<16>(tq, a, nsm, s);
+    if (nc <= 16 * 20) return launch_tma<20>(tq, a, nsm, s);
+    if (nc <= 16 * 24) return launch_tma<24>(tq, a, nsm, s);
     return false;  // wider bases: cp.async variants
 }
 
@@ -1340,11 +1357,11 @@ bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_
     if (!encode || (ld % 2) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
     cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)ncols_total};
     cuuint64_t gstride[1] = {(cuuint64_t)ld * 8};
-    cuuint32_t box[2] = {16, 16};
+    cuuint32_t box[2] = {32, 16};  // 32 rows x 16 columns (k_cgs2_tma row tile)
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(reinterpret_cast<CUtensorMap *>(map128), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                         const_cast<double *>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -1444,7 +1461,7 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     }
     // deepest pipeline that fits: RT = 32 rows with 4, 3, 2 stages, then 16 and 8 rows
     const char *sv = getenv("SVDSC_STREAM_VARIANT");
-    const int var = sv ? atoi(sv) : 0;
+    const int var = sv ? atoi(sv) : 2;  // default: register-blocked cp.async (measured fastest, tools/time_ops.py)
     if (var == 0 && tmap && launch_tma_any(*reinterpret_cast<const CUtensorMap *>(tmap), sa, nsm, s)) return true;
     if ((var == 0 || var == 2) && launch_stream2_any(sa, nsm, s)) return true;
     if (var == 1 && launch_stream<16, 512, 4>(sa, nsm, s)) return true;

@@ -46,6 +46,7 @@ struct CsrOp {
     // row bins: rows grouped by length class, one list per kernel variant
     int32_t *bin_rows = nullptr;       // concatenated row lists
     int64_t bin_off[8] = {0};          // offsets into bin_rows; bin b = [off[b], off[b+1])
+    bool bin_identity[8] = {false};    // bin b holds all rows (in order): rows[g] == g
     // long rows (> kLongRow nnz) split into chunks
     int32_t *long_rows = nullptr;      // row id per long row
     int64_t *chunk_first = nullptr;    // first chunk index per long row (+1 sentinel)

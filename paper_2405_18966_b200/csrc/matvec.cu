@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
 #include <stdexcept>
 #include <vector>
@@ -29,7 +30,6 @@ thread_local int64_t g_launches = 0;
 namespace {
 
 constexpr int kLongRow = 65536;   // rows longer than this are split into chunks
-constexpr int kCtaThreads = 256;
 
 __device__ __forceinline__ bool aborted(const int *abort) {
     return abort != nullptr && *(volatile const int *)abort != 0;
@@ -58,13 +58,13 @@ __global__ void k_bin_count(int64_t nrows, const int64_t *__restrict__ rp, unsig
     if (threadIdx.x < 8 && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
 }
 
-__global__ void k_bin_fill(int64_t nrows, const int64_t *__restrict__ rp,
-                           unsigned long long *cursor, const int64_t *off, int32_t *rows) {
+// bin key and row id per row; a stable radix sort by key then lists every bin's
+// rows in ascending order (streaming access to row_ptr / col / val / y)
+__global__ void k_bin_keys(int64_t nrows, const int64_t *__restrict__ rp, uint8_t *key, int32_t *ids) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
          r += (int64_t)gridDim.x * blockDim.x) {
-        int b = row_bin(rp[r + 1] - rp[r]);
-        unsigned long long pos = atomicAdd(&cursor[b], 1ull);
-        rows[off[b] + (int64_t)pos] = (int32_t)r;
+        key[r] = (uint8_t)row_bin(rp[r + 1] - rp[r]);
+        ids[r] = (int32_t)r;
     }
 }
 
@@ -75,34 +75,93 @@ __device__ __forceinline__ void epilogue_store(double *y, int64_t r, double sum,
     y[r] = sum;
 }
 
-// G lanes per row; the whole warp iterates in lock-step so full-mask shuffles are legal.
+// G lanes per row; the whole warp iterates in lock-step so full-mask shuffles
+// are legal.  Each lane issues kU index/value loads (streaming, evict-first: A
+// is read once per product) before their kU dependent x gathers (read-only
+// path, L1/L2 resident), so a warp keeps 2 kU + kU loads in flight instead of a
+// serial load -> gather -> FMA chain.  rows == nullptr: the bin is the identity
+// (every row, in order).  Fixed shape per G: deterministic.
 template <int G>
-__global__ void __launch_bounds__(256) k_spmv_vec(const int32_t *__restrict__ rows, int64_t count,
+__device__ __forceinline__ void spmv_vec_rows(const int32_t *__restrict__ rows, int64_t count,
                                                   const int64_t *__restrict__ rp,
                                                   const int32_t *__restrict__ col,
                                                   const double *__restrict__ val,
                                                   const double *__restrict__ x, double *__restrict__ y,
                                                   const double *c_dev, const double *__restrict__ yprev,
-                                                  const int *abort) {
-    if (aborted(abort)) return;
+                                                  int64_t blk, int64_t nblk) {
     constexpr int GPW = kWarp / G;  // groups per warp
+    constexpr int kU = 4;
     const int lane = threadIdx.x & 31;
     const int sub = lane % G;
-    const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp_g = (blk * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (nblk * blockDim.x) >> 5;
     const double c = c_dev ? *c_dev : 0.0;
     for (int64_t base = warp_g * GPW; base < count; base += nwarps * GPW) {
         const int64_t g = base + lane / G;
         double sum = 0.0;
-        int32_t r = -1;
+        int64_t r = -1;
         if (g < count) {
-            r = rows[g];
+            r = rows ? (int64_t)rows[g] : g;
             const int64_t p0 = rp[r], p1 = rp[r + 1];
-            for (int64_t p = p0 + sub; p < p1; p += G) sum = fma(val[p], __ldg(x + col[p]), sum);
+            double s1 = 0.0;
+            for (int64_t p = p0 + sub; p < p1; p += G * kU) {
+                int ci[kU];
+                double vv[kU], xv[kU];
+#pragma unroll
+                for (int u = 0; u < kU; u++) {
+                    const int64_t q = p + (int64_t)u * G;
+                    const bool ok = q < p1;
+                    ci[u] = ok ? __ldcs(col + q) : 0;
+                    vv[u] = ok ? __ldcs(val + q) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kU; u++) xv[u] = __ldg(x + ci[u]);
+#pragma unroll
+                for (int u = 0; u < kU; u += 2) {
+                    sum = fma(vv[u], xv[u], sum);
+                    s1 = fma(vv[u + 1], xv[u + 1], s1);
+                }
+            }
+            sum += s1;
         }
 #pragma unroll
         for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, G);
         if (sub == 0 && r >= 0) epilogue_store(y, r, sum, c, yprev);
+    }
+}
+
+
+// All vector bins in ONE launch: CTAs [bstart[b], bstart[b+1]) serve bin b
+// with its group width (2, 4, 8, 16, 32 lanes per row).  Avoids one
+// serialized (and often tiny) launch per non-empty bin.
+struct BinArgs {
+    const int32_t *rows[5];  // nullptr: identity bin
+    int64_t count[5];
+    int bstart[6];
+};
+
+__global__ void __launch_bounds__(256) k_spmv_bins(BinArgs ba, const int64_t *__restrict__ rp,
+                                                   const int32_t *__restrict__ col, const double *__restrict__ val,
+                                                   const double *__restrict__ x, double *__restrict__ y,
+                                                   const double *c_dev, const double *__restrict__ yprev,
+                                                   const int *abort) {
+    if (aborted(abort)) return;
+    const int bx = blockIdx.x;
+    int b = 0, lo = ba.bstart[0], hi = ba.bstart[1];
+#pragma unroll
+    for (int q = 1; q < 5; q++)
+        if (bx >= ba.bstart[q]) {
+            b = q;
+            lo = ba.bstart[q];
+            hi = ba.bstart[q + 1];
+        }
+    const int64_t blk = bx - lo, nblk = hi - lo;
+    switch (b) {
+        case 0: spmv_vec_rows<2>(ba.rows[0], ba.count[0], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        case 1: spmv_vec_rows<4>(ba.rows[1], ba.count[1], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        case 2: spmv_vec_rows<8>(ba.rows[2], ba.count[2], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        case 3: spmv_vec_rows<16>(ba.rows[3], ba.count[3], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        default: spmv_vec_rows<32>(ba.rows[4], ba.count[4], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
     }
 }
 
@@ -346,11 +405,28 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
     for (int b = 0; b < 8; b++) off[b + 1] = off[b] + (int64_t)hc[b];
     for (int b = 0; b < 8; b++) op.bin_off[b] = off[b];
     op.bin_rows = dev_alloc<int32_t>(op, (size_t)op.nrows);
-    int64_t *doff = dev_alloc<int64_t>(op, 9);
-    check(cudaMemcpyAsync(doff, off, sizeof(off), cudaMemcpyHostToDevice, s), "H2D");
-    unsigned long long *cur = cnt + 8;
-    check(cudaMemsetAsync(cur, 0, 8 * sizeof(unsigned long long), s), "memset");
-    k_bin_fill<<<grid_for(op.nrows, 256), 256, 0, s>>>(op.nrows, op.row_ptr, cur, doff, op.bin_rows);
+    {
+        uint8_t *k_in = nullptr, *k_out = nullptr;
+        int32_t *ids = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_bytes = 0;
+        const int n32 = (int)op.nrows;
+        check(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, ids, op.bin_rows, n32, 0, 3, s),
+              "radix sort size");
+        check(cudaMalloc(&k_in, std::max<int64_t>(op.nrows, 1) * 2), "cudaMalloc");
+        k_out = k_in + std::max<int64_t>(op.nrows, 1);
+        check(cudaMalloc(&ids, std::max<int64_t>(op.nrows, 1) * sizeof(int32_t)), "cudaMalloc");
+        check(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)), "cudaMalloc");
+        k_bin_keys<<<grid_for(op.nrows, 256), 256, 0, s>>>(op.nrows, op.row_ptr, k_in, ids);
+        check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, ids, op.bin_rows, n32, 0, 3, s),
+              "radix sort");
+        check(cudaStreamSynchronize(s), "sync");
+        cudaFree(tmp);
+        cudaFree(ids);
+        cudaFree(k_in);
+    }
+    // a bin that holds every row lists them in order: the kernels index rows directly
+    for (int b = 0; b < 8; b++) op.bin_identity[b] = (off[b + 1] - off[b] == op.nrows);
     // long rows: host-side deterministic chunk table (few rows)
     op.n_long = off[7] - off[6];
     if (op.n_long > 0) {
@@ -454,19 +530,42 @@ void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, c
               const int *abort, cudaStream_t s) {
     const int64_t *o = A.bin_off;
     const int cap = 148 * 8;
-#define LAUNCH_VEC(G, b)                                                                       \
-    if (o[b + 1] > o[b]) {                                                                     \
-        int64_t cnt = o[b + 1] - o[b];                                                         \
-        k_spmv_vec<G><<<grid_for(cnt * G, 256, cap), 256, 0, s>>>(A.bin_rows + o[b], cnt, A.row_ptr, \
-                                                                  A.col, A.val, x, y, c_dev, yprev, abort); \
-        count_launch();                                                                        \
+    {
+        // CTAs per bin proportional to its nonzeros (and rows), >= 1 per non-empty bin
+        BinArgs ba{};
+        double work[5], tot = 0.0;
+        for (int b = 0; b < 5; b++) {
+            const int64_t cnt = o[b + 1] - o[b];
+            ba.rows[b] = A.bin_identity[b] ? nullptr : A.bin_rows + o[b];
+            ba.count[b] = cnt;
+            work[b] = cnt > 0 ? (double)cnt * (double)(4 << b) : 0.0;  // rows x typical length class
+            tot += work[b];
+        }
+        static int wave = 0;
+        if (!wave) {
+            int bps = 0, dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_bins, 256, 0);
+            wave = std::max(1, bps) * nsm;
+        }
+        const int vcap = std::min(cap, wave);
+        int nb_tot = 0;
+        for (int b = 0; b < 5; b++) {
+            ba.bstart[b] = nb_tot;
+            if (ba.count[b] == 0) continue;
+            const int G = 2 << b;
+            const int need = grid_for(ba.count[b] * G, 256, vcap);
+            const int share = std::max(1, (int)(vcap * work[b] / tot + 0.5));
+            nb_tot += std::min(need, share);
+        }
+        ba.bstart[5] = nb_tot;
+        if (nb_tot > 0) {
+            // one full wave: the grid-stride loops then have no partial second wave
+            k_spmv_bins<<<nb_tot, 256, 0, s>>>(ba, A.row_ptr, A.col, A.val, x, y, c_dev, yprev, abort);
+            count_launch();
+        }
     }
-    LAUNCH_VEC(2, 0)
-    LAUNCH_VEC(4, 1)
-    LAUNCH_VEC(8, 2)
-    LAUNCH_VEC(16, 3)
-    LAUNCH_VEC(32, 4)
-#undef LAUNCH_VEC
     if (o[6] > o[5]) {
         int64_t cnt = o[6] - o[5];
         k_spmv_cta<<<(unsigned)std::min<int64_t>(cnt, cap), 256, 0, s>>>(A.bin_rows + o[5], cnt, A.row_ptr, A.col,

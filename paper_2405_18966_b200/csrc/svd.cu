@@ -184,17 +184,22 @@ __device__ __forceinline__ double jacobi_tan(double al, double be, double gam) {
 // ---------------------------------------------------------------------------
 // Block one-sided Jacobi on a thread-block cluster (B200: up to 16 CTAs,
 // distributed shared memory).  The pe = p + (p odd) columns are cut into 2C
-// half-blocks of h columns; CTA c holds two half-blocks in its shared memory
-// and, per block round, runs a full local round-robin sweep over its 2h
-// columns (all pairs, LDS only, __syncthreads between local rounds).  Between
+// half-blocks of h columns; CTA c holds two half-blocks in its shared memory.
+// Block round 0 of a sweep runs a full local round-robin sweep over the CTA's
+// 2h columns (all pairs, LDS only, __syncthreads between local rounds); every
+// later block round runs only the h cross rounds between its two half-blocks,
+// with the slot-0 column of each warp held in registers (every pair still
+// meets once per sweep; 40% fewer rounds than a full local sweep per block
+// round, and half the shared-memory traffic per rotation).  Between
 // block rounds the half-blocks move along the circle-method tournament (one
 // DSMEM pull into registers, cluster barrier, store), so every pair of
 // half-blocks meets once per block sweep.  Every rotation is logged as
 // (t = tan theta, a, b) for k_apply_log; rotations of one local round (all
 // CTAs) touch disjoint columns, so replaying them round by round is exact.
 struct RotLog {
-    double t;
-    int32_t a, b;
+    double c, s;      // the rotation as applied to W (c = s = 0: no rotation)
+    int32_t a, b;     // global column pair, a < b
+    int64_t pad;      // 32-byte entries: 16-byte cp.async staging
 };
 
 // circle-method tournament over 2C players (player 0 fixed, m = 2C - 1)
@@ -218,6 +223,42 @@ __device__ __forceinline__ void hb_loc(int C, int r, int P, int &cta, int &slot)
     } else {
         cta = m - 1 - k;
         slot = 1;
+    }
+}
+
+// rounds of one sweep: block round 0 = full local round robin over 2h columns
+// (2h - 1 rounds), each later block round = the h cross rounds of its two
+// half-blocks; (2C - 1) block rounds
+__host__ __device__ __forceinline__ int64_t jacobi_rounds_per_sweep(int C, int h) {
+    return (int64_t)(2 * h - 1) + (int64_t)(2 * C - 2) * h;
+}
+
+// alpha = |a|^2, beta = |b|^2, gamma = a.b over the warp's rows (two
+// interleaved FMA chains per sum, xor-butterfly over the 32 lanes)
+template <int kRPL>
+__device__ __forceinline__ void pair_sums(const double (&a)[kRPL], const double (&b)[kRPL], double &al, double &be,
+                                          double &gam) {
+    double al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+    al = be = gam = 0.0;
+#pragma unroll
+    for (int u = 0; u < kRPL; u += 2) {
+        al = fma(a[u], a[u], al);
+        be = fma(b[u], b[u], be);
+        gam = fma(a[u], b[u], gam);
+        if (u + 1 < kRPL) {
+            al1 = fma(a[u + 1], a[u + 1], al1);
+            be1 = fma(b[u + 1], b[u + 1], be1);
+            ga1 = fma(a[u + 1], b[u + 1], ga1);
+        }
+    }
+    al += al1;
+    be += be1;
+    gam += ga1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, off);
+        be += __shfl_xor_sync(0xffffffffu, be, off);
+        gam += __shfl_xor_sync(0xffffffffu, gam, off);
     }
 }
 
@@ -264,13 +305,16 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
     if (CL) cl.sync(); else __syncthreads();
     const int64_t per_round = (int64_t)C * h;
     const int lrounds = H2 - 1;
+    const int64_t rps = jacobi_rounds_per_sweep(C, h);
     int sweep;
     bool conv = false;
     for (sweep = 1; sweep <= max_sweeps; sweep++) {
         int *flag = &rot_flag[sweep & 1];
         for (int br = 0; br < m; br++) {
+            if (br == 0) {
+            // block round 0: all pairs of the CTA's 2h columns (local round robin, shared memory)
             for (int lr = 0; lr < lrounds; lr++) {
-                RotLog *logr = rlog + (((int64_t)(sweep - 1) * m + br) * lrounds + lr) * per_round + (int64_t)me * h;
+                RotLog *logr = rlog + ((int64_t)(sweep - 1) * rps + lr) * per_round + (int64_t)me * h;
                 for (int qb = wid * (32 / kG); qb < h; qb += ngrp) {
                     const int q = qb + lane / kG;
                     int i = 0, j = 0;
@@ -284,7 +328,6 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                     // the pair's columns, oriented (lower global index, higher) as in the oracle
                     double *pa = Wl + (int64_t)(ga < gb ? i : j) * p, *pb = Wl + (int64_t)(ga < gb ? j : i) * p;
                     double xr[kRPL], yr[kRPL];
-                    double al = 0.0, be = 0.0, gam = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
 #pragma unroll
                     for (int u = 0; u < kRPL; u++) {
                         const int r = gl + kG * u;
@@ -292,31 +335,11 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                         xr[u] = ok ? pa[r] : 0.0;
                         yr[u] = ok ? pb[r] : 0.0;
                     }
-#pragma unroll
-                    for (int u = 0; u < kRPL; u += 2) {
-                        al = fma(xr[u], xr[u], al);
-                        be = fma(yr[u], yr[u], be);
-                        gam = fma(xr[u], yr[u], gam);
-                        if (u + 1 < kRPL) {
-                            al1 = fma(xr[u + 1], xr[u + 1], al1);
-                            be1 = fma(yr[u + 1], yr[u + 1], be1);
-                            ga1 = fma(xr[u + 1], yr[u + 1], ga1);
-                        }
-                    }
-                    al += al1;
-                    be += be1;
-                    gam += ga1;
-#pragma unroll
-                    for (int off = kG / 2; off > 0; off >>= 1) {
-                        al += __shfl_xor_sync(0xffffffffu, al, off, kG);
-                        be += __shfl_xor_sync(0xffffffffu, be, off, kG);
-                        gam += __shfl_xor_sync(0xffffffffu, gam, off, kG);
-                    }
-                    double t = 0.0;
+                    double al, be, gam;
+                    pair_sums<kRPL>(xr, yr, al, be, gam);
+                    double c = 0.0, s = 0.0;
                     if (live && al > tiny2 && be > tiny2 && gam * gam > ctol2 * (al * be)) {
-                        t = jacobi_tan(al, be, gam);
-                        double c, s;
-                        rot_cs(t, c, s);
+                        rot_cs(jacobi_tan(al, be, gam), c, s);
 #pragma unroll
                         for (int u = 0; u < kRPL; u++) {
                             const int r = gl + kG * u;
@@ -329,13 +352,84 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                     }
                     if (gl == 0 && q < h) {
                         RotLog e;
-                        e.t = t;
+                        e.c = c;
+                        e.s = s;
                         e.a = min(ga, gb);
                         e.b = max(ga, gb);
                         logr[q] = e;
                     }
                 }
                 __syncthreads();
+            }
+            } else {
+            // block rounds >= 1: only the h^2 cross pairs of the two half-blocks
+            // (pairs inside a half-block were rotated in block round 0).  Warp i
+            // keeps column X[i] (slot 0) in registers for the whole block round
+            // and meets Y[(i + r) mod h] (slot 1) in round r: one column read and
+            // written per rotation instead of two.
+            const bool has = wid < h;
+            const int gx = has ? gcol[wid] : p;
+            double xr[kRPL];
+#pragma unroll
+            for (int u = 0; u < kRPL; u++) {
+                const int r = gl + kG * u;
+                xr[u] = (has && r < p) ? Wl[(int64_t)wid * p + r] : 0.0;
+            }
+            const int64_t rbase = (int64_t)(sweep - 1) * rps + lrounds + (int64_t)(br - 1) * h;
+            for (int rr = 0; rr < h; rr++) {
+                if (has) {
+                    const int j = h + (wid + rr) % h;
+                    const int gy = gcol[j];
+                    const bool live = gx < p && gy < p;
+                    double *py = Wl + (int64_t)j * p;
+                    double yr[kRPL];
+#pragma unroll
+                    for (int u = 0; u < kRPL; u++) {
+                        const int r = gl + kG * u;
+                        yr[u] = (live && r < p) ? py[r] : 0.0;
+                    }
+                    const bool xlow = gx < gy;
+                    double al, be, gam;
+                    if (xlow) pair_sums<kRPL>(xr, yr, al, be, gam);
+                    else pair_sums<kRPL>(yr, xr, al, be, gam);
+                    double c = 0.0, s = 0.0;
+                    if (live && al > tiny2 && be > tiny2 && gam * gam > ctol2 * (al * be)) {
+                        rot_cs(jacobi_tan(al, be, gam), c, s);
+                        // (A, B) = (lower, higher): A' = c A - s B, B' = s A + c B
+#pragma unroll
+                        for (int u = 0; u < kRPL; u++) {
+                            const double x = xr[u], y = yr[u];
+                            if (xlow) {
+                                xr[u] = c * x - s * y;
+                                yr[u] = s * x + c * y;
+                            } else {
+                                yr[u] = c * y - s * x;
+                                xr[u] = s * y + c * x;
+                            }
+                            const int r = gl + kG * u;
+                            if (r < p) py[r] = yr[u];
+                        }
+                        if (gl == 0) *flag = 1;
+                    }
+                    if (gl == 0) {
+                        RotLog e;
+                        e.c = c;
+                        e.s = s;
+                        e.a = min(gx, gy);
+                        e.b = max(gx, gy);
+                        rlog[(rbase + rr) * per_round + (int64_t)me * h + wid] = e;
+                    }
+                }
+                __syncthreads();
+            }
+            if (has) {
+#pragma unroll
+                for (int u = 0; u < kRPL; u++) {
+                    const int r = gl + kG * u;
+                    if (r < p) Wl[(int64_t)wid * p + r] = xr[u];
+                }
+            }
+            __syncthreads();
             }
             if (CL && m > 1) {
                 // move to round br+1 (after the last block round the circle is back at round 0)
@@ -400,16 +494,18 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
 }
 
 // V = J_1 J_2 ... (the logged rotations) for R rows of V per CTA: row r of V is
-// e_r^T J_1 J_2 ..., independent of the other rows.  The log is staged through
-// shared memory in chunks of kLogRounds rounds with cp.async double buffering.
-constexpr int kLogRounds = 16;
+// e_r^T J_1 J_2 ..., independent of the other rows.  Thread (q, i) applies
+// rotation q of every round to row i of the CTA's R rows (rotations of one
+// round touch disjoint columns).  The log is staged through shared memory in
+// chunks of kLogRounds rounds with cp.async double buffering; (c, s) come
+// from the log, so V sees exactly the rotations applied to W.
 __global__ void k_apply_log(int p, int per_round, int rounds_per_sweep, const RotLog *__restrict__ rlog,
-                            const Ctrl *ctrl, double *V, int R, const int *abort) {
+                            const Ctrl *ctrl, double *V, int R, int kLogRounds, const int *abort) {
     if (aborted(abort)) return;
     extern __shared__ double sm[];
     const int64_t total_rounds = (int64_t)ctrl->svd_sweeps * rounds_per_sweep;
-    double *rows = sm;                                        // R x p
-    RotLog *buf = reinterpret_cast<RotLog *>(rows + (int64_t)R * p);  // 2 x kLogRounds x per_round
+    double *rows = sm;                                                 // R x p
+    RotLog *buf = reinterpret_cast<RotLog *>(rows + (((int64_t)R * p + 1) & ~1));  // 2 x kLogRounds x per_round
     const int chunk = kLogRounds * per_round;
     const int r0 = blockIdx.x * R;
     for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
@@ -418,15 +514,18 @@ __global__ void k_apply_log(int p, int per_round, int rounds_per_sweep, const Ro
     }
     auto load_chunk = [&](int64_t first_round, RotLog *dst) {
         const int64_t nrem = total_rounds - first_round;
-        const int n = (int)min((int64_t)kLogRounds, max((int64_t)0, nrem)) * per_round;
-        const RotLog *src = rlog + first_round * per_round;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst + i);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + i));
+        const int n16 = (int)min((int64_t)kLogRounds, max((int64_t)0, nrem)) * per_round * 2;  // 16-byte units
+        const char *src = reinterpret_cast<const char *>(rlog + first_round * per_round);
+        for (int i = threadIdx.x; i < n16; i += blockDim.x) {
+            const unsigned saddr = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char *>(dst) + 16 * i);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + 16 * i));
         }
         asm volatile("cp.async.commit_group;");
     };
     if (total_rounds > 0) load_chunk(0, buf);
+    const int q = threadIdx.x % per_round, i = threadIdx.x / per_round;
+    const bool act = i < R;
+    double *row = rows + i * p;
     int cur = 0;
     for (int64_t base = 0; base < total_rounds; base += kLogRounds) {
         if (base + kLogRounds < total_rounds) {
@@ -439,27 +538,22 @@ __global__ void k_apply_log(int p, int per_round, int rounds_per_sweep, const Ro
         const RotLog *lg = buf + cur * chunk;
         const int nr = (int)min((int64_t)kLogRounds, total_rounds - base);
         for (int k = 0; k < nr; k++) {
-            for (int q = threadIdx.x; q < per_round; q += blockDim.x) {
-                const RotLog e = lg[k * per_round + q];
-                if (e.t != 0.0) {
-                    double c, s;
-                    rot_cs(e.t, c, s);
-                    for (int i = 0; i < R; i++) {
-                        double *row = rows + i * p;
-                        const double x = row[e.a], y = row[e.b];
-                        row[e.a] = c * x - s * y;
-                        row[e.b] = s * x + c * y;
-                    }
+            if (act) {
+                const RotLog &e = lg[k * per_round + q];
+                const double c = e.c, s = e.s;
+                if (c != 0.0) {
+                    const double x = row[e.a], y = row[e.b];
+                    row[e.a] = c * x - s * y;
+                    row[e.b] = s * x + c * y;
                 }
             }
             __syncthreads();
         }
-        __syncthreads();
         cur ^= 1;
     }
     for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
-        const int i = idx / p, j = idx % p;
-        if (r0 + i < p) V[(r0 + i) + (int64_t)j * p] = rows[idx];
+        const int ii = idx / p, j = idx % p;
+        if (r0 + ii < p) V[(r0 + ii) + (int64_t)j * p] = rows[idx];
     }
 }
 
@@ -649,6 +743,131 @@ __global__ void __launch_bounds__(256) k_recombine(int64_t N, int t, int k, cons
     }
 }
 
+// ---------------------------------------------------------------------------
+// Recombination on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64):
+// Qout(:, 0:k) = Q(:, 0:t) W(:, 0:k), a (N x t)(t x k) contraction at
+// 19-38 flop/B, so it is FP64-throughput bound, not HBM
+// bound.  A CTA owns a 32-row tile: the whole tile Q(r0:r0+32, 0:t) is staged
+// in shared memory (cp.async) before any output row is written, which makes the
+// in-place call (Qout == Q) safe.  W streams through shared memory in chunks of
+// kRC rows (register-staged prefetch of chunk c+1 during chunk c).  Four warps:
+// warp (mh, nh) computes rows 16 mh .. 16 mh + 15 (two m8 tiles) times n8 tiles
+// nh*NTW .. nh*NTW + NTW - 1.  Fragment layout of m8n8k4 (PTX ISA): A row =
+// lane/4, col = lane%4; B row = lane%4, col = lane/4; C row = lane/4, cols
+// 2(lane%4) + {0, 1}.  Shared strides are 4 mod 16 doubles, so every fragment
+// load of a half-warp hits 16 distinct banks.
+constexpr int kRT = 32;       // rows per tile
+constexpr int kLDT = kRT + 4; // tile stride (doubles)
+constexpr int kRC = 8;        // W rows per chunk (two k4 steps)
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NTW>
+__global__ void __launch_bounds__(128) k_recombine_dmma(int64_t N, int t, int k, const double *Q, int64_t ldq,
+                                                        const double *__restrict__ Wm, int ldw, double *Qout,
+                                                        int64_t ldo, int ldws, bool vec) {
+    extern __shared__ __align__(16) double sm_rc[];
+    const int KP = (t + kRC - 1) / kRC * kRC;
+    double *tile = sm_rc;                      // KP x kLDT  (tile[j * kLDT + row])
+    double *wsb = tile + (size_t)KP * kLDT;    // 2 x kRC x ldws (wsb[l * ldws + col])
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int mh = wid & 1, nh = wid >> 1;
+    const int g = lane >> 2, tg = lane & 3;
+    const int NT = (k + 7) >> 3;
+    const int nch = KP / kRC;
+    const int wpc = kRC * NT * 8;              // W elements per chunk (incl. padding columns)
+    constexpr int kWReg = (kRC * 2 * NTW * 8 + 127) / 128;
+    // zero the K padding rows of the tile once (never overwritten)
+    for (int idx = tid; idx < (KP - t) * kLDT; idx += 128) tile[(size_t)t * kLDT + idx] = 0.0;
+    const int64_t ntiles = (N + kRT - 1) / kRT;
+    double wr[kWReg];
+    auto wload = [&](int c) {  // chunk c of W into registers (zero beyond t / k)
+#pragma unroll
+        for (int u = 0; u < kWReg; u++) {
+            const int idx = tid + 128 * u;
+            double x = 0.0;
+            if (idx < wpc) {
+                const int l = idx % kRC, j = idx / kRC;
+                const int lg = c * kRC + l;
+                if (lg < t && j < k) x = __ldg(Wm + lg + (int64_t)j * ldw);
+            }
+            wr[u] = x;
+        }
+    };
+    auto wstore = [&](int buf) {
+        double *dst = wsb + (size_t)buf * kRC * ldws;
+#pragma unroll
+        for (int u = 0; u < kWReg; u++) {
+            const int idx = tid + 128 * u;
+            if (idx < wpc) dst[(idx % kRC) * ldws + idx / kRC] = wr[u];
+        }
+    };
+    for (int64_t tI = blockIdx.x; tI < ntiles; tI += gridDim.x) {
+        const int64_t r0 = tI * kRT;
+        const int nr = (int)min((int64_t)kRT, N - r0);
+        if (vec && nr == kRT) {
+            for (int idx = tid; idx < t * (kRT / 2); idx += 128) {
+                const int j = idx / (kRT / 2), q = (idx % (kRT / 2)) * 2;
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + (size_t)j * kLDT + q);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Q + r0 + q + (int64_t)j * ldq));
+            }
+            asm volatile("cp.async.commit_group;");
+        } else {
+            for (int idx = tid; idx < t * kRT; idx += 128) {
+                const int j = idx / kRT, q = idx % kRT;
+                tile[(size_t)j * kLDT + q] = q < nr ? Q[r0 + q + (int64_t)j * ldq] : 0.0;
+            }
+        }
+        wload(0);
+        wstore(0);
+        asm volatile("cp.async.wait_group 0;");
+        __syncthreads();
+        double acc[2][NTW][2];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int n = 0; n < NTW; n++) acc[i][n][0] = acc[i][n][1] = 0.0;
+        for (int c = 0; c < nch; c++) {
+            if (c + 1 < nch) wload(c + 1);
+            const double *wb = wsb + (size_t)(c & 1) * kRC * ldws;
+#pragma unroll
+            for (int ks = 0; ks < kRC / 4; ks++) {
+                const int kk = c * kRC + ks * 4 + tg;
+                const double a0 = tile[(size_t)kk * kLDT + mh * 16 + g];
+                const double a1 = tile[(size_t)kk * kLDT + mh * 16 + 8 + g];
+#pragma unroll
+                for (int n = 0; n < NTW; n++) {
+                    const int nt = nh * NTW + n;
+                    if (nt < NT) {
+                        const double b = wb[(ks * 4 + tg) * ldws + nt * 8 + g];
+                        dmma(acc[0][n][0], acc[0][n][1], a0, b);
+                        dmma(acc[1][n][0], acc[1][n][1], a1, b);
+                    }
+                }
+            }
+            if (c + 1 < nch) wstore((c + 1) & 1);
+            __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const int row = mh * 16 + i * 8 + g;
+            if (row < nr) {
+#pragma unroll
+                for (int n = 0; n < NTW; n++) {
+                    const int col = (nh * NTW + n) * 8 + tg * 2;
+                    if (col < k) Qout[r0 + row + (int64_t)col * ldo] = acc[i][n][0];
+                    if (col + 1 < k) Qout[r0 + row + (int64_t)(col + 1) * ldo] = acc[i][n][1];
+                }
+            }
+        }
+        __syncthreads();  // the tile buffer is reloaded next iteration
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -696,7 +915,7 @@ size_t small_svd_log_doubles(int p) {
     int C, h;
     jacobi_geometry(p, C, h);
     if (!C) return 1;
-    const int64_t per_sweep = (int64_t)(2 * C - 1) * (2 * h - 1) * C * h;
+    const int64_t per_sweep = jacobi_rounds_per_sweep(C, h) * C * h;
     return (size_t)(50 * per_sweep * (sizeof(RotLog) / sizeof(double)));
 }
 
@@ -724,12 +943,14 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
         if (e == cudaSuccess) {
             count_launch();
             const int per_round = C * h;
-            const int rps = (2 * C - 1) * (2 * h - 1);
-            const int R = 4;
-            const int threads = std::min(1024, std::max(32, ((per_round + 31) / 32) * 32));
-            const size_t smem2 = (size_t)R * p * 8 + 2 * (size_t)kLogRounds * per_round * sizeof(RotLog);
+            const int rps = (int)jacobi_rounds_per_sweep(C, h);
+            const int R = std::max(1, std::min(8, 1024 / per_round));
+            const int threads = ((per_round * R + 31) / 32) * 32;
+            const size_t rows_b = (size_t)(R * p + 2) * 8;
+            const int lrc = (int)std::max<size_t>(1, std::min<size_t>(16, (200 * 1024 - rows_b) / (2 * per_round * sizeof(RotLog))));
+            const size_t smem2 = rows_b + 2 * (size_t)lrc * per_round * sizeof(RotLog);
             cudaFuncSetAttribute(k_apply_log, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            k_apply_log<<<(p + R - 1) / R, threads, smem2, s>>>(p, per_round, rps, rlog, ctrl, Vw, R, abort);
+            k_apply_log<<<(p + R - 1) / R, threads, smem2, s>>>(p, per_round, rps, rlog, ctrl, Vw, R, lrc, abort);
             count_launch();
             done = true;
         } else {
@@ -755,8 +976,42 @@ void restart_T(int t, int k, double *T, int ldt, const double *Uh, const double 
     count_launch();
 }
 
+template <int NTW>
+bool launch_recombine_dmma(int64_t N, int t, int k, const double *Q, int64_t ldq, const double *W, int ldw,
+                           double *Qout, int64_t ldo, int nsm, cudaStream_t s) {
+    const int NT = (k + 7) / 8;
+    const int KP = (t + kRC - 1) / kRC * kRC;
+    const int ldws = (NT * 8 + 15) / 16 * 16 + 4;
+    const size_t smem = ((size_t)KP * kLDT + 2 * (size_t)kRC * ldws) * sizeof(double);
+    if (smem > 220 * 1024) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_recombine_dmma<NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_recombine_dmma<NTW>, 128, smem);
+    if (bps < 1) return false;
+    const bool vec = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0);
+    const int64_t ntiles = (N + kRT - 1) / kRT;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nsm * bps));
+    k_recombine_dmma<NTW><<<grid, 128, smem, s>>>(N, t, k, Q, ldq, W, ldw, Qout, ldo, ldws, vec);
+    count_launch();
+    return true;
+}
+
 void recombine(int64_t N, int t, int k, const double *Q, int64_t ldq, const double *W, int ldw, double *Qout,
                int64_t ldo, int nsm, cudaStream_t s) {
+    {
+        const int ntw = ((k + 7) / 8 + 1) / 2;
+        bool ok = false;
+        if (ntw <= 1) ok = launch_recombine_dmma<1>(N, t, k, Q, ldq, W, ldw, Qout, ldo, nsm, s);
+        else if (ntw <= 2) ok = launch_recombine_dmma<2>(N, t, k, Q, ldq, W, ldw, Qout, ldo, nsm, s);
+        else if (ntw <= 4) ok = launch_recombine_dmma<4>(N, t, k, Q, ldq, W, ldw, Qout, ldo, nsm, s);
+        else if (ntw <= 7) ok = launch_recombine_dmma<7>(N, t, k, Q, ldq, W, ldw, Qout, ldo, nsm, s);
+        else if (ntw <= 13) ok = launch_recombine_dmma<13>(N, t, k, Q, ldq, W, ldw, Qout, ldo, nsm, s);
+        if (ok) return;
+    }
     int RT = 64;
     while (RT > 8 && (size_t)t * (RT + 1) * 8 > 100 * 1024) RT >>= 1;
     const size_t smem = (size_t)t * (RT + 1) * sizeof(double);

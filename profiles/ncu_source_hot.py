@@ -13,7 +13,9 @@ def main(path, top=30):
     stall_cols = [i for i, x in enumerate(h) if x.startswith("stall_") and "Not Issued" not in x]
     data = []
     for r in rows[hi + 1:]:
-        if len(r) <= ai:
+        if r[0] == "Kernel Name":
+            break  # next kernel's section
+        if len(r) < len(h):
             continue
         v = float(r[ai] or 0)
         reasons = sorted(((float(r[i] or 0), h[i][6:]) for i in stall_cols), reverse=True)[:3]
