@@ -29,6 +29,7 @@
 
 namespace svdsc {
 unsigned long long *g_ktbuf = nullptr;
+unsigned long long *g_qtbuf = nullptr;  // Q-resident kernel phase timers (SVDSC_KTIMING=1)
 namespace {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -56,29 +57,35 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
     return v;
 }
 
-__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
-// Grid barrier over all CTAs of a cooperative launch: arrival counter +
-// generation word (flags[0], flags[1]); the last CTA to arrive resets the
-// counter and bumps the generation.  (A flag-per-CTA barrier with all-to-all
-// polling measured slower on B200: L2 polling contention.)
-__device__ __forceinline__ void grid_sync(unsigned int *flags, unsigned int) {
+// Grid barrier over all CTAs of a cooperative launch, on a monotonic arrival
+// counter: every CTA adds 1 (red.release, no return value) and polls until the
+// counter reaches n x gridDim.x for the launch's n-th barrier (1.2 us per
+// barrier on B200 vs 2.4 us for a returning atomicAdd + generation flag,
+// tools/barrier_bench.cu).  `v` = epoch + n with epoch a per-launch multiple of
+// 16 (n < 16); launch epoch/16 owns counter slot (epoch/16) % 512, which the
+// previous launch on the stream zeroed (grid_prepare) and the per-solve /
+// per-op Ctrl memset zeroes initially.
+constexpr int kBarSlots = 512;
+__device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void grid_sync(unsigned int *flags, unsigned int v) {
+    unsigned int *ctr = flags + 2 + ((v >> 4) & (kBarSlots - 1));
+    const unsigned int target = (v & 15u) * gridDim.x;
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned int gen = ld_acquire(flags + 1);
         __threadfence();
-        if (atomicAdd(flags, 1u) == gridDim.x - 1) {
-            flags[0] = 0;
-            __threadfence();
-            atomicAdd(flags + 1, 1u);
-        } else {
-            while (ld_acquire(flags + 1) == gen) __nanosleep(20);
+        red_release_add(ctr, 1u);
+        while (ld_acquire(ctr) < target) {
         }
         __threadfence();
     }
     __syncthreads();
+}
+// zero the barrier slot of the NEXT launch (stream order makes this safe)
+__device__ __forceinline__ void grid_prepare(unsigned int *flags, unsigned int epoch) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) flags[2 + (((epoch >> 4) + 1) & (kBarSlots - 1))] = 0u;
 }
 
 constexpr int kTile = 16;
@@ -115,16 +122,18 @@ struct Args {
     int rpb;              // rows per CTA
     int RT;               // row tile of phase B (streaming mode)
     int wsmem;            // keep the CTA's w rows in shared memory
+    unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
 };
 
 // out[j] = sum_b partial[b][j] for the columns owned by this CTA
-__device__ void reduce_cols(const Args &a, int ncols_tot, double *out, double *sh) {
-    const int nb = gridDim.x;
-    for (int j = blockIdx.x; j < ncols_tot; j += nb) {
+__device__ void reduce_cols(const Args &a, int ncols_tot, double *out, double *) {
+    const int nb = gridDim.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int tw = gridDim.x * nw;
+    for (int j = blockIdx.x * nw + (threadIdx.x >> 5); j < ncols_tot; j += tw) {
         double s = 0.0;
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
-        s = block_sum_all(s, sh);
-        if (threadIdx.x == 0) out[j] = s;
+        for (int t = lane; t < nb; t += 32) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
+        s = warp_sum(s);
+        if (lane == 0) out[j] = s;
     }
 }
 
@@ -136,6 +145,13 @@ __device__ __forceinline__ double qval(const Args &a, const double *qsh, int ldq
 
 template <bool QS>
 __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
+    long long tq[12];
+    int ntq = 0;
+    auto qstamp = [&]() {
+        if (a.tdbg && ntq < 12) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq[ntq++]));
+    };
+    qstamp();
+    grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the grid
     unsigned int nbar = 0;
     extern __shared__ double sm[];
@@ -151,19 +167,22 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     double *wsh = hs + ncols + 2;            // rpb (if wsmem)
     double *qsh = wsh + (a.wsmem ? a.rpb : 0);  // QS: ncols x (rpb+1); else tile ncols x (RT+1)
     const int LDT = a.RT + 1;
-    double *part = qsh + (QS ? 0 : (int64_t)ncols * LDT);  // 256
+    double *part = qsh + (QS ? (int64_t)ncols * ldqs : (int64_t)ncols * LDT);  // 256 (QS: row-dot scratch)
     double *wpt = part + 256;                               // RT
     double *wv = a.wsmem ? wsh : (a.w + r0);  // generic pointer to this CTA's rows of w
 
     if (a.wsmem)
         for (int i = tid; i < nr; i += blockDim.x) wsh[i] = a.w[r0 + i];
-    if (QS) {
-        for (int idx = tid; idx < ncols * nr; idx += blockDim.x) {
-            const int j = idx / nr, i = idx - j * nr;
-            qsh[j * ldqs + i] = a.Q[r0 + i + (int64_t)j * a.ldq];
-        }
+    if (QS) {  // the CTA's rows of Q, all copies in flight at once (cp.async, 8 B each)
+        for (int j = wid; j < ncols; j += 8)
+            for (int i = lane; i < nr; i += 32) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(qsh + j * ldqs + i);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(a.Q + r0 + i + (int64_t)j * a.ldq));
+            }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    qstamp();
     if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = a.pre_h[j];
         __syncthreads();
@@ -175,16 +194,54 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
         __syncthreads();
     }
 
+    // QS helpers.  Column dots: one thread per column, four interleaved chains
+    // over the CTA's rows (ldqs odd: the 32 columns of a warp hit 32 banks).
+    auto qs_coldots = [&](const double *v) {
+        for (int j = tid; j < ncols; j += blockDim.x) {
+            const double *qj = qsh + j * ldqs;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int i = 0;
+            for (; i + 4 <= nr; i += 4) {
+                s0 = fma(qj[i], v[i], s0);
+                s1 = fma(qj[i + 1], v[i + 1], s1);
+                s2 = fma(qj[i + 2], v[i + 2], s2);
+                s3 = fma(qj[i + 3], v[i + 3], s3);
+            }
+            for (; i < nr; i++) s0 = fma(qj[i], v[i], s0);
+            a.partial[(int64_t)blockIdx.x * a.PS + j] = (s0 + s1) + (s2 + s3);
+        }
+    };
+    // Row dots Q_b h: thread (row i, column group g) sums columns g, g + G, ...;
+    // the G partials of a row are combined in fixed order.  Result in rdot[i].
+    double *rdot = part;  // >= 256 doubles of scratch (part region)
+    auto qs_rowdots = [&](const double *h) {
+        const int G = max(1, (int)blockDim.x / max(nr, 1));
+        const int i = tid % max(nr, 1), g = tid / max(nr, 1);
+        double s0 = 0.0, s1 = 0.0;
+        if (g < G && i < nr) {
+            int j = g;
+            for (; j + G < ncols; j += 2 * G) {
+                s0 = fma(qsh[j * ldqs + i], h[j], s0);
+                s1 = fma(qsh[(j + G) * ldqs + i], h[j + G], s1);
+            }
+            if (j < ncols) s0 = fma(qsh[j * ldqs + i], h[j], s0);
+        }
+        __syncthreads();
+        if (g < G && i < nr) rdot[g * nr + i] = s0 + s1;
+        __syncthreads();
+        if (tid < nr) {
+            double t = 0.0;
+            for (int q = 0; q < G; q++) t += rdot[q * nr + tid];
+            rdot[tid] = t;  // (G partials of row tid read above by this thread only)
+        }
+        __syncthreads();
+    };
+
     double nrm_wp = 0.0;  // ||w'||^2 partial (thread-local)
     if (ncols > 0) {
         // ---------------- phase A: partial h1 ----------------
         if (QS) {
-            for (int j = wid; j < ncols; j += 8) {
-                double s = 0.0;
-                for (int i = lane; i < nr; i += 32) s = fma(qsh[j * ldqs + i], wv[i], s);
-                s = warp_sum(s);
-                if (lane == 0) a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
-            }
+            qs_coldots(wv);
         } else {
             for (int j0 = 0; j0 < ncols; j0 += kTile) {
                 const int nc = min(kTile, ncols - j0);
@@ -210,28 +267,24 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
                 __syncthreads();
             }
         }
+        qstamp();
         grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, ncols, a.h1, sh);
         grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
         __syncthreads();
+        qstamp();
 
         // ---------------- phase B: w' = w - Q h1, partial h2, ||w'||^2 ----------------
         if (QS) {
+            qs_rowdots(hs);
             for (int i = tid; i < nr; i += blockDim.x) {
-                double s = 0.0;
-                for (int j = 0; j < ncols; j++) s = fma(qsh[j * ldqs + i], hs[j], s);
-                const double v = wv[i] - s;
+                const double v = wv[i] - rdot[i];
                 wv[i] = v;
                 nrm_wp = fma(v, v, nrm_wp);
             }
             __syncthreads();
-            for (int j = wid; j < ncols; j += 8) {
-                double s = 0.0;
-                for (int i = lane; i < nr; i += 32) s = fma(qsh[j * ldqs + i], wv[i], s);
-                s = warp_sum(s);
-                if (lane == 0) a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
-            }
+            qs_coldots(wv);
         } else {
             const int RT = a.RT, P = blockDim.x / RT;
             const int rr = tid % RT, pp = tid / RT;
@@ -279,11 +332,13 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
         }
         const double bn = block_sum_all(nrm_wp, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+        qstamp();
         grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, ncols + 1, a.h2, sh);
         grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j <= ncols; j += blockDim.x) hs[j] = __ldcg(a.h2 + j);
         __syncthreads();
+        qstamp();
     } else {
         // plain norm: ||w||^2 into hs[0] (ncols == 0)
         for (int i = tid; i < nr; i += blockDim.x) nrm_wp = fma(wv[i], wv[i], nrm_wp);
@@ -305,13 +360,22 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     const bool pyth = beta2 > 0.5 * nrmp;
     double nrm2 = 0.0;
     if (ncols > 0) {
-        for (int i = tid; i < nr; i += blockDim.x) {
-            double s = 0.0;
+        if (QS) {
+            qs_rowdots(hs);
+            for (int i = tid; i < nr; i += blockDim.x) {
+                const double v = wv[i] - rdot[i];
+                wv[i] = v;
+                nrm2 = fma(v, v, nrm2);
+            }
+        } else {
+            for (int i = tid; i < nr; i += blockDim.x) {
+                double s = 0.0;
 #pragma unroll 8
-            for (int j = 0; j < ncols; j++) s = fma(qval<QS>(a, qsh, ldqs, r0, i, j), hs[j], s);
-            const double v = wv[i] - s;
-            wv[i] = v;
-            nrm2 = fma(v, v, nrm2);
+                for (int j = 0; j < ncols; j++) s = fma(qval<QS>(a, qsh, ldqs, r0, i, j), hs[j], s);
+                const double v = wv[i] - s;
+                wv[i] = v;
+                nrm2 = fma(v, v, nrm2);
+            }
         }
     }
     __syncthreads();
@@ -338,8 +402,13 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
             a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
         }
     }
-    if (bd) return;
-    for (int i = tid; i < nr; i += blockDim.x) a.w[r0 + i] = wv[i] / beta;
+    if (!bd)
+        for (int i = tid; i < nr; i += blockDim.x) a.w[r0 + i] = wv[i] / beta;
+    qstamp();
+    if (a.tdbg && tid == 0 && blockIdx.x == 0 && ntq == 7) {
+        for (int q = 1; q < 7; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tq[q] - tq[q - 1]));
+        atomicAdd(a.tdbg + 7, 1ull);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -457,19 +526,23 @@ __device__ __forceinline__ void tile_coldot(const double *T, const double *x, in
     }
 }
 
-__device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double *sh) {
-    const int nb = gridDim.x;
-    for (int j = blockIdx.x; j < ncols_tot; j += nb) {
+// one warp per column (fixed lane-strided order + xor tree: deterministic);
+// a block-wide reduction per column cost ~2 us per column (3 __syncthreads)
+__device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double *) {
+    const int nb = gridDim.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int tw = gridDim.x * nw;
+    for (int j = blockIdx.x * nw + (threadIdx.x >> 5); j < ncols_tot; j += tw) {
         double s = 0.0;
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
-        s = block_sum_all(s, sh);
-        if (threadIdx.x == 0) out[j] = s;
+        for (int t = lane; t < nb; t += 32) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
+        s = warp_sum(s);
+        if (lane == 0) out[j] = s;
     }
 }
 
 template <int RT, int kSThr, int NS>
 __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
     constexpr int NQ = 1024 / kSThr;  // columns per thread (ncols <= 1024)
+    grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
     unsigned int nbar = 0;
     extern __shared__ __align__(16) double smem_s[];
@@ -656,6 +729,7 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
 template <int RT, int NS, int M>
 __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     constexpr int kSThr = 512, NW = 16, RPW = RT / NW, kCh = RT / 2;
+    grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
     unsigned int nbar = 0;
     extern __shared__ __align__(16) double smem_s[];
@@ -994,90 +1068,105 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-// named barrier over the 16 consumer warps (the producer warp never joins)
+// named barrier over the 16 warps (row-dot partial exchange)
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
-constexpr int kTmaNW = 16;           // consumer warps
-constexpr int kTmaThreads = 17 * 32; // + one producer warp
+constexpr int kTmaNW = 16;           // warps; thread 0 also issues the copies
+constexpr int kTmaThreads = kTmaNW * 32;  // 4 warps per SMSP: up to 128 registers per thread
+                                           // (a 17th, producer-only warp capped them at 96)
 constexpr int kTmaRT = 32;           // rows per tile
 constexpr int kTmaMaxNS = 8;
 
 template <int M>
-__global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap tq, SArgs a, int ns) {
+__global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_constant__ CUtensorMap tq, SArgs a, int ns,
+                                                             int nsplit) {
     constexpr int RT = kTmaRT, NW = kTmaNW, J = M;
+    unsigned long long g_entry = 0;
+    if (a.tdbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+    grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
     unsigned int nbar = 0;
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full[kTmaMaxNS], empty[kTmaMaxNS];
     __shared__ double sh[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const bool producer = wid == NW;
-    const int ptid = NW * 32;  // the producer thread
+    constexpr bool producer = false;  // no producer-only warp
+    const int ptid = 0;               // the thread that issues the copies
     const int ncols = a.ncols;
     const int nbox = (ncols + 15) >> 4;
-    const int stage_d = nbox * 512 + RT;  // doubles per stage: boxes, then the tile's w rows
+    // a tile is split into nsplit column groups, each its own pipeline unit
+    // (stage): warps [g NW/nsplit, (g+1) NW/nsplit) own the group's columns,
+    // so more, smaller units are in flight per tile (a full-width 32 x 300
+    // tile is 77 KB: only two fit)
+    const int wpg = NW / nsplit;            // warps per group
+    const int gbox = wpg * M / 16;          // boxes per group
+    const int grp = wid / wpg;              // this warp's group
+    const int stage_d = gbox * 512 + RT;    // doubles per unit: boxes, then the tile's w rows
     double *smem_t = smem_raw;
     double *rpart = smem_t + (size_t)ns * stage_d;  // [2][NW][RT] row-dot partials
     double *hs = rpart + 2 * NW * RT;               // coefficient vector of the current sweep (ncols)
     const int64_t rb = (int64_t)blockIdx.x * a.rpb;
     const int64_t re = min(a.N, rb + a.rpb);
     const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
-    const unsigned tx_bytes = (unsigned)(nbox * 4096 + RT * 8);
+    const int nunits = ntiles * nsplit;
     if (tid == ptid) {
         for (int q = 0; q < ns; q++) {
             mbar_init(&full[q], 1);
-            mbar_init(&empty[q], NW);
+            mbar_init(&empty[q], wpg);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     // producer state (meaningful in the producer thread only)
-    int g_issue = 0, k_issued = 0;
-    // consumer state
-    int g_use = 0;
+    int g_issue = 0, u_issued = 0;
     int sweep_no = 0;
     auto tile_of = [&](int k) { return (sweep_no & 1) ? ntiles - 1 - k : k; };
-    auto issue_next = [&]() {  // producer thread: next tile of the current sweep into the ring
+    auto issue_next = [&]() {  // producer thread: next unit of the current sweep into the ring
         const int st = g_issue % ns;
         if (g_issue >= ns) mbar_wait(&empty[st], (unsigned)(((g_issue / ns) - 1) & 1));
-        const int64_t r0 = rb + (int64_t)tile_of(k_issued) * RT;
+        const int k = u_issued / nsplit, g = u_issued % nsplit;
+        const int64_t r0 = rb + (int64_t)tile_of(k) * RT;
+        const int b0 = g * gbox, b1 = min(nbox, b0 + gbox);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[st], tx_bytes);
+        mbar_expect_tx(&full[st], (unsigned)(max(0, b1 - b0) * 4096 + RT * 8));
         double *dst = smem_t + (size_t)st * stage_d;
-        for (int b = 0; b < nbox; b++) tma_load_2d(dst + b * 512, &tq, (int)r0, 16 * b, &full[st]);
-        bulk_load(dst + nbox * 512, a.w + r0, RT * 8, &full[st]);
+        for (int b = b0; b < b1; b++) tma_load_2d(dst + (b - b0) * 512, &tq, (int)r0, 16 * b, &full[st]);
+        bulk_load(dst + gbox * 512, a.w + r0, RT * 8, &full[st]);
         g_issue++;
-        k_issued++;
+        u_issued++;
     };
-    auto prefetch = [&]() {  // first stages of the current sweep (before a grid barrier)
+    auto prefetch = [&]() {  // first units of the current sweep (before a grid barrier)
         if (tid == ptid)
-            while (k_issued < ntiles && k_issued < ns) issue_next();
+            while (u_issued < nunits && u_issued < ns) issue_next();
     };
+    // consumer: unit of tile k for this warp's group is global use index
+    // base + k nsplit + grp (units are issued in that order)
+    int use_base = 0;
     auto run_tiles = [&](auto &&body) {
         if (ntiles > 0) {
-            if (producer) {
-                if (lane == 0)
-                    while (k_issued < ntiles) issue_next();
-            } else {
-                for (int k = 0; k < ntiles; k++) {
-                    const int st = g_use % ns;
-                    mbar_wait(&full[st], (unsigned)((g_use / ns) & 1));
-                    const double *T = smem_t + (size_t)st * stage_d;
-                    body(tile_of(k), k, T, T + nbox * 512);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[st]);
-                    g_use++;
-                }
+            for (int k = 0; k < ntiles; k++) {
+                // keep ns units in flight: unit u goes into the stage of unit
+                // u - ns (a tile <= k - 1), released before tile k is entered
+                if (tid == ptid)
+                    while (u_issued < nunits && u_issued < k * nsplit + ns) issue_next();
+                const int gu = use_base + k * nsplit + grp;
+                const int st = gu % ns;
+                mbar_wait(&full[st], (unsigned)((gu / ns) & 1));
+                const double *T = smem_t + (size_t)st * stage_d;
+                body(tile_of(k), k, T, T + gbox * 512);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
             }
         }
+        use_base += nunits;
         sweep_no++;
-        k_issued = 0;
+        u_issued = 0;
     };
     // element of the thread's row (lane) and column w M + j
     const int row = lane;
     auto colof = [&](int j) { return wid * M + j; };
-    auto qaddr = [&](int j) {
-        const int c = colof(j);
+    auto qaddr = [&](int j) {  // within the group's stage
+        const int c = colof(j) - grp * wpg * M;
         return ((c >> 4) << 9) + ((c & 15) << 5) + row;
     };
     auto load_q = [&](const double *T, double (&q)[J]) {
@@ -1128,13 +1217,19 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
             load_q(T, q);
             const double s = row_dot(k, q);
             const int64_t r = rb + (int64_t)kt * RT + row;
-            if (wid == 0 && r < re) a.w[r] = W[row] - s;
+            if (wid == NW - 1 && r < re) a.w[r] = W[row] - s;
         });
         __threadfence();
         asm volatile("fence.proxy.async.global;" ::: "memory");
         grid_sync(a.flags, a.epoch + (++nbar));
     }
 
+    long long tk[8];
+    int ntk = 0;
+    auto stamp = [&]() {
+        if (a.tdbg && ntk < 8) tk[ntk++] = clock64();
+    };
+    stamp();
     double nrm_wp = 0.0;
     if (ncols > 0) {
         double acc[J];
@@ -1150,10 +1245,14 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
         });
         flush_cols(acc);
         prefetch();
+        stamp();
         grid_sync(a.flags, a.epoch + (++nbar));
+        stamp();
         sreduce_cols(a, ncols, a.h1, sh);
+        stamp();
         grid_sync(a.flags, a.epoch + (++nbar));
         load_h(a.h1);
+        stamp();
 #pragma unroll
         for (int j = 0; j < J; j++) acc[j] = 0.0;
         // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
@@ -1163,7 +1262,7 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
             const double s = row_dot(k, q);
             const int64_t r = rb + (int64_t)kt * RT + row;
             const double v = (r < re) ? W[row] - s : 0.0;
-            if (wid == 0 && r < re) {
+            if (wid == NW - 1 && r < re) {
                 a.w[r] = v;
                 nrm_wp = fma(v, v, nrm_wp);
             }
@@ -1174,7 +1273,7 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
     } else {
         run_tiles([&](int kt, int, const double *, const double *W) {
             const int64_t r = rb + (int64_t)kt * RT + row;
-            if (wid == 0 && r < re) nrm_wp = fma(W[row], W[row], nrm_wp);
+            if (wid == NW - 1 && r < re) nrm_wp = fma(W[row], W[row], nrm_wp);
         });
     }
     {
@@ -1187,16 +1286,15 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
         __syncthreads();
         prefetch();
     }
+    stamp();
     grid_sync(a.flags, a.epoch + (++nbar));
     sreduce_cols(a, ncols + 1, a.h2, sh);
     grid_sync(a.flags, a.epoch + (++nbar));
     load_h(a.h2);
+    stamp();
     const double nrmp = __ldcg(a.h2 + ncols);
     double hh = 0.0;
-    for (int j = tid; j < ncols; j += kTmaThreads) {
-        const double x = __ldcg(a.h2 + j);
-        hh = fma(x, x, hh);
-    }
+    for (int j = tid; j < ncols; j += kTmaThreads) hh = fma(hs[j], hs[j], hh);
     hh = block_sum_all(hh, sh);
     double beta2 = nrmp - hh;
     const bool pyth = beta2 > 0.5 * nrmp;
@@ -1213,7 +1311,7 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
                 load_q(T, q);
                 const double s = row_dot(k, q);
                 const int64_t r = rb + (int64_t)kt * RT + row;
-                if (wid == 0 && r < re) a.w[r] = (W[row] - s) / beta;
+                if (wid == NW - 1 && r < re) a.w[r] = (W[row] - s) / beta;
             });
         } else if (!bd) {
             for (int64_t r = rb + tid; r < re; r += kTmaThreads) a.w[r] = a.w[r] / beta;
@@ -1226,7 +1324,7 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
                 load_q(T, q);
                 const double s = row_dot(k, q);
                 const int64_t r = rb + (int64_t)kt * RT + row;
-                if (wid == 0 && r < re) {
+                if (wid == NW - 1 && r < re) {
                     const double v = W[row] - s;
                     a.w[r] = v;
                     nrm2 = fma(v, v, nrm2);
@@ -1245,14 +1343,23 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
         if (!bd)
             for (int64_t r = rb + tid; r < re; r += kTmaThreads) a.w[r] = a.w[r] / beta;
     }
+    stamp();
+    if (a.tdbg && tid == 0 && ntk == 8) {
+        for (int q = 1; q < 8; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
+        atomicAdd(a.tdbg + 10, 1ull);
+        atomicAdd(a.tdbg + 11, (unsigned long long)ntiles);
+        if (blockIdx.x == 0) {
+            unsigned long long g_exit;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+            atomicAdd(a.tdbg + 8, g_exit - g_entry);  // ns, CTA 0 entry -> exit
+            atomicAdd(a.tdbg + 9, (unsigned long long)(tk[0] - 0));
+        }
+    }
     // phase C prefetched but skipped (breakdown): wait for those copies so
     // that no bulk copy is in flight when the CTA exits
-    if (!producer && ncols > 0 && pyth && bd) {
-        for (int q = 0; q < min(ntiles, ns); q++) {
-            const int st = g_use % ns;
-            mbar_wait(&full[st], (unsigned)((g_use / ns) & 1));
-            g_use++;
-        }
+    if (tid == ptid && ncols > 0 && pyth && bd) {
+        for (int gu = use_base; gu < use_base + min(nunits, ns); gu++)
+            mbar_wait(&full[gu % ns], (unsigned)((gu / ns) & 1));
     }
     if (blockIdx.x == 0 && tid == 0) {
         if (bd) {
@@ -1271,12 +1378,18 @@ __global__ void __maxnreg__(112) k_cgs2_tma(const __grid_constant__ CUtensorMap 
 template <int M>
 bool launch_tma(const CUtensorMap &tq, const SArgs &a0, int nsm, cudaStream_t s) {
     SArgs a = a0;
-    const int nbox = (a.ncols + 15) / 16;
-    const size_t stage_b = ((size_t)nbox * 512 + kTmaRT) * sizeof(double);
-    const size_t fixed = ((size_t)2 * kTmaNW * kTmaRT + a.ncols + 2) * sizeof(double) + 128;
     if (a.ncols > kTmaNW * M) return false;
+    // column groups per tile: smallest split with units <= ~48 KB (deeper ring)
+    int nsplit = 1;
+    int unit_kb = 1024;  // SVDSC_TMA_UNIT_KB: split tiles into column groups of at most this many KB
+    if (const char *e = getenv("SVDSC_TMA_UNIT_KB")) unit_kb = atoi(e);
+    while (nsplit < 4 && (kTmaNW / nsplit) * M * 32 * 8 > unit_kb * 1024 && (M * (kTmaNW / (2 * nsplit))) % 16 == 0)
+        nsplit *= 2;
+    const int gbox = (kTmaNW / nsplit) * M / 16;
+    const size_t stage_b = ((size_t)gbox * 512 + kTmaRT) * sizeof(double);
+    const size_t fixed = ((size_t)2 * kTmaNW * kTmaRT + a.ncols + 2) * sizeof(double) + 128;
     const int ns = (int)std::min<size_t>(kTmaMaxNS, (200 * 1024 - fixed) / stage_b);
-    if (ns < 2) return false;
+    if (ns < 2 * nsplit) return false;
     const size_t smem = ns * stage_b + fixed;
     static bool attr = false;
     if (!attr) {
@@ -1292,7 +1405,7 @@ bool launch_tma(const CUtensorMap &tq, const SArgs &a0, int nsm, cudaStream_t s)
     a.rpb = rpb;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
     CUtensorMap map = tq;
-    void *args[] = {&map, &a, (void *)&ns};
+    void *args[] = {&map, &a, (void *)&ns, (void *)&nsplit};
     if (cudaLaunchCooperativeKernel((void *)k_cgs2_tma<M>, grid, kTmaThreads, args, smem, s) != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -1368,14 +1481,23 @@ bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_
 
 // debugging aid (SVDSC_KTIMING=1): per-phase cycle counters of the TMA kernel
 void ktiming_dump() {
+    if (g_qtbuf) {
+        unsigned long long q[16];
+        cudaMemcpy(q, g_qtbuf, sizeof(q), cudaMemcpyDeviceToHost);
+        cudaMemset(g_qtbuf, 0, sizeof(q));
+        const double n = q[7] ? (double)q[7] : 1.0;
+        fprintf(stderr, "[qtiming] calls=%llu  loadQ=%.0f phaseA=%.0f red1=%.0f phaseB=%.0f red2=%.0f phaseC=%.0f ns (CTA 0)\n",
+                q[7], q[0] / n, q[1] / n, q[2] / n, q[3] / n, q[4] / n, q[5] / n);
+    }
     if (!g_ktbuf) return;
     unsigned long long h[16];
     cudaMemcpy(h, g_ktbuf, sizeof(h), cudaMemcpyDeviceToHost);
     cudaMemset(g_ktbuf, 0, sizeof(h));
-    const double n = h[6] ? (double)h[6] : 1.0;
+    const double n = h[10] ? (double)h[10] : 1.0;
     fprintf(stderr,
-            "[ktiming] calls(x CTAs)=%llu avg tiles/CTA=%.1f  phaseA=%.0f red1=%.0f phaseB=%.0f red2=%.0f phaseC=%.0f cycles\n",
-            h[6], h[7] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n);
+            "[ktiming] calls(x CTAs)=%llu avg tiles/CTA=%.1f  phaseA=%.0f wait1=%.0f reduce1=%.0f bar2+load=%.0f "
+            "phaseB=%.0f red2=%.0f phaseC=%.0f cycles  CTA0 entry->exit total %.3f ms\n",
+            h[10], h[11] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[8] * 1e-6);
 }
 
 // returns false if the fused path cannot be used (caller falls back)
@@ -1401,13 +1523,25 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     a.t_entry = t_entry;
     a.check = check;
     a.pre_h = pre_h;
+    a.tdbg = nullptr;
+    if (const char *kt = getenv("SVDSC_KTIMING")) {
+        if (kt[0] == '1') {
+            if (!g_qtbuf) {
+                cudaMalloc(&g_qtbuf, 16 * sizeof(unsigned long long));
+                cudaMemset(g_qtbuf, 0, 16 * sizeof(unsigned long long));
+            }
+            a.tdbg = g_qtbuf;
+        }
+    }
     // try Q-resident mode: 2 CTAs per SM, then 1 (SVDSC_FORCE_STREAM=1 skips it: test hook)
     const char *fse = getenv("SVDSC_FORCE_STREAM");
     const bool force_stream = fse && fse[0] == '1';
-    for (int per_sm = 2; per_sm >= 1 && !force_stream; per_sm--) {
+    int qs_first = 1;  // CTAs per SM tried first: 1 measured faster (fewer CTAs in each grid barrier / reduction); SVDSC_QS_PER_SM overrides
+    if (const char *e = getenv("SVDSC_QS_PER_SM")) qs_first = std::max(1, std::min(2, atoi(e)));
+    for (int per_sm = qs_first; per_sm >= 1 && !force_stream; per_sm--) {
         const int nb = nsm * per_sm;
         const int64_t rpb = (N + nb - 1) / nb;
-        const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1)) * sizeof(double);
+        const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1) + 256) * sizeof(double);
         if (ncols > 0 && smem * per_sm <= 220 * 1024 && smem <= smem_cap && rpb >= 1) {
             a.rpb = (int)rpb;
             a.RT = 1;

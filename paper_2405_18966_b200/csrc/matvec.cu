@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <vector>
 
@@ -546,6 +547,8 @@ void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, c
             int bps = 0, dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            if (const char *co = getenv("SVDSC_CARVEOUT"))  // experiment: shared-memory carveout of the SpMV
+                cudaFuncSetAttribute(k_spmv_bins, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_bins, 256, 0);
             wave = std::max(1, bps) * nsm;
         }

