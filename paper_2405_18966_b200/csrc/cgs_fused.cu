@@ -213,9 +213,23 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     };
     // Row dots Q_b h: thread (row i, column group g) sums columns g, g + G, ...;
     // the G partials of a row are combined in fixed order.  Result in rdot[i].
-    double *rdot = part;  // >= 256 doubles of scratch (part region)
+    double *rdot = part;  // >= max(256, rpb) doubles of scratch (part region)
     auto qs_rowdots = [&](const double *h) {
-        const int G = max(1, (int)blockDim.x / max(nr, 1));
+        const int G = (int)blockDim.x / max(nr, 1);
+        if (G <= 1) {  // at least as many rows as threads: one thread per row
+            for (int i = tid; i < nr; i += blockDim.x) {
+                double s0 = 0.0, s1 = 0.0;
+                int j = 0;
+                for (; j + 1 < ncols; j += 2) {
+                    s0 = fma(qsh[j * ldqs + i], h[j], s0);
+                    s1 = fma(qsh[(j + 1) * ldqs + i], h[j + 1], s1);
+                }
+                if (j < ncols) s0 = fma(qsh[j * ldqs + i], h[j], s0);
+                rdot[i] = s0 + s1;
+            }
+            __syncthreads();
+            return;
+        }
         const int i = tid % max(nr, 1), g = tid / max(nr, 1);
         double s0 = 0.0, s1 = 0.0;
         if (g < G && i < nr) {
@@ -1541,7 +1555,7 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     for (int per_sm = qs_first; per_sm >= 1 && !force_stream; per_sm--) {
         const int nb = nsm * per_sm;
         const int64_t rpb = (N + nb - 1) / nb;
-        const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1) + 256) * sizeof(double);
+        const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1) + std::max<int64_t>(256, rpb)) * sizeof(double);
         if (ncols > 0 && smem * per_sm <= 220 * 1024 && smem <= smem_cap && rpb >= 1) {
             a.rpb = (int)rpb;
             a.RT = 1;

@@ -139,7 +139,7 @@ def test_cgs2(S, H, N, c):
 @pytest.mark.parametrize("variant", ["qs", "stream", "stream2", "tma"])
 @pytest.mark.parametrize("N,c", [(10007, 37), (200000, 300), (4096, 150), (1250, 64), (333, 5), (4096, 65),
                                  (4096, 96), (4096, 128), (4096, 129), (65536, 150), (70001, 257),
-                                 (4096, 600), (30011, 17)])
+                                 (4096, 600), (30011, 17), (70001, 9), (40000, 30)])
 def test_cgs2_fused_variants(S, H, N, c, variant, monkeypatch):
     """The solver's fused CGS2 + normalize kernels (Q-resident, cp.async
     streaming, register-blocked streaming, TMA streaming) against the oracle."""
