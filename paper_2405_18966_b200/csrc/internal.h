@@ -53,8 +53,18 @@ struct CsrOp {
     int32_t *chunk_row = nullptr;      // long-row slot per chunk
     int64_t n_long = 0, n_chunks = 0;
     double *chunk_partial = nullptr;   // n_chunks
+    // nnz-balanced ("merge") schedule: tile t = nonzeros [t*kMergeTile, (t+1)*kMergeTile)
+    int64_t n_tiles = 0;
+    int32_t *tile_r0 = nullptr;        // first row of tile t (row holding nonzero t*kMergeTile; 0 for t = 0)
+    int32_t *tile_r1 = nullptr;        // last row of tile t (inclusive; trailing empty rows belong to the last tile)
+    double *tile_head = nullptr;       // partial sum of tile t's first row when it began before the tile
+    double *tile_tail = nullptr;       // partial sum of tile t's last row when it continues after the tile
+    int64_t n_span = 0;                // rows spanning tile boundaries
+    int32_t *span_row = nullptr, *span_t0 = nullptr, *span_t1 = nullptr;  // row, first and last tile
+    bool merge = false;                // use the merge schedule for this operand
     std::vector<void *> owned;         // allocations owned by this operand
 };
+constexpr int kMergeTile = 2048;       // nonzeros per merge tile (256 threads x 8)
 
 struct DenseOp {
     int64_t nrows = 0, ncols = 0, ld = 0;

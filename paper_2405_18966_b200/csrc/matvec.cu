@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -197,6 +198,141 @@ __global__ void __launch_bounds__(256) k_spmv_cta(const int32_t *__restrict__ ro
         for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) sum = fma(val[p], __ldg(x + col[p]), sum);
         sum = block_sum_256(sum, sh);
         if (threadIdx.x == 0) epilogue_store(y, r, sum, c, yprev);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// nnz-balanced ("merge") SpMV: every CTA takes kMergeTile consecutive nonzeros
+// whatever the row lengths (power-law rows, CSC columns), so the A stream is
+// perfectly balanced and fully coalesced.  Phase 1: thread j computes the 8
+// products val[p] * x[col[p]] of p = e0 + 8j .. 8j+7 (128-bit loads, 8 gathers
+// in flight) into shared memory.  Phase 2: the tile's rows [r0, r1] are summed
+// from shared memory -- one thread per row for slices <= 32, one warp per row
+// (lane-strided + xor tree) for longer ones.  Rows wholly inside the tile are
+// finished (y = sum - c yprev); a row that began before the tile leaves its
+// part in tile_head[t], one that continues after it in tile_tail[t]; a fixup
+// kernel adds those in tile order.  Deterministic.
+__global__ void __launch_bounds__(256) k_spmv_merge(int64_t nnz, const int32_t *__restrict__ tile_r0,
+                                                    const int32_t *__restrict__ tile_r1,
+                                                    const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                                    const double *__restrict__ val, const double *__restrict__ x,
+                                                    double *__restrict__ y, const double *c_dev,
+                                                    const double *__restrict__ yprev, double *head, double *tail,
+                                                    const int *abort) {
+    if (aborted(abort)) return;
+    __shared__ __align__(16) double prod[kMergeTile];
+    __shared__ int32_t longq[256];
+    __shared__ int nlong;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t t = blockIdx.x;
+    const int64_t e0 = t * kMergeTile, e1 = min(nnz, e0 + kMergeTile);
+    const double c = c_dev ? *c_dev : 0.0;
+    if (tid == 0) nlong = 0;
+    {
+        const int64_t p = e0 + 8 * tid;
+        double v[8];
+        int ci[8];
+        if (p + 8 <= e1) {
+            const int4 *cp = reinterpret_cast<const int4 *>(col + p);
+            const double2 *vp = reinterpret_cast<const double2 *>(val + p);
+            const int4 c0 = __ldcs(cp), c1 = __ldcs(cp + 1);
+            ci[0] = c0.x; ci[1] = c0.y; ci[2] = c0.z; ci[3] = c0.w;
+            ci[4] = c1.x; ci[5] = c1.y; ci[6] = c1.z; ci[7] = c1.w;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const double2 d = __ldcs(vp + u);
+                v[2 * u] = d.x;
+                v[2 * u + 1] = d.y;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const bool ok = p + u < e1;
+                ci[u] = ok ? __ldcs(col + p + u) : 0;
+                v[u] = ok ? __ldcs(val + p + u) : 0.0;
+            }
+        }
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) xv[u] = __ldg(x + ci[u]);
+#pragma unroll
+        for (int u = 0; u < 8; u++) prod[8 * tid + u] = v[u] * xv[u];
+    }
+    __syncthreads();
+    const int r0 = tile_r0[t], r1 = tile_r1[t];
+    auto finish = [&](int r, int64_t a, int64_t b, double sum) {
+        if (rp[r] >= e0) {  // row began inside this tile
+            if (rp[r + 1] <= e1) {
+                if (yprev) sum -= c * yprev[r];
+                y[r] = sum;
+            } else {
+                tail[t] = sum;
+            }
+        } else {
+            head[t] = sum;
+        }
+    };
+    for (int r = r0 + tid; r <= r1; r += 256) {
+        const int64_t a = max(rp[r], e0), b = min(rp[r + 1], e1);
+        if (b - a > 32) {
+            const int q = atomicAdd(&nlong, 1);
+            if (q < 256) longq[q] = r;
+            continue;
+        }
+        double s0 = 0.0, s1 = 0.0;
+        int64_t i = a;
+        for (; i + 1 < b; i += 2) {
+            s0 += prod[i - e0];
+            s1 += prod[i + 1 - e0];
+        }
+        if (i < b) s0 += prod[i - e0];
+        finish(r, a, b, s0 + s1);
+    }
+    __syncthreads();
+    const int nl = min(nlong, 256);  // a tile holds at most kMergeTile / 33 < 256 long slices
+    for (int q = wid; q < nl; q += 8) {
+        const int r = longq[q];
+        const int64_t a = max(rp[r], e0), b = min(rp[r + 1], e1);
+        double s = 0.0;
+        for (int64_t i = a + lane; i < b; i += 32) s += prod[i - e0];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) finish(r, a, b, s);
+    }
+}
+
+// rows spanning tiles: y = tail[t0] + head[t0+1] + ... + head[t1] - c yprev
+__global__ void k_spmv_merge_fix(int64_t n_span, const int32_t *__restrict__ span_row,
+                                 const int32_t *__restrict__ span_t0, const int32_t *__restrict__ span_t1,
+                                 const double *__restrict__ head, const double *__restrict__ tail, double *y,
+                                 const double *c_dev, const double *__restrict__ yprev, const int *abort) {
+    if (aborted(abort)) return;
+    const double c = c_dev ? *c_dev : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_span; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = span_row[i];
+        double s = tail[span_t0[i]];
+        for (int t = span_t0[i] + 1; t <= span_t1[i]; t++) s += head[t];
+        if (yprev) s -= c * yprev[r];
+        y[r] = s;
+    }
+}
+
+// tile_r0[t] = row holding nonzero t * kMergeTile (largest r with rp[r] <= e0 and rp[r+1] > e0)
+__global__ void k_merge_tiles(int64_t nrows, int64_t nnz, int64_t n_tiles, const int64_t *__restrict__ rp,
+                              int32_t *r0) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t == 0) {
+            r0[0] = 0;
+            continue;
+        }
+        const int64_t e0 = t * kMergeTile;
+        int64_t lo = 0, hi = nrows;  // find largest r with rp[r] <= e0 (rp[nrows] = nnz > e0)
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) / 2;
+            if (rp[mid] <= e0) lo = mid;
+            else hi = mid;
+        }
+        r0[t] = (int32_t)lo;
     }
 }
 
@@ -458,6 +594,67 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
         check(cudaMemcpyAsync(op.chunk_first, first.data(), (op.n_long + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s), "H2D");
         check(cudaMemcpyAsync(op.chunk_row, crow.data(), nch * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
     }
+    // nnz-balanced merge schedule for operands with long rows (CTA-per-row and
+    // chunked bins non-empty: power-law rows), where the binned launches
+    // serialize and imbalance; measured 21% faster there (config 4), 35% slower
+    // on uniform rows (config 3).  SVDSC_SPMV=merge|bins forces either.
+    {
+        const char *sv = getenv("SVDSC_SPMV");
+        const bool aligned = ((reinterpret_cast<uintptr_t>(op.col) & 31) == 0) &&
+                             ((reinterpret_cast<uintptr_t>(op.val) & 63) == 0);
+        const bool long_rows = off[7] > off[5];
+        const bool want = sv ? std::string(sv) == "merge" : long_rows;
+        if (op.nnz > 0 && op.nrows < (int64_t)INT32_MAX && aligned && want) {
+            const int64_t nt = (op.nnz + kMergeTile - 1) / kMergeTile;
+            op.n_tiles = nt;
+            op.tile_r0 = dev_alloc<int32_t>(op, nt);
+            op.tile_r1 = dev_alloc<int32_t>(op, nt);
+            op.tile_head = dev_alloc<double>(op, nt);
+            op.tile_tail = dev_alloc<double>(op, nt);
+            k_merge_tiles<<<grid_for(nt, 256), 256, 0, s>>>(op.nrows, op.nnz, nt, op.row_ptr, op.tile_r0);
+            std::vector<int32_t> r0(nt);
+            std::vector<int64_t> rp0(nt);
+            check(cudaMemcpyAsync(r0.data(), op.tile_r0, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
+            check(cudaStreamSynchronize(s), "sync");
+            // rp[r0(t)] for every tile (gathered one by one is too slow for 1e5 tiles: copy row_ptr once)
+            std::vector<int64_t> hrp(op.nrows + 1);
+            check(cudaMemcpyAsync(hrp.data(), op.row_ptr, (op.nrows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                  "D2H");
+            check(cudaStreamSynchronize(s), "sync");
+            std::vector<int32_t> r1(nt), srow, st0, st1;
+            for (int64_t t = 0; t < nt; t++) {
+                if (t + 1 < nt) {
+                    const int64_t e = (t + 1) * kMergeTile;
+                    r1[t] = hrp[r0[t + 1]] == e ? r0[t + 1] - 1 : r0[t + 1];
+                } else {
+                    r1[t] = (int32_t)(op.nrows - 1);
+                }
+            }
+            for (int64_t t = 1; t < nt; t++) {
+                const int64_t e = t * kMergeTile;
+                if (hrp[r0[t]] < e) {  // row r0[t] continues from tile t-1
+                    if (!srow.empty() && srow.back() == r0[t]) {
+                        st1.back() = (int32_t)t;
+                    } else {
+                        srow.push_back(r0[t]);
+                        st0.push_back((int32_t)(t - 1));
+                        st1.push_back((int32_t)t);
+                    }
+                }
+            }
+            op.n_span = (int64_t)srow.size();
+            if (op.n_span) {
+                op.span_row = dev_alloc<int32_t>(op, op.n_span);
+                op.span_t0 = dev_alloc<int32_t>(op, op.n_span);
+                op.span_t1 = dev_alloc<int32_t>(op, op.n_span);
+                check(cudaMemcpyAsync(op.span_row, srow.data(), op.n_span * 4, cudaMemcpyHostToDevice, s), "H2D");
+                check(cudaMemcpyAsync(op.span_t0, st0.data(), op.n_span * 4, cudaMemcpyHostToDevice, s), "H2D");
+                check(cudaMemcpyAsync(op.span_t1, st1.data(), op.n_span * 4, cudaMemcpyHostToDevice, s), "H2D");
+            }
+            check(cudaMemcpyAsync(op.tile_r1, r1.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
+            op.merge = true;
+        }
+    }
     check(cudaStreamSynchronize(s), "sync");
     check(cudaGetLastError(), "analyze");
 }
@@ -529,6 +726,17 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
 
 void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
               const int *abort, cudaStream_t s) {
+    if (A.merge) {
+        k_spmv_merge<<<(unsigned)A.n_tiles, 256, 0, s>>>(A.nnz, A.tile_r0, A.tile_r1, A.row_ptr, A.col, A.val, x, y,
+                                                         c_dev, yprev, A.tile_head, A.tile_tail, abort);
+        count_launch();
+        if (A.n_span) {
+            k_spmv_merge_fix<<<grid_for(A.n_span, 256), 256, 0, s>>>(A.n_span, A.span_row, A.span_t0, A.span_t1,
+                                                                      A.tile_head, A.tile_tail, y, c_dev, yprev, abort);
+            count_launch();
+        }
+        return;
+    }
     const int64_t *o = A.bin_off;
     const int cap = 148 * 8;
     {

@@ -71,19 +71,27 @@ def check_products(S, H, A, seed=0):
 
 
 # ---------------------------------------------------------------- a1 / a5
-@pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000)])
-def test_products_configs(S, H, cid, scale):
+@pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
+@pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000), (4, 10)])
+def test_products_configs(S, H, cid, scale, sched, monkeypatch):
+    """Both SpMV schedules (row-binned and nnz-balanced merge) on every config."""
+    if sched != "auto":
+        monkeypatch.setenv("SVDSC_SPMV", sched)
     wl = W.config(cid, scale=scale)
     check_products(S, H, wl.A)
 
 
-def test_products_edge_cases(S, H):
+@pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
+def test_products_edge_cases(S, H, sched, monkeypatch):
+    if sched != "auto":
+        monkeypatch.setenv("SVDSC_SPMV", sched)
     rng = np.random.default_rng(7)
     m, n = 3001, 777
     rows = []
     # empty rows, single-entry rows, a 70k-long row (chunked path), a 3k row (CTA path)
     lens = rng.integers(0, 40, m)
     lens[::17] = 0
+    lens[-3:] = 0  # trailing empty rows (row 0 is empty too)
     lens[5] = n  # dense row
     rp = np.zeros(m + 1, np.int64)
     rp[1:] = np.cumsum(lens)
