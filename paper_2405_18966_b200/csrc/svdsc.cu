@@ -691,6 +691,16 @@ svdsc_status svdsc_create(svdsc_handle **h, void *stream) {
         ck(cudaDeviceGetAttribute(&H->nsm, cudaDevAttrMultiProcessorCount, H->device), "attr");
         H->stream = reinterpret_cast<cudaStream_t>(stream);
         ck(cudaMallocHost(&H->hctrl, sizeof(Ctrl)), "cudaMallocHost");
+        // stream-ordered allocations (NULL workspace, host-buffer entry points)
+        // come from the device's default pool: keep its memory mapped between
+        // solves instead of returning it at every synchronization (re-mapping
+        // the 800 MB operand of BASELINE config 2 cost ~40 ms per solve)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, H->device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
     });
     if (st != SVDSC_OK) {
         delete H;

@@ -272,7 +272,7 @@ def _e2e(S, H, wl, fixed=True, **kw):
 
 
 @pytest.mark.parametrize("mode", ["fused", "stream", "split"])
-@pytest.mark.parametrize("cid,scale", [(1, 1), (2, 4), (3, 20)])
+@pytest.mark.parametrize("cid,scale", [(1, 1), (2, 4), (3, 20), (6, 10), (7, 10), (8, 10)])
 def test_svds_parity(S, H, cid, scale, mode, monkeypatch):
     if mode == "split":
         monkeypatch.setenv("SVDSC_NO_FUSED", "1")
@@ -289,7 +289,10 @@ def test_svds_parity(S, H, cid, scale, mode, monkeypatch):
     assert orth_error(U) <= 1e-10 and orth_error(V) <= 1e-10
     r1, r2 = certificates(wl.A, s, U, V)
     assert np.all(r1 <= 1e-10 * s[0])
-    assert np.all(np.abs(r2 - r.resid.cpu().numpy()) <= 1e-8 * max(1.0, r2.max()))
+    # Eq. (4) residual vs the true ||A^T u - s v|| / s: they agree to rounding
+    # of the computed vectors, ~eps ||A|| / s_j relative -- compared absolutely,
+    # in units of sigma_1 (reading Q16a: Decay3 has s_k / s_1 = 1e-6)
+    assert np.all(np.abs(r2 - r.resid.cpu().numpy()) * s <= 1e-8 * s[0])
     # free-running GPU stops on the same pass as the oracle here
     M = S.Matrix.from_host(H, wl.A)
     rf = S.svds_c(M, k, tol=wl.tol, t=wl.t, maxit=wl.maxit, v0=dev(wl.v0))

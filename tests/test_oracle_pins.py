@@ -319,3 +319,18 @@ def test_decay_spectra_golden():
         s = W.spectrum(kind, max(e["i"]))
         got = s[np.array(e["i"]) - 1]
         assert np.allclose(got, e["sigma"], rtol=1e-15, atol=0), e["cite"]
+
+
+@pytest.mark.parametrize("cid", [6, 7, 8])
+def test_dense1_3_closed_form(cid):
+    """Dense1-3 at 1/20 scale: the oracle's
+    k = 100 Ritz values equal the Decay1/2/3 spectra of Eq. (16),
+    which the generator imposes exactly (closed form), and its residual
+    certificates hold."""
+    wl = W.config(cid, scale=20)
+    r = O.svds(wl.A, wl.k, wl.v0, tol=wl.tol, t=wl.t, maxit=wl.maxit)
+    sig = W.spectrum(f"decay{cid - 5}", wl.A.m)[: wl.k]
+    assert r.converged
+    assert np.abs(r.S - sig).max() <= 1e-10 * sig[0]
+    D = wl.A.dense
+    assert np.linalg.norm(D @ r.V - r.U * r.S, axis=0).max() <= 1e-10 * sig[0]

@@ -239,6 +239,11 @@ CONFIG_NAMES = {
     3: "sparse200000x100000_r50_k100",
     4: "powerlaw4Mx2M_k100",
     5: "banded30Mx5M_k200",
+    # the paper's own dense workload Dense1-3,
+    # 10,000 x 10,000 with the Decay1/2/3 spectra of Eq. (16)
+    6: "dense1_10000_decay1_k100",
+    7: "dense2_10000_decay2_k100",
+    8: "dense3_10000_decay3_k100",
 }
 
 
@@ -265,6 +270,10 @@ def config(cid: int, seed: int = 0, scale: int = 1, r0: int = 0, r1: int | None 
         m, n = 30_000_000 // f, 5_000_000 // f
         A = sparse_banded(m, n, 20, max(1000 // f, 10), seed, r0, r1)
         k, t = 200, 600
+    elif cid in (6, 7, 8):
+        m = n = 10_000 // f
+        A = dense_with_spectrum(m, n, spectrum(f"decay{cid - 5}", m), seed, keep_factors)
+        k, t = 100, 300
     else:
         raise ValueError(cid)
     name = CONFIG_NAMES[cid] + (f"_div{f}" if f != 1 else "")
