@@ -9,7 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsvdsc.so")
-SOURCES = ["svdsc.cu", "matvec.cu", "cgs.cu", "cgs_fused.cu", "svd.cu"]
+SOURCES = ["svdsc.cu", "matvec.cu", "cgs.cu", "cgs_fused.cu", "svd.cu", "paper_api.cpp"]
+CLI = os.path.join(HERE, "svdsc-cli")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
@@ -21,7 +22,9 @@ def stale() -> bool:
         return True
     t = os.path.getmtime(OUT)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(HERE, "..", "include", "svdsc.h"))
+    deps += [os.path.join(HERE, "..", "include", f) for f in ("svdsc.h", "svdsc_paper.h")]
+    if not os.path.exists(CLI):
+        return True
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -32,7 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
     procs = []
     for src in SOURCES:
-        obj = os.path.join(HERE, "build", src.replace(".cu", ".o"))
+        obj = os.path.join(HERE, "build", os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *FLAGS, "-dc" if False else "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
@@ -44,6 +47,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
             "-o", OUT, *objs, "-ldl", "-lpthread", "-Xlinker", "--no-undefined"]
     subprocess.check_call(link)
+    # batch CLI (host C++ over the C ABI), rpath to the in-tree library
+    subprocess.check_call(["g++", "-O2", "-std=c++17", os.path.join(CSRC, "cli.cpp"), "-o", CLI,
+                           "-L" + HERE, "-lsvdsc", "-Wl,-rpath,$ORIGIN"])
     return OUT
 
 

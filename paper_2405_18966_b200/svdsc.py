@@ -50,6 +50,18 @@ class Info(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class PaperCsr(ctypes.Structure):
+    """mat_csr of PAPER.md:293-299: 1-based cols, pointerB / pointerE (MKL LP64)."""
+    _fields_ = [("nnz", ctypes.c_int64), ("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64),
+                ("values", ctypes.POINTER(ctypes.c_double)), ("cols", ctypes.POINTER(ctypes.c_int)),
+                ("pointerB", ctypes.POINTER(ctypes.c_int)), ("pointerE", ctypes.POINTER(ctypes.c_int))]
+
+
+class PaperMat(ctypes.Structure):
+    """mat of PAPER.md:301-304: column-major nrows x ncols."""
+    _fields_ = [("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64), ("d", ctypes.POINTER(ctypes.c_double))]
+
+
 EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_error", "svdsc_version",
            "svdsc_matrix_csr", "svdsc_matrix_dense", "svdsc_matrix_destroy", "svdsc_workspace_size",
            "svdsc_solve", "svdsc_solve_host_csr", "svdsc_solve_host_dense", "svdsc_op_matvec",
@@ -97,6 +109,23 @@ def lib():
         L.svdsc_partition_rows.argtypes = [I64, P, I64, ctypes.c_int, P]
         L.svdsc_profile_enable.argtypes = [P, ctypes.c_int]
         L.svdsc_profile_read.argtypes = [P, P, P]
+        # the paper's interface (include/svdsc_paper.h)
+        PM, PC = ctypes.POINTER(PaperMat), ctypes.POINTER(PaperCsr)
+        for f in ("svds_C", "svds_C_opt"):
+            getattr(L, f).argtypes = [PC, PM, PM, PM, ctypes.c_int] + (
+                [ctypes.c_double, ctypes.c_int, ctypes.c_int] if f.endswith("opt") else [])
+        for f in ("svds_C_dense", "svds_C_dense_opt"):
+            getattr(L, f).argtypes = [PM, PM, PM, PM, ctypes.c_int] + (
+                [ctypes.c_double, ctypes.c_int, ctypes.c_int] if f.endswith("opt") else [])
+        L.svdsc_mat_free.argtypes = [PM]
+        L.svdsc_mat_free.restype = None
+        L.svdsc_mat_csr_free.argtypes = [PC]
+        L.svdsc_mat_csr_free.restype = None
+        L.svdsc_paper_csr_to_csr.argtypes = [PC, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                             ctypes.POINTER(I64)]
+        L.svdsc_read_mm.argtypes = [ctypes.c_char_p, PC, PM, ctypes.POINTER(ctypes.c_int)]
+        L.svdsc_write_mm.argtypes = [ctypes.c_char_p, PC, PM]
+        L.svdsc_paper_last_error.restype = ctypes.c_char_p
         for name in EXPORTS:
             f = getattr(L, name)
             if f.restype is ctypes.c_int:  # default
@@ -347,3 +376,93 @@ def lbp(M: Matrix, t, v0, seed=0, reorth=2):
     M.h._check(lib().svdsc_op_lbp(M.ptr, ctypes.byref(o), t, _ptr(v0.contiguous()), _ptr(U), _ld(U),
                                   _ptr(V), _ld(V), _ptr(T), ctypes.byref(info)))
     return U, V, T, info.as_dict()
+
+
+# ---- the paper's interface and Matrix Market I/O ----------------
+class PaperError(RuntimeError):
+    pass
+
+
+def _paper_check(st):
+    if st < 0:
+        raise PaperError(f"status {st}: {lib().svdsc_paper_last_error().decode()}")
+    return st
+
+
+def paper_csr(nrows, ncols, values, cols1, pointerB, pointerE):
+    """Build a PaperCsr over numpy arrays (kept alive on the returned object)."""
+    values = np.ascontiguousarray(values, np.float64)
+    cols1 = np.ascontiguousarray(cols1, np.int32)
+    pointerB = np.ascontiguousarray(pointerB, np.int32)
+    pointerE = np.ascontiguousarray(pointerE, np.int32)
+    A = PaperCsr(values.size, nrows, ncols, values.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                 cols1.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                 pointerB.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                 pointerE.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    A._keep = (values, cols1, pointerB, pointerE)
+    return A
+
+
+def paper_csr_to_csr(A: PaperCsr):
+    """svdsc_paper_csr_to_csr: the paper layout -> (row_ptr, col_idx, values), 0-based."""
+    rp, ci, va, nk = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    _paper_check(lib().svdsc_paper_csr_to_csr(ctypes.byref(A), ctypes.byref(rp), ctypes.byref(ci),
+                                              ctypes.byref(va), ctypes.byref(nk)))
+    libc = ctypes.CDLL(None)
+    libc.free.argtypes = [ctypes.c_void_p]
+    out = (np.ctypeslib.as_array(ctypes.cast(rp, ctypes.POINTER(ctypes.c_int64)), (A.nrows + 1,)).copy(),
+           np.ctypeslib.as_array(ctypes.cast(ci, ctypes.POINTER(ctypes.c_int32)), (max(nk.value, 1),))[:nk.value].copy(),
+           np.ctypeslib.as_array(ctypes.cast(va, ctypes.POINTER(ctypes.c_double)), (max(nk.value, 1),))[:nk.value].copy())
+    for p in (rp, ci, va):
+        libc.free(p)
+    return out
+
+
+def _mat_to_numpy(M: PaperMat):
+    a = np.ctypeslib.as_array(M.d, (M.ncols * M.nrows,)).reshape(M.ncols, M.nrows).T.copy()
+    lib().svdsc_mat_free(ctypes.byref(M))
+    return a
+
+
+def read_mm(path):
+    """svdsc_read_mm -> ("csr", PaperCsr-as-numpy dict) or ("dense", ndarray)."""
+    A, D, dense = PaperCsr(), PaperMat(), ctypes.c_int()
+    _paper_check(lib().svdsc_read_mm(str(path).encode(), ctypes.byref(A), ctypes.byref(D), ctypes.byref(dense)))
+    if dense.value:
+        return "dense", _mat_to_numpy(D)
+    K = A.nnz
+    d = {"nrows": A.nrows, "ncols": A.ncols,
+         "values": np.ctypeslib.as_array(A.values, (max(K, 1),))[:K].copy(),
+         "cols": np.ctypeslib.as_array(A.cols, (max(K, 1),))[:K].copy(),
+         "pointerB": np.ctypeslib.as_array(A.pointerB, (max(A.nrows, 1),))[:A.nrows].copy(),
+         "pointerE": np.ctypeslib.as_array(A.pointerE, (max(A.nrows, 1),))[:A.nrows].copy()}
+    lib().svdsc_mat_csr_free(ctypes.byref(A))
+    return "csr", d
+
+
+def write_mm(path, csr=None, dense=None):
+    if csr is not None:
+        A = paper_csr(csr["nrows"], csr["ncols"], csr["values"], csr["cols"], csr["pointerB"], csr["pointerE"])
+        _paper_check(lib().svdsc_write_mm(str(path).encode(), ctypes.byref(A), None))
+    else:
+        D = np.asfortranarray(dense, np.float64)
+        M = PaperMat(D.shape[0], D.shape[1], D.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        _paper_check(lib().svdsc_write_mm(str(path).encode(), None, ctypes.byref(M)))
+
+
+def svds_C(A, k, tol=None, t=None, r=None):
+    """The paper's svds_C / svds_C_opt (sparse PaperCsr) or svds_C_dense(_opt)
+    (numpy 2-D array): host in, host out; returns (U, S, V, status)."""
+    U, Sm, V = PaperMat(), PaperMat(), PaperMat()
+    opt = tol is not None or t is not None or r is not None
+    extra = (1e-10 if tol is None else tol, 0 if t is None else t, 10 if r is None else r)
+    if isinstance(A, PaperCsr):
+        f = lib().svds_C_opt if opt else lib().svds_C
+        args = [ctypes.byref(A), ctypes.byref(U), ctypes.byref(Sm), ctypes.byref(V), k]
+    else:
+        D = np.asfortranarray(A, np.float64)
+        M = PaperMat(D.shape[0], D.shape[1], D.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        f = lib().svds_C_dense_opt if opt else lib().svds_C_dense
+        args = [ctypes.byref(M), ctypes.byref(U), ctypes.byref(Sm), ctypes.byref(V), k]
+    st = _paper_check(f(*args, *extra) if opt else f(*args))
+    return _mat_to_numpy(U), _mat_to_numpy(Sm)[:, 0], _mat_to_numpy(V), st

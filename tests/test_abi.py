@@ -9,14 +9,17 @@ import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HDR = os.path.join(ROOT, "include", "svdsc.h")
+HDRS = [os.path.join(ROOT, "include", f) for f in ("svdsc.h", "svdsc_paper.h")]
 SO = os.path.join(ROOT, "paper_2405_18966_b200", "libsvdsc.so")
 
 
 def declared():
-    src = open(HDR).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(svdsc_[a-z_0-9]+)\s*\(", src)))
+    out = set()
+    for hdr in HDRS:
+        src = open(hdr).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        out |= set(re.findall(r"\b(svdsc_[a-z_0-9]+|svds_C[a-z_]*)\s*\(", src))
+    return sorted(out)
 
 
 @pytest.fixture(scope="module")
@@ -28,7 +31,7 @@ def so():
 
 def test_exports_match_header(so):
     out = subprocess.check_output(["nm", "-D", "--defined-only", so]).decode()
-    exported = set(re.findall(r" T (svdsc_\w+)", out))
+    exported = set(re.findall(r" T (svdsc_\w+|svds_C\w*)", out))
     decl = declared()
     assert len(decl) >= 20
     missing = [d for d in decl if d not in exported]
