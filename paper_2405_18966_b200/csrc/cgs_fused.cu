@@ -123,6 +123,7 @@ struct Args {
     int RT;               // row tile of phase B (streaming mode)
     int wsmem;            // keep the CTA's w rows in shared memory
     unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
+    PreReduce pre;        // pending split-K reduction of w (pre.partial != NULL)
 };
 
 // out[j] = sum_b partial[b][j] for the columns owned by this CTA
@@ -172,7 +173,16 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     double *wv = a.wsmem ? wsh : (a.w + r0);  // generic pointer to this CTA's rows of w
 
     if (a.wsmem)
-        for (int i = tid; i < nr; i += blockDim.x) wsh[i] = a.w[r0 + i];
+        for (int i = tid; i < nr; i += blockDim.x) {
+            if (a.pre.partial) {  // finish the dense product (k_split_reduce order: bitwise equal)
+                double sacc = 0.0;
+                for (int q = 0; q < a.pre.splits; q++) sacc += a.pre.partial[q * a.N + r0 + i];
+                if (a.pre.yprev) sacc -= *a.pre.c_dev * a.pre.yprev[r0 + i];
+                wsh[i] = sacc;
+            } else {
+                wsh[i] = a.w[r0 + i];
+            }
+        }
     if (QS) {  // the CTA's rows of Q, all copies in flight at once (cp.async, 8 B each)
         for (int j = wid; j < ncols; j += 8)
             for (int i = lane; i < nr; i += 32) {
@@ -1560,6 +1570,7 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             a.rpb = (int)rpb;
             a.RT = 1;
             a.wsmem = 1;
+            if (fs.pre) a.pre = *fs.pre;
             static bool attr = false;
             if (!attr) {
                 cudaFuncSetAttribute(k_cgs2_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -1576,7 +1587,9 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             return true;
         }
     }
-    // streaming mode (tall bases): cp.async row tiles through shared memory
+    // streaming mode (tall bases): cp.async row tiles through shared memory;
+    // a pending dense reduction is finished first (the tiles read w from HBM)
+    if (fs.pre) split_reduce(N, *fs.pre, w, ctrl ? &ctrl->abort : nullptr, s);
     const bool aligned = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
     if (!aligned || ncols > 1024) return false;

@@ -117,11 +117,26 @@ void axpy_dev(int64_t N, double *y, const double *c_dev, const double *x, const 
               cudaStream_t s);  // y -= c x
 
 // Fused single-kernel CGS2 + norm + normalize (single GPU, cooperative launch).
+// A dense product left as split-K partials: w[r] = sum_q partial[q*N + r] - c*yprev[r]
+// (the k_split_reduce epilogue), to be finished by the CGS2 kernel that reads w.
+struct PreReduce {
+    const double *partial = nullptr;
+    int splits = 0;
+    const double *c_dev = nullptr;
+    const double *yprev = nullptr;
+};
+void split_reduce(int64_t N, const PreReduce &pr, double *y, const int *abort, cudaStream_t s);
+void gemv_n_partial(const DenseOp &A, const double *x, PreReduce &pr, const double *c_dev, const double *yprev,
+                    const int *abort, cudaStream_t s);
+void gemv_t_partial(const DenseOp &A, const double *x, PreReduce &pr, const double *c_dev, const double *yprev,
+                    const int *abort, cudaStream_t s);
+
 struct FusedScratch {
     double *partial;      // >= 2*nsm x (ncols+2)
     double *h1, *h2, *h3; // >= ncols+2
     unsigned int *flags;  // >= 2*nsm grid-barrier flags, zeroed once per solve
     unsigned int epoch;   // unique increasing base per launch (multiple of 16)
+    const PreReduce *pre = nullptr;  // pending dense split-K reduction of w (or NULL)
 };
 // false: the fused path is not applicable (caller uses cgs_p1/p2/p3 + normalize)
 // tmap: optional CUtensorMap (128 B) of Q for the TMA streaming variant

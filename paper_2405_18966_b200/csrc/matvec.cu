@@ -853,6 +853,64 @@ __global__ void __launch_bounds__(256) k_gemv_n(int64_t m, int64_t n, const doub
     }
 }
 
+// y_partial[split][c] = sum over rows of split of A[r,c] x[r]; each warp owns
+// 4 adjacent columns, so every x value loaded (128-bit, L1) serves 4 columns of
+// A (one 128-bit streaming load each): x traffic per A byte drops 4x.
+__global__ void __launch_bounds__(256) k_gemv_t4(int64_t m, int64_t n, const double *__restrict__ A, int64_t ld,
+                                                 const double *__restrict__ x, double *partial, int64_t rows_per_split,
+                                                 const int *abort) {
+    if (aborted(abort)) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t c0 = (blockIdx.x * 8ll + w) * 4;
+    const int64_t r0 = blockIdx.y * rows_per_split;
+    const int64_t r1 = min(m, r0 + rows_per_split);
+    if (c0 >= n) return;
+    const int nc = (int)min((int64_t)4, n - c0);
+    const double *col[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) col[q] = A + min(c0 + q, n - 1) * ld;  // clamped: extra columns unused
+    double acc[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; q++) acc[q][0] = acc[q][1] = 0.0;
+    int64_t r = r0 + 2 * lane;
+    for (; r + 64 * 3 + 1 < r1; r += 64 * 4) {
+        double2 v[4][4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            xv[u] = __ldg(reinterpret_cast<const double2 *>(x + r + 64 * u));
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q][u] = __ldcs(reinterpret_cast<const double2 *>(col[q] + r + 64 * u));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                acc[q][0] = fma(v[q][u].x, xv[u].x, acc[q][0]);
+                acc[q][1] = fma(v[q][u].y, xv[u].y, acc[q][1]);
+            }
+    }
+    for (; r + 1 < r1; r += 64) {
+        const double2 xv = __ldg(reinterpret_cast<const double2 *>(x + r));
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const double2 v = __ldcs(reinterpret_cast<const double2 *>(col[q] + r));
+            acc[q][0] = fma(v.x, xv.x, acc[q][0]);
+            acc[q][1] = fma(v.y, xv.y, acc[q][1]);
+        }
+    }
+    if (r < r1) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[q][0] = fma(col[q][r], x[r], acc[q][0]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        double s = acc[q][0] + acc[q][1];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0 && q < nc) partial[blockIdx.y * n + c0 + q] = s;
+    }
+}
+
 // y_partial[split][c] = sum over rows of split of A[r,c] x[r]; warp per column.
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_gemv_t(int64_t m, int64_t n, const double *__restrict__ A, int64_t ld,
@@ -910,6 +968,11 @@ __global__ void k_split_reduce(int64_t len, int splits, const double *__restrict
 
 }  // namespace
 
+void split_reduce(int64_t N, const PreReduce &pr, double *y, const int *abort, cudaStream_t s) {
+    k_split_reduce<<<grid_for(N, 256), 256, 0, s>>>(N, pr.splits, pr.partial, y, pr.c_dev, pr.yprev, abort);
+    count_launch();
+}
+
 void gemv_n(const DenseOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
             const int *abort, cudaStream_t s) {
     const int64_t m = A.nrows, n = A.ncols;
@@ -931,14 +994,60 @@ void gemv_t(const DenseOp &A, const double *x, double *y, const double *c_dev, c
     const int splits = A.splits_t;
     int64_t rps = (m + splits - 1) / splits;
     rps = (rps + 1) & ~1ll;  // even, keeps 16-byte alignment of every split start
-    dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
     const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    if (vec) k_gemv_t<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
-    else k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    const char *g4 = getenv("SVDSC_GEMV_T1");  // experiment: the one-column-per-warp kernel
+    if (vec && !(g4 && g4[0] == '1')) {
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)splits);
+        k_gemv_t4<<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    } else {
+        dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
+        if (vec) k_gemv_t<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+        else k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    }
     k_split_reduce<<<grid_for(n, 256), 256, 0, s>>>(n, splits, A.partial, y, c_dev, yprev, abort);
     count_launch();
     count_launch();
+}
+
+// the products without their split-K reduction (finished by the next CGS2 kernel)
+void gemv_n_partial(const DenseOp &A, const double *x, PreReduce &pr, const double *c_dev, const double *yprev,
+                    const int *abort, cudaStream_t s) {
+    const int64_t m = A.nrows, n = A.ncols;
+    const int64_t rb = (m + 63) / 64;
+    const int splits = A.splits_n;
+    const int64_t cps = (n + splits - 1) / splits;
+    dim3 grid((unsigned)rb, (unsigned)splits);
+    const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0);
+    if (vec) k_gemv_n<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, cps, abort);
+    else k_gemv_n<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, cps, abort);
+    count_launch();
+    pr.partial = A.partial;
+    pr.splits = splits;
+    pr.c_dev = c_dev;
+    pr.yprev = yprev;
+}
+
+void gemv_t_partial(const DenseOp &A, const double *x, PreReduce &pr, const double *c_dev, const double *yprev,
+                    const int *abort, cudaStream_t s) {
+    const int64_t m = A.nrows, n = A.ncols;
+    const int splits = A.splits_t;
+    int64_t rps = (m + splits - 1) / splits;
+    rps = (rps + 1) & ~1ll;
+    const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if (vec) {
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)splits);
+        k_gemv_t4<<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    } else {
+        dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
+        k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    }
+    count_launch();
+    pr.partial = A.partial;
+    pr.splits = splits;
+    pr.c_dev = c_dev;
+    pr.yprev = yprev;
 }
 
 }  // namespace svdsc

@@ -278,12 +278,19 @@ constexpr int kMaxPairs = kJThreads / 32;
 template <bool CL, int kRPL>
 __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const double *__restrict__ W0, double *Wout,
                                                        RotLog *rlog, int max_sweeps, Ctrl *ctrl, const int *abort,
-                                                       double ctol) {
+                                                       double ctol, int use_bulk) {
     if (aborted(abort)) return;
     cg::cluster_group cl = cg::this_cluster();
     const int C = CL ? (int)cl.num_blocks() : 1;
     const int me = CL ? (int)cl.block_rank() : 0;
-    extern __shared__ double Wl[];  // slot s, local column i: Wl + (s*h + i)*p
+    extern __shared__ __align__(16) double Wsm[];  // slot s, local column i: Wl + (s*h + i)*p
+    // bulk-copy exchange: two half-block buffer sets, Wl = the current one
+    // (push model: every CTA sends its two half-blocks to their next owners
+    // with cp.async.bulk shared::cta -> shared::cluster, completing on the
+    // receiver's mbarrier); else one set and a register pull through DSMEM
+    const bool bulk = CL && use_bulk;
+    double *Wl = Wsm;
+    __shared__ __align__(8) uint64_t xbar;
     __shared__ int rot_flag[2];
     __shared__ int src_cta[2], src_slot[2];
     const double tiny = *(volatile double *)&ctrl->svd_tiny;
@@ -308,7 +315,15 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
         const int col = hb[lc / h] * h + (lc % h);
         Wl[idx] = (col < p) ? W0[r + (int64_t)col * p] : 0.0;
     }
-    if (threadIdx.x == 0) rot_flag[0] = rot_flag[1] = 0;
+    if (threadIdx.x == 0) {
+        rot_flag[0] = rot_flag[1] = 0;
+        if (bulk) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&xbar))
+                         : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+    }
+    unsigned xphase = 0;
     if (CL) cl.sync(); else __syncthreads();
     const int64_t per_round = (int64_t)C * h;
     const int lrounds = H2 - 1;
@@ -450,7 +465,52 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
             }
             __syncthreads();
             }
-            if (CL && m > 1) {
+            if (CL && m > 1 && bulk) {
+                const long long x0 = (kJacobiTiming && me == 0 && threadIdx.x == 0) ? clock64() : 0;
+                const int rn = (br + 1) % m;
+                const int n = h * p;
+                double *Wn = (Wl == Wsm) ? Wsm + 2 * n : Wsm;  // the other buffer set
+                const unsigned bar = (unsigned)__cvta_generic_to_shared(&xbar);
+                if (threadIdx.x == 0) {
+                    // two incoming half-blocks; armed before the cluster barrier
+                    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                                 "r"((unsigned)(2 * n * 8))
+                                 : "memory");
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk reads
+                }
+                cl.sync();  // block round done everywhere; every CTA's barrier is armed
+                if (threadIdx.x < 2) {
+                    const int sl = threadIdx.x;
+                    int ct, ds;
+                    hb_loc(C, rn, hb_at(C, br, me, sl), ct, ds);  // where my slot-sl half-block goes
+                    const unsigned src = (unsigned)__cvta_generic_to_shared(Wl + (int64_t)sl * n);
+                    const unsigned dloc = (unsigned)__cvta_generic_to_shared(Wn + (int64_t)ds * n);
+                    unsigned dst, rbar;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(dloc), "r"(ct));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(bar), "r"(ct));
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst),
+                        "r"(src), "r"((unsigned)(n * 8)), "r"(rbar)
+                        : "memory");
+                }
+                // wait for my two incoming half-blocks
+                asm volatile(
+                    "{\n.reg .pred P1;\nXW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra XW_%=;\n}\n" ::"r"(
+                        bar),
+                    "r"(xphase)
+                    : "memory");
+                xphase ^= 1;
+                Wl = Wn;
+                hb[0] = hb_at(C, rn, me, 0);
+                hb[1] = hb_at(C, rn, me, 1);
+                for (int lc = threadIdx.x; lc < H2; lc += blockDim.x) gcol[lc] = hb[lc / h] * h + (lc % h);
+                __syncthreads();
+                if (kJacobiTiming && me == 0 && threadIdx.x == 0) {
+                    atomicAdd(&g_jt[5], (unsigned long long)(clock64() - x0));
+                    atomicAdd(&g_jt[6], 1ull);
+                }
+            } else if (CL && m > 1) {
                 // move to round br+1 (after the last block round the circle is back at round 0)
                 const long long x0 = (kJacobiTiming && me == 0 && threadIdx.x == 0) ? clock64() : 0;
                 const int rn = (br + 1) % m;
@@ -928,9 +988,13 @@ cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *r
                           double ctol, cudaStream_t s) {
     if (C == 1) {
         cudaFuncSetAttribute(k_jacobi_block<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol);
+        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol, 0);
         return cudaGetLastError();
     }
+    // bulk-copy exchange needs the second buffer set (SVDSC_JACOBI_PULL=1: register pull)
+    const char *pe = getenv("SVDSC_JACOBI_PULL");
+    const int use_bulk = (2 * smem <= 210 * 1024 && !(pe && pe[0] == '1')) ? 1 : 0;
+    if (use_bulk) smem *= 2;
     cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (C > 8) cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
@@ -945,7 +1009,8 @@ cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *r
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort, ctol);
+    return cudaLaunchKernelEx(&cfg, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort, ctol,
+                              use_bulk);
 }
 
 size_t small_svd_log_doubles(int p) {

@@ -321,15 +321,28 @@ struct Solver {
         }
         H->prof.begin(0, s);
         if (M->kind == 0) spmv_csr(M->A, x, z, c_dev, zprev, abort, s);
+        else if (defer_reduce()) gemv_n_partial(M->D, x, pending, c_dev, zprev, abort, s);
         else gemv_n(M->D, x, z, c_dev, zprev, abort, s);
         H->prof.end(s);
         matvecs++;
+    }
+    // dense single-GPU products leave their split-K partials for the fused CGS2
+    // kernel, which finishes the reduction while staging w (one launch less per
+    // half-step); any other consumer calls finish_pending() first
+    PreReduce pending;
+    bool defer_reduce() const { return M->kind == 1 && P == 1 && fused_ok && o->reorth != 0; }
+    void finish_pending(int64_t N, double *wv) {
+        if (pending.partial) {
+            split_reduce(N, pending, wv, abort, s);
+            pending = PreReduce{};
+        }
     }
     // wslice = (A^T u)_slice - c wprev
     void Atu(const double *u, double *wcol, const double *c_dev, const double *wprev) {
         if (P == 1) {
             H->prof.begin(1, s);
             if (M->kind == 0) spmv_csr(M->At, u, wcol, c_dev, wprev, abort, s);
+            else if (defer_reduce()) gemv_t_partial(M->D, u, pending, c_dev, wprev, abort, s);
             else gemv_t(M->D, u, wcol, c_dev, wprev, abort, s);
             H->prof.end(s);
         } else {
@@ -372,15 +385,20 @@ struct Solver {
     void orth_norm(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, double *t_entry, int chk,
                    const double *pre_h) {
         if (P == 1 && o->reorth != 0 && fused_ok) {
-            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches)};
+            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches),
+                            pending.partial ? &pending : nullptr};
             H->prof.begin(11, s);
             const void *tm = have_tmap ? (Q == w.U ? (const void *)tmapU : (Q == w.V ? (const void *)tmapV : nullptr))
                                        : nullptr;
             const bool ok = cgs2_fused(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s, tm);
             H->prof.end(s);
-            if (ok) return;
+            if (ok) {
+                pending = PreReduce{};
+                return;
+            }
             fused_ok = false;
         }
+        finish_pending(N, wv);
         if (pre_h) cgs_p3(N, ncols, Q, ldq, wv, pre_h, rb, abort, nsm, s);
         cgs2(N, ncols, Q, ldq, wv, false);
         H->prof.begin(5, s);
@@ -667,7 +685,7 @@ void matrix_common_dense_setup(svdsc_matrix *M) {
     const int64_t rb = (m + 63) / 64;
     D.splits_n = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)nsm * 8 + rb - 1) / std::max<int64_t>(rb, 1)));
     D.splits_n = (int)std::min<int64_t>(D.splits_n, std::max<int64_t>(1, n / 16));
-    const int64_t cb = (n + 7) / 8;
+    const int64_t cb = (n + 31) / 32;  // k_gemv_t4: 8 warps x 4 columns per CTA
     D.splits_t = (int)std::max<int64_t>(1, std::min<int64_t>({64, ((int64_t)nsm * 8 + cb - 1) / cb, std::max<int64_t>(1, m / 1024)}));
     const size_t need = std::max<size_t>((size_t)D.splits_n * m, (size_t)D.splits_t * n);
     ck(cudaMalloc(&M->dense_partial, need * sizeof(double)), "cudaMalloc");
