@@ -176,8 +176,10 @@ SVDSC_API svdsc_status svdsc_op_lbp(svdsc_matrix *M, const svdsc_opts *o, int32_
  * the handle's stream and accumulates device milliseconds per family (read
  * after the solve).  Families: 0 A v products (a5), 1 A^T u products (a1),
  * 2 CGS sweep p1, 3 p2, 4 p3, 5 normalize, 6 small SVD (a7), 7 residuals,
- * 8 recombination (a8/a9), 9 restart misc, 10 collectives.  enable resets the
- * counters.  ms / calls: host arrays of 16 entries. */
+ * 8 recombination (a8/a9), 9 restart misc, 10 collectives, 11 fused CGS2.
+ * enable: 0 off, 1 every family, < 0 only the families of the bitmask -enable
+ * (fewer event records inside a timed region).  enable resets the counters.
+ * ms / calls: host arrays of 16 entries. */
 #define SVDSC_PROF_FAMILIES 16
 SVDSC_API svdsc_status svdsc_profile_enable(svdsc_handle *h, int enable);
 SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int64_t *calls);

@@ -996,8 +996,10 @@ void gemv_t(const DenseOp &A, const double *x, double *y, const double *c_dev, c
     rps = (rps + 1) & ~1ll;  // even, keeps 16-byte alignment of every split start
     const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    const char *g4 = getenv("SVDSC_GEMV_T1");  // experiment: the one-column-per-warp kernel
-    if (vec && !(g4 && g4[0] == '1')) {
+    // k_gemv_t4 (4 columns per warp) measured slower at config 2 (153 vs 127 us):
+    // opt-in experiment only (SVDSC_GEMV_T4=1)
+    const char *g4 = getenv("SVDSC_GEMV_T4");
+    if (vec && g4 && g4[0] == '1') {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)splits);
         k_gemv_t4<<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
     } else {
@@ -1036,13 +1038,9 @@ void gemv_t_partial(const DenseOp &A, const double *x, PreReduce &pr, const doub
     rps = (rps + 1) & ~1ll;
     const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    if (vec) {
-        dim3 grid((unsigned)((n + 31) / 32), (unsigned)splits);
-        k_gemv_t4<<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
-    } else {
-        dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
-        k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
-    }
+    dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
+    if (vec) k_gemv_t<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
+    else k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
     count_launch();
     pr.partial = A.partial;
     pr.splits = splits;

@@ -93,6 +93,7 @@ inline void einval(bool bad, const std::string &m) {
 // per-family CUDA-event timing (svdsc_profile_enable)
 struct Prof {
     bool on = false;
+    unsigned mask = 0xffffffffu;  // families recorded
     double ms[SVDSC_PROF_FAMILIES] = {0};
     int64_t calls[SVDSC_PROF_FAMILIES] = {0};
     struct Pair {
@@ -113,7 +114,7 @@ struct Prof {
         return e;
     }
     void begin(int fam, cudaStream_t s) {
-        if (!on) return;
+        if (!on || !((mask >> fam) & 1u)) return;
         open_fam = fam;
         open_ev = take();
         cudaEventRecord(open_ev, s);
@@ -685,7 +686,7 @@ void matrix_common_dense_setup(svdsc_matrix *M) {
     const int64_t rb = (m + 63) / 64;
     D.splits_n = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)nsm * 8 + rb - 1) / std::max<int64_t>(rb, 1)));
     D.splits_n = (int)std::min<int64_t>(D.splits_n, std::max<int64_t>(1, n / 16));
-    const int64_t cb = (n + 31) / 32;  // k_gemv_t4: 8 warps x 4 columns per CTA
+    const int64_t cb = (n + 7) / 8;  // k_gemv_t: 8 warps x 1 column per CTA
     D.splits_t = (int)std::max<int64_t>(1, std::min<int64_t>({64, ((int64_t)nsm * 8 + cb - 1) / cb, std::max<int64_t>(1, m / 1024)}));
     const size_t need = std::max<size_t>((size_t)D.splits_n * m, (size_t)D.splits_t * n);
     ck(cudaMalloc(&M->dense_partial, need * sizeof(double)), "cudaMalloc");
@@ -1092,6 +1093,7 @@ svdsc_status svdsc_profile_enable(svdsc_handle *h, int enable) {
     cudaStreamSynchronize(h->stream);
     h->prof.harvest();
     h->prof.on = enable != 0;
+    h->prof.mask = enable < 0 ? (unsigned)(-enable) : 0xffffffffu;
     for (int i = 0; i < SVDSC_PROF_FAMILIES; i++) {
         h->prof.ms[i] = 0.0;
         h->prof.calls[i] = 0;

@@ -170,8 +170,13 @@ class Handle:
         self._check(lib().svdsc_comm_init(self.ptr, nranks, rank, uid))
         self.nranks, self.rank = nranks, rank
 
-    def profile(self, enable=True):
-        self._check(lib().svdsc_profile_enable(self.ptr, int(enable)))
+    def profile(self, enable=True, families=None):
+        """CUDA-event timing per operation family; `families`: names to record
+        (None: all) -- fewer events inside a timed region."""
+        v = int(bool(enable))
+        if enable and families is not None:
+            v = -sum(1 << PROF_FAMILIES.index(f) for f in families)
+        self._check(lib().svdsc_profile_enable(self.ptr, v))
 
     def profile_read(self):
         ms = np.zeros(16)
