@@ -687,7 +687,11 @@ void matrix_common_dense_setup(svdsc_matrix *M) {
     D.splits_n = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)nsm * 8 + rb - 1) / std::max<int64_t>(rb, 1)));
     D.splits_n = (int)std::min<int64_t>(D.splits_n, std::max<int64_t>(1, n / 16));
     const int64_t cb = (n + 7) / 8;  // k_gemv_t: 8 warps x 1 column per CTA
-    D.splits_t = (int)std::max<int64_t>(1, std::min<int64_t>({64, ((int64_t)nsm * 8 + cb - 1) / cb, std::max<int64_t>(1, m / 1024)}));
+    // ~2500 CTAs (2.8 waves at 6 CTAs/SM): measured best at config 2 (splits 4-5:
+    // 120 us vs 127 us at 2 splits; tools/timeline.py sweep)
+    D.splits_t = (int)std::max<int64_t>(1, std::min<int64_t>({64, (2500 + cb / 2) / cb, std::max<int64_t>(1, m / 1024)}));
+    if (const char *e = getenv("SVDSC_SPLITS_T")) D.splits_t = std::max(1, atoi(e));  // experiment
+    if (const char *e = getenv("SVDSC_SPLITS_N")) D.splits_n = std::max(1, atoi(e));  // experiment
     const size_t need = std::max<size_t>((size_t)D.splits_n * m, (size_t)D.splits_t * n);
     ck(cudaMalloc(&M->dense_partial, need * sizeof(double)), "cudaMalloc");
     D.partial = M->dense_partial;
