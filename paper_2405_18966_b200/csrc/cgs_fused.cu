@@ -1368,7 +1368,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
             for (int64_t r = rb + tid; r < re; r += kTmaThreads) a.w[r] = a.w[r] / beta;
     }
     stamp();
-    if (a.tdbg && tid == 0 && ntk == 8) {
+    const char *kfilter = nullptr;  // (device: filter set via a.tdbg[15] = min N)
+    (void)kfilter;
+    if (a.tdbg && tid == 0 && ntk == 8 && a.N >= (int64_t)a.tdbg[15] && ncols >= (int)a.tdbg[14]) {
         for (int q = 1; q < 8; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
         atomicAdd(a.tdbg + 10, 1ull);
         atomicAdd(a.tdbg + 11, (unsigned long long)ntiles);
@@ -1516,7 +1518,7 @@ void ktiming_dump() {
     if (!g_ktbuf) return;
     unsigned long long h[16];
     cudaMemcpy(h, g_ktbuf, sizeof(h), cudaMemcpyDeviceToHost);
-    cudaMemset(g_ktbuf, 0, sizeof(h));
+    cudaMemset(g_ktbuf, 0, 14 * sizeof(unsigned long long));  // keep the filter in [14], [15]
     const double n = h[10] ? (double)h[10] : 1.0;
     fprintf(stderr,
             "[ktiming] calls(x CTAs)=%llu avg tiles/CTA=%.1f  phaseA=%.0f wait1=%.0f reduce1=%.0f bar2+load=%.0f "
@@ -1616,6 +1618,11 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             if (!g_ktbuf) {
                 cudaMalloc(&g_ktbuf, 16 * sizeof(unsigned long long));
                 cudaMemset(g_ktbuf, 0, 16 * sizeof(unsigned long long));
+                // SVDSC_KTIMING_MIN_N / _MIN_COLS: only calls at least this large are timed
+                unsigned long long flt[2] = {0, 0};
+                if (const char *e = getenv("SVDSC_KTIMING_MIN_COLS")) flt[0] = strtoull(e, nullptr, 10);
+                if (const char *e = getenv("SVDSC_KTIMING_MIN_N")) flt[1] = strtoull(e, nullptr, 10);
+                cudaMemcpy(g_ktbuf + 14, flt, sizeof(flt), cudaMemcpyHostToDevice);
             }
             sa.tdbg = g_ktbuf;
         }

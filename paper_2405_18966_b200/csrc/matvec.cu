@@ -83,7 +83,7 @@ __device__ __forceinline__ void epilogue_store(double *y, int64_t r, double sum,
 // path, L1/L2 resident), so a warp keeps 2 kU + kU loads in flight instead of a
 // serial load -> gather -> FMA chain.  rows == nullptr: the bin is the identity
 // (every row, in order).  Fixed shape per G: deterministic.
-template <int G>
+template <int G, int kU>
 __device__ __forceinline__ void spmv_vec_rows(const int32_t *__restrict__ rows, int64_t count,
                                                   const int64_t *__restrict__ rp,
                                                   const int32_t *__restrict__ col,
@@ -92,7 +92,6 @@ __device__ __forceinline__ void spmv_vec_rows(const int32_t *__restrict__ rows, 
                                                   const double *c_dev, const double *__restrict__ yprev,
                                                   int64_t blk, int64_t nblk) {
     constexpr int GPW = kWarp / G;  // groups per warp
-    constexpr int kU = 4;
     const int lane = threadIdx.x & 31;
     const int sub = lane % G;
     const int64_t warp_g = (blk * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -136,6 +135,19 @@ __device__ __forceinline__ void spmv_vec_rows(const int32_t *__restrict__ rows, 
 // All vector bins in ONE launch: CTAs [bstart[b], bstart[b+1]) serve bin b
 // with its group width (2, 4, 8, 16, 32 lanes per row).  Avoids one
 // serialized (and often tiny) launch per non-empty bin.
+// group shape (lanes per row, loads in flight per lane) of bins 3 and 4
+// (compile-time tunables: -DSVDSC_BIN3_G=... etc.)
+#ifndef SVDSC_BIN3_G
+#define SVDSC_BIN3_G 8
+#define SVDSC_BIN3_U 8
+#endif
+#ifndef SVDSC_BIN4_G
+#define SVDSC_BIN4_G 16
+#define SVDSC_BIN4_U 8
+#endif
+constexpr int kBin3G = SVDSC_BIN3_G, kBin3U = SVDSC_BIN3_U;
+constexpr int kBin4G = SVDSC_BIN4_G, kBin4U = SVDSC_BIN4_U;
+
 struct BinArgs {
     const int32_t *rows[5];  // nullptr: identity bin
     int64_t count[5];
@@ -159,11 +171,14 @@ __global__ void __launch_bounds__(256) k_spmv_bins(BinArgs ba, const int64_t *__
         }
     const int64_t blk = bx - lo, nblk = hi - lo;
     switch (b) {
-        case 0: spmv_vec_rows<2>(ba.rows[0], ba.count[0], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
-        case 1: spmv_vec_rows<4>(ba.rows[1], ba.count[1], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
-        case 2: spmv_vec_rows<8>(ba.rows[2], ba.count[2], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
-        case 3: spmv_vec_rows<16>(ba.rows[3], ba.count[3], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
-        default: spmv_vec_rows<32>(ba.rows[4], ba.count[4], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        // (lanes per row, loads in flight per lane): rows of 17-64 nnz take 8 lanes x 8
+        // (one pass for up to 64 nnz, 4 rows per warp), 65-2048 take 16 x 8 -- measured
+        // best of the tried shapes (config 3: 53.5 vs 58 us; config 4 A^T: 798 vs 868 us)
+        case 0: spmv_vec_rows<2, 4>(ba.rows[0], ba.count[0], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        case 1: spmv_vec_rows<4, 4>(ba.rows[1], ba.count[1], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        case 2: spmv_vec_rows<8, 4>(ba.rows[2], ba.count[2], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        case 3: spmv_vec_rows<kBin3G, kBin3U>(ba.rows[3], ba.count[3], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
+        default: spmv_vec_rows<kBin4G, kBin4U>(ba.rows[4], ba.count[4], rp, col, val, x, y, c_dev, yprev, blk, nblk); break;
     }
 }
 
@@ -765,7 +780,7 @@ void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, c
         for (int b = 0; b < 5; b++) {
             ba.bstart[b] = nb_tot;
             if (ba.count[b] == 0) continue;
-            const int G = 2 << b;
+            const int G = b == 3 ? kBin3G : (b == 4 ? kBin4G : (2 << b));
             const int need = grid_for(ba.count[b] * G, 256, vcap);
             const int share = std::max(1, (int)(vcap * work[b] / tot + 0.5));
             nb_tot += std::min(need, share);

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libsvdsc.so")
+_SO = os.path.join(_HERE, os.environ.get("SVDSC_LIB_VARIANT", "libsvdsc.so"))  # variant: tuning experiments
 _lib = None
 
 OK, NOT_CONVERGED = 0, 1
