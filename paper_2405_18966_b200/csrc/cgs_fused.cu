@@ -460,6 +460,7 @@ struct SArgs {
     const double *pre_h;
     int64_t rpb;  // rows per CTA, multiple of RT
     unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
+    int snake;    // stream2 sweep-direction policy (see k_cgs2_stream2)
 };
 
 template <int RT>
@@ -769,13 +770,20 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
     const int sw = lane & (kCh - 1);  // swizzle term of every column this lane owns
 
+    // sweeps alternate direction (forward, backward, ...): each sweep starts on
+    // the tiles the previous one read last, which are still in L2
+    // (measured gain for the 2-stage ring, loss for the 3-stage one: snake only
+    // where it wins, SVDSC_SNAKE=0/1/2 = never/always/2-stage)
+    int sweep_no = 0;
+    const bool snake = a.snake == 1 || (a.snake == 2 && NS == 2);
+    auto tile_of = [&](int k) { return (snake && (sweep_no & 1)) ? ntiles - 1 - k : k; };
     // prologue: the first NS-1 tiles of a phase (issued early, e.g. before the
     // grid barrier of the previous reduction, so the ramp-up hides behind it)
     auto prefetch = [&]() {
 #pragma unroll
         for (int p = 0; p < NS - 1; p++) {
             if (p < ntiles) {
-                const int64_t r1 = rb + (int64_t)p * RT;
+                const int64_t r1 = rb + (int64_t)tile_of(p) * RT;
                 issue_tile<RT, kSThr>(a, buf + p * tile_d, wt + p * RT, r1, (int)min((int64_t)RT, re - r1));
             } else {
                 cp_commit();
@@ -790,7 +798,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         for (int k = 0; k < ntiles; k++) {
             const int kn = k + NS - 1;
             if (kn < ntiles) {
-                const int64_t r1 = rb + (int64_t)kn * RT;
+                const int64_t r1 = rb + (int64_t)tile_of(kn) * RT;
                 issue_tile<RT, kSThr>(a, buf + (kn % NS) * tile_d, wt + (kn % NS) * RT, r1,
                                       (int)min((int64_t)RT, re - r1));
             } else {
@@ -798,10 +806,11 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             }
             cp_wait<NS - 1>();
             __syncthreads();
-            body(k, buf + (k % NS) * tile_d, wt + (k % NS) * RT);
+            body(tile_of(k), buf + (k % NS) * tile_d, wt + (k % NS) * RT);
             __syncthreads();
         }
         cp_wait<0>();
+        sweep_no++;
     };
     // element (row rr, column lane + 32 m) of a tile
     auto tval = [&](const double *T, int rr, int m) -> double {
@@ -1612,6 +1621,8 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     sa.t_entry = t_entry;
     sa.check = check;
     sa.pre_h = pre_h;
+    sa.snake = 1;
+    if (const char *e = getenv("SVDSC_SNAKE")) sa.snake = atoi(e);
     {
         const char *kt = getenv("SVDSC_KTIMING");
         if (kt && kt[0] == '1') {
