@@ -16,6 +16,7 @@
 // Reductions over CTAs: partials [block][column], then CTA b reduces columns
 // b, b + nb, ... in a fixed tree order (deterministic), grid barrier, and
 // every CTA reads the reduced vector.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -1535,6 +1536,168 @@ void ktiming_dump() {
             h[10], h[11] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[8] * 1e-6);
 }
 
+// ---------------------------------------------------------------------------
+// Single-cluster CGS2 for small bases (BASELINE config 1, the V side of config
+// 2): C <= 16 CTAs of one thread-block cluster own contiguous row blocks; Q is
+// read from L2 (it is L2-resident between calls at these sizes), w lives in
+// shared memory, and each global reduction is an all-gather of the C partial
+// vectors through distributed shared memory + one cluster barrier (hardware,
+// sub-microsecond) instead of two grid barriers and a reduction kernel phase.
+// Every CTA sums the C partials in the same fixed order: bitwise identical
+// coefficients everywhere, deterministic.
+constexpr int kClThreads = 512;
+struct CArgs {
+    int64_t N;
+    int ncols;
+    const double *Q;
+    int64_t ldq;
+    double *w;
+    Ctrl *ctrl;
+    double *t_entry;
+    int check;
+    const double *pre_h;
+    PreReduce pre;
+    int rpb;  // rows per CTA
+    unsigned int *flags;  // grid-barrier slots: this launch zeroes the next launch's slot
+    unsigned int epoch;
+};
+
+__global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    grid_prepare(a.flags, a.epoch);  // keep the barrier-slot chain of the fused launches intact
+    if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the cluster
+    const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NWc = kClThreads / 32;
+    const int ncols = a.ncols, PS = ncols + 2;
+    extern __shared__ __align__(16) double csm[];
+    double *ws = csm;                       // rpb: this CTA's rows of w
+    double *hs = ws + a.rpb;                // PS: reduced coefficients
+    double *part = hs + PS;                 // 3 x PS: partial vectors (one buffer per reduction)
+    __shared__ double sh[32];
+    const int64_t r0 = (int64_t)me * a.rpb;
+    const int nr = (int)max((int64_t)0, min((int64_t)a.rpb, a.N - r0));
+    const double *Qb = a.Q + r0;
+    for (int i = tid; i < nr; i += kClThreads) {
+        double x;
+        if (a.pre.partial) {  // finish a dense split-K product (k_split_reduce order)
+            x = 0.0;
+            for (int q = 0; q < a.pre.splits; q++) x += a.pre.partial[q * a.N + r0 + i];
+            if (a.pre.yprev) x -= *a.pre.c_dev * a.pre.yprev[r0 + i];
+        } else {
+            x = a.w[r0 + i];
+        }
+        ws[i] = x;
+    }
+    __syncthreads();
+    // column dots of Q_b^T v (v in shared memory) -> part buffer pb[0..ncols)
+    auto coldots = [&](const double *v, double *pb) {
+        for (int j = wid; j < ncols; j += NWc) {
+            const double *qj = Qb + (int64_t)j * a.ldq;
+            double s0 = 0.0, s1 = 0.0;
+            int i = lane;
+            for (; i + 32 < nr; i += 64) {
+                s0 = fma(__ldg(qj + i), v[i], s0);
+                s1 = fma(__ldg(qj + i + 32), v[i + 32], s1);
+            }
+            if (i < nr) s0 = fma(__ldg(qj + i), v[i], s0);
+            double t = s0 + s1;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            if (lane == 0) pb[j] = t;
+        }
+    };
+    // v[i] -= sum_j Q[i][j] h[j] for the CTA's rows (thread per row, coalesced over rows)
+    auto rowupdate = [&](double *v, const double *h, double *nrm) {
+        for (int i = tid; i < nr; i += kClThreads) {
+            double s0 = 0.0, s1 = 0.0;
+            int j = 0;
+            for (; j + 1 < ncols; j += 2) {
+                s0 = fma(__ldg(Qb + i + (int64_t)j * a.ldq), h[j], s0);
+                s1 = fma(__ldg(Qb + i + (int64_t)(j + 1) * a.ldq), h[j + 1], s1);
+            }
+            if (j < ncols) s0 = fma(__ldg(Qb + i + (int64_t)j * a.ldq), h[j], s0);
+            const double x = v[i] - (s0 + s1);
+            v[i] = x;
+            if (nrm) *nrm = fma(x, x, *nrm);
+        }
+    };
+    // all CTAs: hs[0..cnt) = sum over the cluster's partial buffers (fixed order)
+    auto allreduce = [&](int buf, int cnt) {
+        cl.sync();  // every CTA's partials written
+        for (int j = tid; j < cnt; j += kClThreads) {
+            double t = 0.0;
+            for (int c = 0; c < C; c++) t += cl.map_shared_rank(part + buf * PS, c)[j];
+            hs[j] = t;
+        }
+        __syncthreads();
+    };
+    auto blocksum = [&](double v) -> double {
+        v = warp_sum(v);
+        __syncthreads();
+        if (lane == 0) sh[wid] = v;
+        __syncthreads();
+        double t = 0.0;
+        for (int q = 0; q < NWc; q++) t += sh[q];
+        __syncthreads();
+        return t;
+    };
+    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
+        for (int j = tid; j < ncols; j += kClThreads) hs[j] = a.pre_h[j];
+        __syncthreads();
+        rowupdate(ws, hs, nullptr);
+        __syncthreads();
+    }
+    double nrm_wp = 0.0;
+    if (ncols > 0) {
+        coldots(ws, part);  // phase A: partial h1
+        allreduce(0, ncols);
+        rowupdate(ws, hs, &nrm_wp);  // phase B: w' = w - Q h1
+        __syncthreads();
+        coldots(ws, part + PS);      // partial h2
+    } else {
+        for (int i = tid; i < nr; i += kClThreads) nrm_wp = fma(ws[i], ws[i], nrm_wp);
+    }
+    {
+        const double bn = blocksum(nrm_wp);
+        if (tid == 0) part[PS + ncols] = bn;
+    }
+    allreduce(1, ncols + 1);
+    const double nrmp = hs[ncols];
+    double hh = 0.0;
+    for (int j = tid; j < ncols; j += kClThreads) hh = fma(hs[j], hs[j], hh);
+    hh = blocksum(hh);
+    double beta2 = nrmp - hh;
+    const bool pyth = beta2 > 0.5 * nrmp;
+    double nrm2 = 0.0;
+    if (ncols > 0) rowupdate(ws, hs, pyth ? nullptr : &nrm2);  // phase C: w'' = w' - Q h2
+    __syncthreads();
+    if (!pyth) {  // explicit norm (uniform branch)
+        const double bn = blocksum(nrm2);
+        if (tid == 0) part[2 * PS] = bn;
+        allreduce(2, 1);
+        beta2 = hs[0];
+    }
+    const double beta = sqrt(fmax(beta2, 0.0));
+    const double amax = a.ctrl->amax[a.check & 1];
+    const bool bd = !(beta > 1e-14 * fmax(amax, 1.0));
+    if (me == 0 && tid == 0) {
+        if (bd) {
+            *a.t_entry = 0.0;
+            a.ctrl->amax[(a.check + 1) & 1] = amax;
+            a.ctrl->abort_check = a.check;
+            __threadfence();
+            a.ctrl->abort = 1;
+        } else {
+            *a.t_entry = beta;
+            a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
+        }
+    }
+    if (!bd)
+        for (int i = tid; i < nr; i += kClThreads) a.w[r0 + i] = ws[i] / beta;
+    cl.sync();  // no CTA exits while its shared memory may still be read remotely
+}
+
 // returns false if the fused path cannot be used (caller falls back)
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
@@ -1566,6 +1729,62 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
                 cudaMemset(g_qtbuf, 0, 16 * sizeof(unsigned long long));
             }
             a.tdbg = g_qtbuf;
+        }
+    }
+    // small bases: one thread-block cluster, DSMEM reductions (SVDSC_CLUSTER_CGS2:
+    // 0 off, else the byte threshold of N x ncols x 8 below which it is used)
+    {
+        static size_t cl_max = 0;
+        static bool cl_init = false;
+        if (!cl_init) {
+            cl_init = true;
+            cl_max = (size_t)2 << 20;  // measured: 12.7 vs 17.2 us per call at config 1 (1.2 MB);
+                                       // slower than the Q-resident kernel at 6 MB (config 2 V side)
+            if (const char *e = getenv("SVDSC_CLUSTER_CGS2")) cl_max = (size_t)strtoull(e, nullptr, 10);
+        }
+        const char *fse0 = getenv("SVDSC_FORCE_STREAM");
+        const int C = 16;
+        const int64_t rpb = (N + C - 1) / C;
+        const size_t smem = ((size_t)rpb + 4 * ((size_t)ncols + 2)) * sizeof(double);
+        if ((size_t)N * (size_t)std::max(ncols, 1) * 8 <= cl_max && smem <= 200 * 1024 && ncols <= 1022 &&
+            !(fse0 && fse0[0] == '1')) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_cgs2_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(k_cgs2_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                attr = true;
+            }
+            CArgs ca{};
+            ca.N = N;
+            ca.ncols = ncols;
+            ca.Q = Q;
+            ca.ldq = ldq;
+            ca.w = w;
+            ca.ctrl = ctrl;
+            ca.t_entry = t_entry;
+            ca.check = check;
+            ca.pre_h = pre_h;
+            if (fs.pre) ca.pre = *fs.pre;
+            ca.rpb = (int)rpb;
+            ca.flags = fs.flags;
+            ca.epoch = fs.epoch;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(C);
+            cfg.blockDim = dim3(kClThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = C;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, k_cgs2_cluster, ca) == cudaSuccess) {
+                count_launch();
+                return true;
+            }
+            cudaGetLastError();
         }
     }
     // try Q-resident mode: 2 CTAs per SM, then 1 (SVDSC_FORCE_STREAM=1 skips it: test hook)
