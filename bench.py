@@ -205,25 +205,33 @@ def main():
     for _ in range(args.warmup):
         solve()
     torch.cuda.synchronize()
+    # per-family breakdown from one untimed, fully profiled solve; it also picks
+    # the dominant kernel family whose CUDA events are kept in the timed region
+    # (one family only: every event record between kernels costs a few us)
+    H.profile(True)
+    solve()
+    torch.cuda.synchronize()
+    prof_all = H.profile_read()
+    H.profile(False)
+    fam = max(("Av", "ATu", "cgs2_fused"), key=lambda f: prof_all[f][0])
 
     # ---- timed region ----
     clocks = ClockSampler(local_rank)
     clocks.start()
-    # CUDA events on the library stream around the A / A^T products only (the
-    # dominant kernel family of the roofline); every other family is profiled in
-    # one extra untimed solve below (fewer event records in the timed region)
-    H.profile(True, families=("Av", "ATu"))
+    # CUDA events on the library stream around the dominant kernel family only
+    H.profile(True, families=(fam,))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    steps_total, launches, passes, res = 0, 0, [], None
+    steps_total, launches, passes, res, bytes_model = 0, 0, [], None, 0
     for _ in range(args.steps):
         res = solve()
         steps_total += res.info["steps"]
         launches += res.info["launches"]
         passes.append(res.info["passes"])
+        bytes_model += res.info["bytes_model"]
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -231,10 +239,6 @@ def main():
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     prof = H.profile_read()
-    H.profile(True)  # per-family breakdown of one more (untimed) solve
-    solve()
-    torch.cuda.synchronize()
-    prof_all = H.profile_read()
     H.profile(False)
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -242,12 +246,20 @@ def main():
         ms = float(tt.item())
     value = steps_total / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel family ----
+    # ---- roofline of the dominant kernel family (by device time in the timed region) ----
     peak, peak_src = load_peaks()
-    fam = max(("Av", "ATu"), key=lambda f: prof[f][0])
-    bytes_per_launch = Al.bytes_one_pass() if Al.kind == "dense" else (
-        12 * Al.nnz + 4 * (Al.m + 1) if fam == "Av" else 12 * Al.nnz + 4 * (Al.n + 1))
     f_ms, f_calls = prof[fam]
+    bA = Al.bytes_one_pass() if Al.kind == "dense" else 12 * Al.nnz + 4 * (Al.m + 1)
+    bAt = Al.bytes_one_pass() if Al.kind == "dense" else 12 * Al.nnz + 4 * (Al.n + 1)
+    if fam == "cgs2_fused":
+        # algorithmic CGS2 bytes (8 N (3i + 5) per re-orthogonalization)
+        # = the solves' modelled step bytes minus the products' (one A and one A^T
+        # pass per step, plus the u_1 product)
+        # (the library's model charges bA for both products of a step)
+        cgs_bytes = bytes_model - steps_total * 2 * bA - args.steps * bA
+        bytes_per_launch = cgs_bytes / max(f_calls, 1)
+    else:
+        bytes_per_launch = bA if fam == "Av" else bAt
     traffic = None
     try:  # DRAM bytes per launch of this kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -313,7 +325,9 @@ def main():
                        "parallelism": f"rows{world}" if world > 1 else "single",
                        "step_hbm_gb_per_s": step_bytes * (steps_total / (ms / 1e3)) / 1e9,
                        "step_bytes_model": step_bytes},
-            "roofline": {"bound": "hbm", "kernel": f"{fam} product ({'gemv' if A.kind == 'dense' else 'spmv'})",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("fused CGS2 re-orthogonalization (3 sweeps of U_i / V_i)" if fam == "cgs2_fused"
+                                    else f"{fam} product ({'gemv' if A.kind == 'dense' else 'spmv'})"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "bytes_per_launch": bytes_per_launch, "avg_launch_us": 1e3 * f_ms / max(f_calls, 1),
