@@ -10,6 +10,9 @@ Tolerances (DESIGN.md "Parity tolerances"):
   * end to end (BASELINE north_star): |s_i - s_i^or| <= 1e-10 s_1, principal
     angles (from sines) <= 1e-8, same pass count (reading Q18).
 """
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -17,6 +20,8 @@ import torch
 import oracle as O
 import workloads as W
 from helpers import certificates, gamma, orth_error, sin_max_angle
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 pytestmark = pytest.mark.gpu
 
@@ -343,3 +348,38 @@ def test_deterministic_and_host_path(S, H):
     Sh, Uh, Vh, Rh, st, info = S.svds_c_host(H, wl.A, wl.k, t=wl.t, v0=wl.v0)
     assert np.array_equal(Sh, a.S.cpu().numpy()) and np.array_equal(Uh, a.U.cpu().numpy())
     assert np.array_equal(Vh, a.V.cpu().numpy())
+
+
+# ---------------------------------------------------------------- scaled replicas of configs 4 and 5
+def test_svds_parity_config4_scaled(S, H):
+    """BASELINE config 4 (power-law rows, 4M x 2M, k = 100, t = 300) at 1/200
+    scale: full oracle parity (SURVEY.md 8(c) pin (i) for configs 4-5)."""
+    wl = W.config(4, scale=200)
+    r, r_or, U, V, s = _e2e(S, H, wl)
+    assert sin_max_angle(U, r_or.U) <= 1e-8 and sin_max_angle(V, r_or.V) <= 1e-8
+    r1, r2 = certificates(wl.A, s, U, V)
+    assert np.all(r1 <= 1e-10 * s[0])
+    assert orth_error(U) <= 1e-10 and orth_error(V) <= 1e-10
+
+
+def test_svds_parity_config5_scaled(S, H):
+    """BASELINE config 5 (banded-plus-random rows, 30M x 5M, k = 200, t = 600) at
+    1/2000 scale against the oracle's stored result (tests/golden/
+    oracle_config5_div2000.json, written by tools/make_golden_c5.py, which calls
+    only oracle/): sigma parity, same pass count, and the a-posteriori
+    certificates of the GPU vectors.  Exercises the t = 600 paths (p = 601
+    cluster Jacobi with the register-pull exchange, 601-column CGS2)."""
+    g = json.load(open(os.path.join(GOLD, "oracle_config5_div2000.json")))
+    wl = W.config(5, scale=2000)
+    assert (wl.A.m, wl.A.n, int(wl.A.nnz), wl.k, wl.t) == (g["m"], g["n"], g["nnz"], g["k"], g["t"])
+    M = S.Matrix.from_host(H, wl.A)
+    r = S.svds_c(M, wl.k, tol=wl.tol, t=wl.t, maxit=wl.maxit, v0=dev(wl.v0), fixed_passes=g["passes"])
+    s = r.S.cpu().numpy()
+    S_or = np.array(g["S"])
+    assert np.abs(s - S_or).max() <= 1e-10 * S_or[0]
+    assert bool(r.info["converged"]) == g["converged"]
+    U, V = r.U.cpu().numpy(), r.V.cpu().numpy()
+    r1, r2 = certificates(wl.A, s, U, V)
+    assert np.all(r1 <= 1e-10 * s[0])
+    assert np.all(np.abs(r2 - r.resid.cpu().numpy()) * s <= 1e-8 * s[0])
+    assert orth_error(U) <= 1e-10 and orth_error(V) <= 1e-10
