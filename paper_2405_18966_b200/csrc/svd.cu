@@ -199,7 +199,10 @@ __device__ __forceinline__ double jacobi_tan(double al, double be, double gam) {
 // (t = tan theta, a, b) for k_apply_log; rotations of one local round (all
 // CTAs) touch disjoint columns, so replaying them round by round is exact.
 // debugging aid (SVDSC_KTIMING=1 builds with kJacobiTiming): cross-round section cycles of CTA 0, warp 0
-constexpr bool kJacobiTiming = true;
+#ifndef SVDSC_JACOBI_TIMING
+#define SVDSC_JACOBI_TIMING 0
+#endif
+constexpr bool kJacobiTiming = SVDSC_JACOBI_TIMING != 0;  // build with -DSVDSC_JACOBI_TIMING=1 to enable
 __device__ unsigned long long g_jt[8];
 
 struct RotLog {

@@ -1,6 +1,7 @@
 # round-1 end check on one B200: GPU tests, smoke, benches (ours + reference arm), ncu launch list + full capture
-mkdir -p gpurun_out/r01
-O=gpurun_out/r01
+mkdir -p gpurun_out/r01b
+mkdir -p gpurun_out/r01b
+O=gpurun_out/r01b
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $O/gpu.txt 2>&1
 lscpu | grep -E "Model name|^CPU\(s\)" > $O/host.txt; nproc >> $O/host.txt
 timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > $O/gpu_tests.log 2>&1; echo tests_exit=$?
@@ -16,5 +17,6 @@ $CMD > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches_config2.csv $CMD > $O/ncu_launch.log 2>&1
 echo launches_exit=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemv_t|k_gemv_n|k_cgs2_fused|k_jacobi_block" -s 20 -c 4 -o $O/prof_config2 $CMD > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_jacobi_block|k_apply_log|k_recombine_dmma" -c 3 -o $O/prof_config2_svd $CMD > $O/ncu_full_svd.log 2>&1
 echo full_exit=$?
 ls -la $O
