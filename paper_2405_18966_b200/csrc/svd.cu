@@ -59,6 +59,17 @@ __global__ void __launch_bounds__(1024) k_copy_T(int p, const double *__restrict
         for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += sh[i];
         ctrl->svd_tiny = (double)p * 2.220446049250313e-16 * sqrt(tot);
     }
+    if (threadIdx.x < 16) ctrl->jprog[threadIdx.x] = 0u;
+    if (threadIdx.x == 16) ctrl->jdone = 0u;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // round-robin (circle method) pairing: round rnd in [0, pe-1), slot q in [0, pe/2)
@@ -278,14 +289,106 @@ constexpr int kJThreads = 640; // 20 warps: one warp per pair, <= 20 pairs per C
 constexpr int kJMaxH = 12;     // preferred half-block width (measured, tools/time_ops.py)
 constexpr int kMaxPairs = kJThreads / 32;
 
+// Replay role of the combined Jacobi launch: replay CTA j owns rows
+// [j R, j R + R) of V (thread (q, i) applies rotation q of a round to row i, as
+// k_apply_log), reading log rounds as soon as every Jacobi CTA has published
+// them (ld.acquire on Ctrl::jprog), and the final round count once jdone is set.
+__device__ void jacobi_replay_role(int p, int per_round, int64_t rps, const RotLog *__restrict__ rlog, Ctrl *ctrl,
+                                   double *V, int R, int lrc, int j, int C) {
+    extern __shared__ __align__(16) double Wsm[];
+    double *rows = Wsm;                                                        // R x p
+    RotLog *buf = reinterpret_cast<RotLog *>(rows + (((int64_t)R * p + 1) & ~1));  // lrc x per_round
+    __shared__ long long s_avail;
+    const int r0 = j * R;
+    if (r0 >= p) return;
+    for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
+        const int i = idx / p, c = idx % p;
+        rows[idx] = (r0 + i == c) ? 1.0 : 0.0;
+    }
+    const int q = threadIdx.x % per_round, i = threadIdx.x / per_round;
+    const bool act = i < R && r0 + i < p;
+    double *row = rows + i * p;
+    int64_t base = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            long long avail;
+            for (;;) {
+                if (ld_acquire_u32(&ctrl->jdone)) {
+                    avail = -1 - (long long)(*(volatile int *)&ctrl->svd_sweeps) * rps;  // encoded: done
+                    break;
+                }
+                unsigned mn = 0xffffffffu;
+                for (int c = 0; c < C; c++) mn = min(mn, ld_acquire_u32(&ctrl->jprog[c]));
+                if ((int64_t)mn >= base + lrc) {
+                    avail = mn;
+                    break;
+                }
+                __nanosleep(200);
+            }
+            s_avail = avail;
+        }
+        __syncthreads();
+        const long long av = s_avail;
+        __syncthreads();
+        const bool done = av < 0;
+        const int64_t upto = done ? (-1 - av) : av;
+        if (base >= upto) {
+            if (done) break;
+            continue;
+        }
+        const int nr = (int)min((int64_t)lrc, upto - base);
+        const int n16 = nr * per_round * 2;
+        const char *src = reinterpret_cast<const char *>(rlog + base * per_round);
+        for (int t = threadIdx.x; t < n16; t += blockDim.x) {
+            const unsigned saddr = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char *>(buf) + 16 * t);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + 16 * t));
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        for (int k = 0; k < nr; k++) {
+            if (act) {
+                const RotLog &e = buf[k * per_round + q];
+                const double c = e.c, s = e.s;
+                if (c != 0.0) {
+                    const double x = row[e.a], y = row[e.b];
+                    row[e.a] = c * x - s * y;
+                    row[e.b] = s * x + c * y;
+                }
+            }
+            __syncthreads();
+        }
+        base += nr;
+    }
+    for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
+        const int ii = idx / p, c = idx % p;
+        if (r0 + ii < p) V[(r0 + ii) + (int64_t)c * p] = rows[idx];
+    }
+}
+
 template <bool CL, int kRPL>
 __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const double *__restrict__ W0, double *Wout,
                                                        RotLog *rlog, int max_sweeps, Ctrl *ctrl, const int *abort,
-                                                       double ctol, int use_bulk) {
+                                                       double ctol, int use_bulk, double *Vrep, int rep_R, int rep_lrc) {
     if (aborted(abort)) return;
     cg::cluster_group cl = cg::this_cluster();
     const int C = CL ? (int)cl.num_blocks() : 1;
     const int me = CL ? (int)cl.block_rank() : 0;
+    if (CL && rep_R > 0 && (int)blockIdx.x >= C) {
+        // replay role (clusters 1..): V rows from the rotation log, following the
+        // Jacobi cluster round by round (co-residency: cooperative launch)
+        jacobi_replay_role(p, C * h, jacobi_rounds_per_sweep(C, h), rlog, ctrl, Vrep, rep_R, rep_lrc,
+                           (int)blockIdx.x - C, C);
+        return;
+    }
+    // publish "rounds logged" for the replay role (after the round's barrier)
+    // (every 8 rounds and at block-round ends: the fence is on the round's
+    // critical path)
+    auto publish = [&](int64_t rounds_done, bool force = false) {
+        if (rep_R > 0 && threadIdx.x == 0 && (force || (rounds_done & 7) == 0)) {
+            __threadfence();
+            st_release_u32(&ctrl->jprog[me], (unsigned)rounds_done);
+        }
+    };
     extern __shared__ __align__(16) double Wsm[];  // slot s, local column i: Wl + (s*h + i)*p
     // bulk-copy exchange: two half-block buffer sets, Wl = the current one
     // (push model: every CTA sends its two half-blocks to their next owners
@@ -385,6 +488,7 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                     }
                 }
                 __syncthreads();
+                publish((int64_t)(sweep - 1) * rps + lr + 1, lr + 1 == lrounds);
             }
             } else {
             // block rounds >= 1: only the h^2 cross pairs of the two half-blocks
@@ -450,6 +554,7 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                 }
                 if (prof) c3 = clock64();
                 __syncthreads();
+                publish(rbase + rr + 1, rr + 1 == h);
                 if (prof) {
                     const long long c4 = clock64();
                     atomicAdd(&g_jt[0], (unsigned long long)(c1 - c0));
@@ -576,6 +681,10 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
     if (me == 0 && threadIdx.x == 0) {
         ctrl->svd_sweeps = conv ? sweep : max_sweeps;
         ctrl->svd_status = conv ? 0 : (int)SVDSC_ESVD_NOCONV;
+        if (rep_R > 0) {
+            __threadfence();
+            st_release_u32(&ctrl->jdone, 1u);
+        }
     }
     if (CL) cl.sync();
 }
@@ -986,12 +1095,14 @@ void jacobi_geometry(int p, int &C, int &h) {
 }
 }  // namespace
 
+// *replayed: set when the V replay ran inside the same (cooperative) launch
 template <int R>
 cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *rlog, Ctrl *ctrl, const int *abort,
-                          double ctol, cudaStream_t s) {
+                          double ctol, cudaStream_t s, double *Vw, bool *replayed) {
+    *replayed = false;
     if (C == 1) {
         cudaFuncSetAttribute(k_jacobi_block<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol, 0);
+        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol, 0, nullptr, 0, 0);
         return cudaGetLastError();
     }
     // bulk-copy exchange needs the second buffer set (SVDSC_JACOBI_PULL=1: register pull)
@@ -1012,8 +1123,38 @@ cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *r
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // combined launch: clusters 1.. replay V from the log while cluster 0 runs the
+    // sweeps (cooperative: every CTA co-resident, else the launch fails and the
+    // replay runs afterwards as k_apply_log; SVDSC_JACOBI_SEPARATE=1 forces that)
+    const char *sep = getenv("SVDSC_JACOBI_SEPARATE");
+    if (!(sep && sep[0] == '1')) {
+        const int per_round = C * h;
+        const int RR = std::max(1, kJThreads / per_round);
+        const int nrep = (p + RR - 1) / RR;
+        const size_t rows_b = ((size_t)RR * p + 2) * 8;
+        const int lrc = (int)std::min<size_t>(16, (200 * 1024 - std::min<size_t>(rows_b, 200 * 1024)) /
+                                                       ((size_t)per_round * sizeof(RotLog)));
+        const int nclus = 1 + (nrep + C - 1) / C;
+        if (lrc >= 1 && rows_b + (size_t)lrc * per_round * sizeof(RotLog) <= 210 * 1024) {
+            cudaLaunchConfig_t c2 = cfg;
+            c2.gridDim = dim3(C * nclus);
+            c2.dynamicSmemBytes = std::max(smem, rows_b + (size_t)lrc * per_round * sizeof(RotLog));
+            cudaLaunchAttribute at2[2];
+            at2[0] = attr[0];
+            at2[1].id = cudaLaunchAttributeCooperative;
+            at2[1].val.cooperative = 1;
+            c2.attrs = at2;
+            c2.numAttrs = 2;
+            if (cudaLaunchKernelEx(&c2, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort,
+                                   ctol, use_bulk, Vw, RR, lrc) == cudaSuccess) {
+                *replayed = true;
+                return cudaSuccess;
+            }
+            cudaGetLastError();
+        }
+    }
     return cudaLaunchKernelEx(&cfg, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort, ctol,
-                              use_bulk);
+                              use_bulk, (double *)nullptr, 0, 0);
 }
 
 size_t small_svd_log_doubles(int p) {
@@ -1037,18 +1178,22 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
         const size_t smem = (size_t)2 * h * p * 8;
         cudaError_t e;
         const int rpl = (p + 31) / 32;
-        e = rpl <= 1 ? launch_jacobi<1>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 2 ? launch_jacobi<2>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 3 ? launch_jacobi<3>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 4 ? launch_jacobi<4>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 5 ? launch_jacobi<5>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 6 ? launch_jacobi<6>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 8 ? launch_jacobi<8>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 10 ? launch_jacobi<10>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 12 ? launch_jacobi<12>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-          : rpl <= 16 ? launch_jacobi<16>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
-                      : launch_jacobi<20>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s);
-        if (e == cudaSuccess) {
+        bool replayed = false;
+        e = rpl <= 1 ? launch_jacobi<1>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 2 ? launch_jacobi<2>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 3 ? launch_jacobi<3>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 4 ? launch_jacobi<4>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 5 ? launch_jacobi<5>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 6 ? launch_jacobi<6>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 8 ? launch_jacobi<8>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 10 ? launch_jacobi<10>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 12 ? launch_jacobi<12>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+          : rpl <= 16 ? launch_jacobi<16>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
+                      : launch_jacobi<20>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed);
+        if (e == cudaSuccess && replayed) {
+            count_launch();
+            done = true;
+        } else if (e == cudaSuccess) {
             count_launch();
             const int per_round = C * h;
             const int rps = (int)jacobi_rounds_per_sweep(C, h);
