@@ -505,12 +505,13 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                 xr[u] = (has && r < p) ? Wl[(int64_t)wid * p + r] : 0.0;
             }
             const int64_t rbase = (int64_t)(sweep - 1) * rps + lrounds + (int64_t)(br - 1) * h;
-            for (int rr = 0; rr < h; rr++) {
+            int jy = wid < h ? wid : 0;  // (wid + rr) mod h, advanced without a division
+            for (int rr = 0; rr < h; rr++, jy = (jy + 1 == h) ? 0 : jy + 1) {
                 long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
                 const bool prof = kJacobiTiming && me == 0 && threadIdx.x == 0;
                 if (prof) c0 = clock64();
                 if (has) {
-                    const int j = h + (wid + rr) % h;
+                    const int j = h + jy;
                     const int gy = gcol[j];
                     const bool live = gx < p && gy < p;
                     double *py = Wl + (int64_t)j * p;
