@@ -1037,7 +1037,8 @@ bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
     if (nc <= 64) return launch_stream2<32, 4, 2>(a, nsm, s);
     if (nc <= 128) return launch_stream2<32, 4, 4>(a, nsm, s);
     if (nc <= 192) return launch_stream2<32, 3, 6>(a, nsm, s);
-    if (nc <= 256) return launch_stream2<32, 3, 8>(a, nsm, s);
+    // (three 32-row stages stop fitting near 245 columns: two stages beyond)
+    if (nc <= 256) return launch_stream2<32, 3, 8>(a, nsm, s) || launch_stream2<32, 2, 8>(a, nsm, s);
     if (nc <= 320) return launch_stream2<32, 2, 10>(a, nsm, s);
     if (nc <= 384) return launch_stream2<32, 2, 12>(a, nsm, s);
     if (nc <= 512) return launch_stream2<16, 2, 16>(a, nsm, s);
