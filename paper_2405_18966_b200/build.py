@@ -15,6 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+FLAGS += os.environ.get("SVDSC_NVCC_EXTRA", "").split()  # tuning experiments only
 
 
 def stale() -> bool:

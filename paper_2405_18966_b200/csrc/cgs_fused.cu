@@ -817,15 +817,47 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     auto tval = [&](const double *T, int rr, int m) -> double {
         return T[(lane + 32 * m) * RT + (((rr >> 1) ^ sw) << 1) + (rr & 1)];
     };
-    // per-row dot with the lane's coefficients hreg; result on every lane
-    auto rowdot = [&](const double *T, int rr, const double (&hreg)[M]) -> double {
-        double s0 = 0.0, s1 = 0.0;
+    // sums of the warp's RPW row partials.  RPW == 2 is a reduce-scatter: the
+    // first level swaps the other row's partial across the half-warps, so both
+    // rows take 5 shuffles instead of 10.  Afterwards p[q] is valid on lanes
+    // [q * kHalf, (q + 1) * kHalf); row q is written by lane q * kHalf.
+    static_assert(RPW == 1 || RPW == 2, "stream2 handles 1 or 2 rows per warp");
+    constexpr int kHalf = 32 / RPW;
+    auto reduce_rows = [&](double (&p)[RPW]) {
+        if constexpr (RPW == 2) {
+            const bool hi = lane & 16;
+            double x = (hi ? p[1] : p[0]) + __shfl_xor_sync(0xffffffffu, hi ? p[0] : p[1], 16);
 #pragma unroll
-        for (int m = 0; m < M; m += 2) {
-            if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
-            if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+            for (int off = 8; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+            p[0] = x;
+            p[1] = x;
+        } else {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
         }
-        return warp_sum(s0 + s1);
+    };
+    // the warp's RPW row dots with the lane's coefficients hreg
+    auto rowdots = [&](const double *T, const double (&hreg)[M], double (&out)[RPW]) {
+#pragma unroll
+        for (int q = 0; q < RPW; q++) {
+            const int rr = wid + NW * q;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < M; m += 2) {
+                if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
+                if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+            }
+            out[q] = s0 + s1;
+        }
+        reduce_rows(out);
+    };
+    // every lane needs both rows' values (phase B's column accumulation)
+    auto allrows = [&](double (&p)[RPW]) {
+        if constexpr (RPW == 2) {
+            const double other = __shfl_xor_sync(0xffffffffu, p[0], 16);
+            if (lane & 16) p[0] = other;
+            else p[1] = other;
+        }
     };
     // cross-warp column sums of acc -> partial[block][j]
     auto flush_cols = [&](const double (&acc)[M]) {
@@ -850,21 +882,31 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         }
     };
 
+    // phase stamps (SVDSC_KTIMING): thread 0 only, kept in shared memory so
+    // they cost no registers in the streaming loops
+    __shared__ long long tk[8];
+    int ntk = 0;
+    auto stamp = [&]() {
+        if (a.tdbg && threadIdx.x == 0 && ntk < 8) tk[ntk] = clock64();
+        ntk++;
+    };
     double hreg[M];
     if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
         load_h(a.pre_h, hreg);
         run_tiles([&](int k, const double *T, const double *W) {
+            double s[RPW];
+            rowdots(T, hreg, s);
 #pragma unroll
             for (int q = 0; q < RPW; q++) {
                 const int rr = wid + NW * q;
-                const double s = rowdot(T, rr, hreg);
                 const int64_t r = rb + (int64_t)k * RT + rr;
-                if (lane == 0 && r < re) a.w[r] = W[rr] - s;
+                if (lane == q * kHalf && r < re) a.w[r] = W[rr] - s[q];
             }
         });
         grid_sync(a.flags, a.epoch + (++nbar));
     }
 
+    stamp();
     double nrm_wp = 0.0;
     if (ncols > 0) {
         // phase A: partial h1
@@ -884,29 +926,66 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         flush_cols(acc);
         prefetch();  // phase B re-reads the same tiles: start them under the reduction
         prefetched = true;
+        stamp();
         grid_sync(a.flags, a.epoch + (++nbar));
+        stamp();
         sreduce_cols(a, ncols, a.h1, sh);
         grid_sync(a.flags, a.epoch + (++nbar));
         load_h(a.h1, hreg);
+        stamp();
         // phase B: w' = w - Q h1 (written back), partial h2, ||w'||^2
 #pragma unroll
         for (int m = 0; m < M; m++) acc[m] = 0.0;
-        run_tiles([&](int k, const double *T, const double *W) {
+        if constexpr (RPW * M > 24 || M > 16) {  // wide bases: registers hold acc + hreg only
+            run_tiles([&](int k, const double *T, const double *W) {
+                double part[RPW];
+                rowdots(T, hreg, part);
+                allrows(part);
 #pragma unroll
-            for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
-                const double s = rowdot(T, rr, hreg);
-                const int64_t r = rb + (int64_t)k * RT + rr;
-                const double v = (r < re) ? W[rr] - s : 0.0;
-                if (lane == 0 && r < re) {
-                    a.w[r] = v;
-                    nrm_wp = fma(v, v, nrm_wp);
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    const double v = (r < re) ? W[rr] - part[q] : 0.0;
+                    if (lane == q * kHalf && r < re) {
+                        a.w[r] = v;
+                        nrm_wp = fma(v, v, nrm_wp);
+                    }
+#pragma unroll
+                    for (int m = 0; m < M; m++)
+                        if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), v, acc[m]);
                 }
+            });
+        } else {  // the tile values read from shared memory once, kept in registers
+            run_tiles([&](int k, const double *T, const double *W) {
+                double tv[RPW][M], part[RPW];
 #pragma unroll
-                for (int m = 0; m < M; m++)
-                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), v, acc[m]);
-            }
-        });
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int m = 0; m < M; m++) {
+                        tv[q][m] = (lane + 32 * m < ncols) ? tval(T, rr, m) : 0.0;
+                        if (m & 1) s1 = fma(tv[q][m], hreg[m], s1);
+                        else s0 = fma(tv[q][m], hreg[m], s0);
+                    }
+                    part[q] = s0 + s1;
+                }
+                reduce_rows(part);
+                allrows(part);
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    const double v = (r < re) ? W[rr] - part[q] : 0.0;
+                    if (lane == q * kHalf && r < re) {
+                        a.w[r] = v;
+                        nrm_wp = fma(v, v, nrm_wp);
+                    }
+#pragma unroll
+                    for (int m = 0; m < M; m++) acc[m] = fma(tv[q][m], v, acc[m]);
+                }
+            });
+        }
         flush_cols(acc);
     } else {
         run_tiles([&](int k, const double *, const double *W) {
@@ -914,7 +993,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             for (int q = 0; q < RPW; q++) {
                 const int rr = wid + NW * q;
                 const int64_t r = rb + (int64_t)k * RT + rr;
-                if (lane == 0 && r < re) nrm_wp = fma(W[rr], W[rr], nrm_wp);
+                if (lane == q * kHalf && r < re) nrm_wp = fma(W[rr], W[rr], nrm_wp);
             }
         });
     }
@@ -928,10 +1007,12 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         prefetch();
         prefetched = true;
     }
+    stamp();
     grid_sync(a.flags, a.epoch + (++nbar));
     sreduce_cols(a, ncols + 1, a.h2, sh);
     grid_sync(a.flags, a.epoch + (++nbar));
     load_h(a.h2, hreg);
+    stamp();
     const double nrmp = __ldcg(a.h2 + ncols);
     double hh = 0.0;
     for (int j = tid; j < ncols; j += kSThr) {
@@ -949,13 +1030,17 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         beta = sqrt(beta2);
         bd = !(beta > thr);
         if (!bd && ncols > 0) {
+            // one reciprocal per kernel instead of a division per row (the
+            // division sequence would double this sweep's instruction count)
+            const double rbeta = 1.0 / beta;
             run_tiles([&](int k, const double *T, const double *W) {
+                double s[RPW];
+                rowdots(T, hreg, s);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
                     const int rr = wid + NW * q;
-                    const double s = rowdot(T, rr, hreg);
                     const int64_t r = rb + (int64_t)k * RT + rr;
-                    if (lane == 0 && r < re) a.w[r] = (W[rr] - s) / beta;
+                    if (lane == q * kHalf && r < re) a.w[r] = (W[rr] - s[q]) * rbeta;
                 }
             });
         } else if (!bd) {
@@ -965,13 +1050,14 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         double nrm2 = 0.0;
         if (ncols > 0) {
             run_tiles([&](int k, const double *T, const double *W) {
+                double s[RPW];
+                rowdots(T, hreg, s);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
                     const int rr = wid + NW * q;
-                    const double s = rowdot(T, rr, hreg);
                     const int64_t r = rb + (int64_t)k * RT + rr;
-                    if (lane == 0 && r < re) {
-                        const double v = W[rr] - s;
+                    if (lane == q * kHalf && r < re) {
+                        const double v = W[rr] - s[q];
                         a.w[r] = v;
                         nrm2 = fma(v, v, nrm2);
                     }
@@ -989,6 +1075,13 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         bd = !(beta > thr);
         if (!bd)
             for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
+    }
+    stamp();
+    if (a.tdbg && threadIdx.x == 0 && ntk == 7 && a.N >= (int64_t)a.tdbg[15] && ncols >= (int)a.tdbg[14]) {
+        // phases: A | wait1 | reduce1+bar2+load | B | red2 | C
+        for (int q = 1; q < 7; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
+        atomicAdd(a.tdbg + 10, 1ull);
+        atomicAdd(a.tdbg + 11, (unsigned long long)ntiles);
     }
     cp_wait<0>();  // a prefetch may be pending if phase C was skipped
     if (blockIdx.x == 0 && tid == 0) {
