@@ -765,7 +765,9 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     const int tile_d = ncols * RT;
     double *buf = smem_s;               // NS x ncols x RT (swizzled)
     double *wt = buf + NS * tile_d;     // NS x RT
-    double *red = wt + NS * RT;         // NW x ncols (cross-warp column sums)
+    // NW x ncols cross-warp column sums: aliases the ring, which is idle when
+    // a phase flushes (its last tile consumed, the next prefetch not issued)
+    double *red = buf;
     const int64_t rb = (int64_t)blockIdx.x * a.rpb;
     const int64_t re = min(a.N, rb + a.rpb);
     const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
@@ -1101,7 +1103,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
 template <int RT, int NS, int M>
 bool launch_stream2(const SArgs &a0, int nsm, cudaStream_t s) {
     SArgs a = a0;
-    const size_t smem = ((size_t)NS * a.ncols * RT + NS * RT + 16 * (size_t)a.ncols) * sizeof(double);
+    const size_t smem = ((size_t)NS * a.ncols * RT + NS * RT) * sizeof(double);
     if (smem > 220 * 1024 || a.ncols > 32 * M) return false;
     static bool attr = false;
     if (!attr) {
@@ -1130,8 +1132,7 @@ bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
     if (nc <= 64) return launch_stream2<32, 4, 2>(a, nsm, s);
     if (nc <= 128) return launch_stream2<32, 4, 4>(a, nsm, s);
     if (nc <= 192) return launch_stream2<32, 3, 6>(a, nsm, s);
-    // (three 32-row stages stop fitting near 245 columns: two stages beyond)
-    if (nc <= 256) return launch_stream2<32, 3, 8>(a, nsm, s) || launch_stream2<32, 2, 8>(a, nsm, s);
+    if (nc <= 256) return launch_stream2<32, 3, 8>(a, nsm, s);
     if (nc <= 320) return launch_stream2<32, 2, 10>(a, nsm, s);
     if (nc <= 384) return launch_stream2<32, 2, 12>(a, nsm, s);
     if (nc <= 512) return launch_stream2<16, 2, 16>(a, nsm, s);

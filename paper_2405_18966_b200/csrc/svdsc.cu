@@ -741,6 +741,7 @@ svdsc_status svdsc_set_stream(svdsc_handle *h, void *stream) {
 
 void svdsc_destroy(svdsc_handle *h) {
     if (!h) return;
+    if (getenv("SVDSC_KTIMING")) ktiming_dump();  // op-level calls (tools/probe_cgs2.py)
     if (h->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm);
     if (h->hctrl) cudaFreeHost(h->hctrl);
     if (h->scratch) cudaFree(h->scratch);

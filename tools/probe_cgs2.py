@@ -36,7 +36,8 @@ def main():
     ts.sort()
     us = ts[len(ts) // 2]
     print(f"{os.environ.get('SVDSC_LIB_VARIANT', 'libsvdsc.so')} N={N} c={c} median {us:.1f} us "
-          f"({3 * 8 * N * c / us / 1e3:.0f} GB/s over 3 sweeps of Q)")
+          f"({3 * 8 * N * c / us / 1e3:.0f} GB/s over 3 sweeps of Q)", flush=True)
+    H.close()  # svdsc_destroy prints the SVDSC_KTIMING phase counters
 
 
 if __name__ == "__main__":
