@@ -40,14 +40,15 @@ class _Matrix(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("tol", ctypes.c_double), ("t", ctypes.c_int32),
                 ("maxit", ctypes.c_int32), ("fixed_passes", ctypes.c_int32),
-                ("reorth", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+                ("reorth", ctypes.c_int32), ("seed", ctypes.c_uint64), ("pro_delta", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
     _fields_ = [("passes", ctypes.c_int32), ("restarts", ctypes.c_int32),
                 ("converged", ctypes.c_int32), ("t_used", ctypes.c_int32),
                 ("steps", ctypes.c_int64), ("matvecs", ctypes.c_int64),
-                ("breakdowns", ctypes.c_int64), ("max_resid", ctypes.c_double)]
+                ("breakdowns", ctypes.c_int64), ("max_resid", ctypes.c_double),
+                ("reorths", ctypes.c_int64)]
 
 
 def lib():
@@ -75,6 +76,11 @@ def lib():
         L.or_lbp.argtypes = [ctypes.POINTER(_Matrix), ctypes.POINTER(_Opts), I64, P, P, P, P,
                              ctypes.POINTER(_Info)]
         L.or_lbp.restype = ctypes.c_int
+        D = ctypes.c_double
+        L.or_pro_anorm.argtypes = [P, I64, I64]
+        L.or_pro_anorm.restype = D
+        L.or_pro_nu_update.argtypes = [P, I64, I64, P, P, D, D]
+        L.or_pro_mu_update.argtypes = [P, I64, I64, P, P, D, D]
         _lib = L
     return _lib
 
@@ -183,12 +189,15 @@ class Result:
     matvecs: int
     breakdowns: int
     max_resid: float
+    reorths: int = 0
 
 
-def svds(A, k, v0, tol=1e-10, t=0, maxit=100, fixed_passes=0, reorth=2, seed=0) -> Result:
-    """Alg. 2: the restarted truncated SVD."""
+def svds(A, k, v0, tol=1e-10, t=0, maxit=100, fixed_passes=0, reorth=2, seed=0, pro_delta=0.0) -> Result:
+    """Alg. 2: the restarted truncated SVD.  reorth: 2 full
+    CGS2, 1 partial (omega recurrence, reading Q20), 0 off."""
     M, keep = _matrix(A)
-    o = _Opts(k=k, tol=tol, t=t, maxit=maxit, fixed_passes=fixed_passes, reorth=reorth, seed=seed)
+    o = _Opts(k=k, tol=tol, t=t, maxit=maxit, fixed_passes=fixed_passes, reorth=reorth, seed=seed,
+              pro_delta=pro_delta)
     v0 = _f64(v0)
     S = np.zeros(k)
     U = np.zeros((A.m, k), order="F")
@@ -200,13 +209,13 @@ def svds(A, k, v0, tol=1e-10, t=0, maxit=100, fixed_passes=0, reorth=2, seed=0) 
     if st < 0:
         raise RuntimeError(f"or_svds failed with status {st}")
     return Result(S, U, V, res, st, info.passes, info.restarts, bool(info.converged),
-                  info.t_used, info.steps, info.matvecs, info.breakdowns, info.max_resid)
+                  info.t_used, info.steps, info.matvecs, info.breakdowns, info.max_resid, info.reorths)
 
 
-def lbp(A, t, v0, reorth=2, seed=0):
+def lbp(A, t, v0, reorth=2, seed=0, pro_delta=0.0):
     """Alg. 1 first pass LBP(A, t+1): returns U (m x t+1), V (n x t+1), T, info."""
     M, keep = _matrix(A)
-    o = _Opts(k=1, tol=1e-10, t=t, maxit=1, fixed_passes=1, reorth=reorth, seed=seed)
+    o = _Opts(k=1, tol=1e-10, t=t, maxit=1, fixed_passes=1, reorth=reorth, seed=seed, pro_delta=pro_delta)
     U = np.zeros((A.m, t + 1), order="F")
     V = np.zeros((A.n, t + 1), order="F")
     T = np.zeros((t + 1, t + 1), order="F")
@@ -217,3 +226,29 @@ def lbp(A, t, v0, reorth=2, seed=0):
     if st < 0:
         raise RuntimeError(f"or_lbp failed with status {st}")
     return U, V, T, info
+
+
+# ---- partial re-orthogonalization (reading Q20): one omega update each ----
+def pro_anorm(T, ncols):
+    T = np.asfortranarray(T, dtype=np.float64)
+    return lib().or_pro_anorm(T.ctypes.data, T.shape[0], ncols)
+
+
+def pro_nu_update(T, i, mu, nu, beta, eps1):
+    """row of v_{i-1} (nu) -> row of v_i, given the row mu of u_{i-1}"""
+    T = np.asfortranarray(T, dtype=np.float64)
+    mu = _f64(mu)
+    out = np.zeros(max(len(nu), i + 1))
+    out[:len(nu)] = nu
+    lib().or_pro_nu_update(T.ctypes.data, T.shape[0], i, _p(mu), _p(out), beta, eps1)
+    return out[:i + 1]
+
+
+def pro_mu_update(T, i, nu, mu, alpha, eps1):
+    """row of u_{i-1} (mu) -> row of u_i, given the row nu of v_i"""
+    T = np.asfortranarray(T, dtype=np.float64)
+    nu = _f64(nu)
+    out = np.zeros(max(len(mu), i + 1))
+    out[:len(mu)] = mu
+    lib().or_pro_mu_update(T.ctypes.data, T.shape[0], i, _p(nu), _p(out), alpha, eps1)
+    return out[:i + 1]

@@ -288,14 +288,17 @@ typedef struct {
     int32_t t;          /* subspace dimension; <= 0 -> max(15, 3k) (Alg. 2 step 1) */
     int32_t maxit;      /* r: maximum number of passes (Q5) */
     int32_t fixed_passes; /* >0: run exactly this many passes (parity hook, Q18) */
-    int32_t reorth;     /* 2 = CGS2 (default), 0 = off (test-only) */
+    int32_t reorth;     /* 2 = CGS2 (default), 1 = partial (PRO, reading Q20),
+                           0 = off (test-only) */
     uint64_t seed;      /* breakdown-vector stream seed */
+    double pro_delta;   /* PRO threshold; <= 0 -> sqrt(eps) (reading Q20) */
 } or_opts;
 
 typedef struct {
     int32_t passes, restarts, converged, t_used;
     int64_t steps, matvecs, breakdowns;
     double max_resid;
+    int64_t reorths;   /* Lanczos half-steps whose vector was re-orthogonalized */
 } or_info;
 
 typedef struct {
@@ -307,6 +310,9 @@ typedef struct {
     uint64_t bd_stream;
     or_info *info;
     double *h;         /* scratch for CGS2 */
+    /* PRO (reorth = 1): mu[l] ~ u_newest^T u_l, nu[l] ~ v_newest^T v_l */
+    double *mu, *nu, *tmp;
+    int force_u, force_v;
 } or_state;
 
 #define Tm(S, i, j) ((S)->T[(i) + (j) * ((S)->t + 1)]) /* 0-based */
@@ -341,6 +347,126 @@ static double finish_vector(or_state *S, int64_t N, int64_t ncols,
     return tval;
 }
 
+/* ------------------------------------------------------------------ */
+/* Partial re-orthogonalization (reorth = 1; reading  */
+/* Q20 of DESIGN.md).  The paper names this class -- PROPACK lansvd,   */
+/* "Lanczos bidiagonalization process with partial re-orthogonalization"*/
+/* -- without giving its rules; this is the omega        */
+/* recurrence of Simon (Lanczos) as extended by Larsen to the          */
+/* bidiagonalization, restated for the T of this algorithm (first pass:*/
+/* upper bidiagonal; after a restart: the arrow of Alg. 2 step 9).     */
+/*                                                                     */
+/* With 0-based columns, T holds the relations                         */
+/*   A v_l   = sum_{p<=l} T(p,l) u_p   (column l of T)                  */
+/*   A^T u_l = sum_{p>=l} T(l,p) v_p   (row l of T)                     */
+/* (Alg. 1 lines 5-8; Eqs. (5)-(7) after a restart).  If mu[p] are the   */
+/* inner products of u_{i-1} with u_p and nu[l] those of v_{i-1} with   */
+/* v_l, then v_i = (A^T u_{i-1} - alpha v_{i-1}) / beta has             */
+/*   beta * (v_i^T v_l) = sum_{p<=l} T(p,l) mu[p] - alpha * nu[l],      */
+/* and u_i = (A v_i - beta u_{i-1}) / alpha has                         */
+/*   alpha * (u_i^T u_l) = sum_{p>=l, p<=i} T(l,p) nu[p] - beta * mu[l] */
+/* with nu now the row of v_i.  Rounding enters as a term of size      */
+/* eps1 = eps * anorm with the sign of the sum (Simon's model), anorm  */
+/* the largest column 1-norm of T seen so far.                          */
+/* ------------------------------------------------------------------ */
+#define OR_EPS 2.220446049250313e-16 /* 2^-52 */
+
+/* largest column 1-norm of T(:, 0:ncols-1) */
+double or_pro_anorm(const double *T, int64_t ldt, int64_t ncols) {
+    double a = 0.0;
+    for (int64_t l = 0; l < ncols; l++) {
+        double c = 0.0;
+        for (int64_t p = 0; p <= l; p++) c += fabs(T[p + l * ldt]);
+        if (c > a) a = c;
+    }
+    return a;
+}
+
+/* nu (length i+1, in place): row of v_{i-1} -> row of v_i.  mu: row of
+ * u_{i-1}.  alpha = T(i-1,i-1); beta = ||A^T u_{i-1} - alpha v_{i-1}||. */
+void or_pro_nu_update(const double *T, int64_t ldt, int64_t i, const double *mu,
+                      double *nu, double beta, double eps1) {
+    double alpha = T[(i - 1) + (i - 1) * ldt];
+    for (int64_t l = 0; l < i; l++) {
+        double x = 0.0;
+        for (int64_t p = 0; p <= l; p++) x += T[p + l * ldt] * mu[p];
+        x -= alpha * nu[l];
+        x += (x < 0.0) ? -eps1 : eps1;
+        nu[l] = x / beta;
+    }
+    nu[i] = 1.0;
+}
+
+/* mu (length i+1, in place): row of u_{i-1} -> row of u_i.  nu: row of
+ * v_i (nu[i] = 1).  beta = T(i-1,i); alpha = ||A v_i - beta u_{i-1}||. */
+void or_pro_mu_update(const double *T, int64_t ldt, int64_t i, const double *nu,
+                      double *mu, double alpha, double eps1) {
+    double beta = T[(i - 1) + i * ldt];
+    for (int64_t l = 0; l < i; l++) {
+        double y = 0.0;
+        for (int64_t p = l; p <= i; p++) y += T[l + p * ldt] * nu[p];
+        y -= beta * mu[l];
+        y += (y < 0.0) ? -eps1 : eps1;
+        mu[l] = y / alpha;
+    }
+    mu[i] = 1.0;
+}
+
+/* The decision for the new vector x (length N, not yet normalized) whose
+ * estimate row `row` (length i+1) was just updated: re-orthogonalize if
+ * some |row[l]| exceeds delta, or if the previous vector of this side was
+ * re-orthogonalized because of its estimate (*force; Larsen: the next
+ * vector inherits the loss through the three-term relation).  A vector
+ * that is re-orthogonalized has its row reset to eps. */
+static int pro_decide(or_state *S, double *row, int64_t i, double nrm, int *force) {
+    double delta = S->o->pro_delta > 0.0 ? S->o->pro_delta : sqrt(OR_EPS);
+    int viol = !(nrm > 0.0);
+    for (int64_t l = 0; l < i; l++)
+        if (!(fabs(row[l]) <= delta)) viol = 1;
+    int reo = viol || *force;
+    *force = viol && !*force;
+    if (reo) {
+        for (int64_t l = 0; l < i; l++) row[l] = OR_EPS;
+        S->info->reorths++;
+    }
+    return reo;
+}
+
+/* V side of step i (computing v_i from w): returns 1 -> re-orthogonalize */
+static int pro_v(or_state *S, int64_t i, const double *w) {
+    int64_t n = S->A->n, ldt = S->t + 1;
+    double beta = or_norm2(n, w);
+    double eps1 = OR_EPS * or_pro_anorm(S->T, ldt, i);
+    or_pro_nu_update(S->T, ldt, i, S->mu, S->nu, beta, eps1);
+    return pro_decide(S, S->nu, i, beta, &S->force_v);
+}
+
+/* U side of step i (computing u_i from z) */
+static int pro_u(or_state *S, int64_t i, const double *z) {
+    int64_t m = S->A->m, ldt = S->t + 1;
+    double alpha = or_norm2(m, z);
+    double eps1 = OR_EPS * or_pro_anorm(S->T, ldt, i);
+    or_pro_mu_update(S->T, ldt, i, S->nu, S->mu, alpha, eps1);
+    return pro_decide(S, S->mu, i, alpha, &S->force_u);
+}
+
+/* After the restart (Alg. 2 steps 8-11): V(:,0:k-1) = V(:,0:t-1) Vh(:,0:k-1)
+ * and v_k = old v_t, so v_k^T v~_j = sum_l (v_t^T v_l) Vh(l,j); u_k was
+ * re-orthogonalized in full, so its row is eps. */
+static void pro_restart(or_state *S, int64_t k, const double *Vh) {
+    int64_t t = S->t;
+    for (int64_t j = 0; j < k; j++) {
+        double s = 0.0;
+        for (int64_t l = 0; l < t; l++) s += S->nu[l] * Vh[l + j * t];
+        S->tmp[j] = s;
+    }
+    for (int64_t j = 0; j < k; j++) S->nu[j] = S->tmp[j];
+    S->nu[k] = 1.0;
+    for (int64_t j = 0; j < k; j++) S->mu[j] = OR_EPS;
+    S->mu[k] = 1.0;
+    S->force_u = S->force_v = 0;
+}
+
 /* Alg. 1 loop body for i = i0..t (1-based), continuing from stored
  * U(:,1:i0), V(:,1:i0), T.  Computes v_{i+1}, beta_i, u_{i+1}, alpha_{i+1}.
  * The literal LBP(A, t+1) also forms u_{t+1} (Q2). */
@@ -353,8 +479,14 @@ static void lbp_steps(or_state *S, int64_t i0, double *w, double *z) {
         mat_mul_t(A, S->U + (i - 1) * m, w);
         S->info->matvecs++;
         for (int64_t r = 0; r < n; r++) w[r] -= alpha_i * S->V[r + (i - 1) * n];
-        /* full re-orthogonalization against V^{(i)} */
-        reorth(S, n, i, S->V, w);
+        /* full re-orthogonalization against V^{(i)}; reorth = 1:
+         * only when the omega estimate asks for it (reading Q20) */
+        if (S->o->reorth == 1) {
+            if (pro_v(S, i, w)) or_cgs2(n, i, S->V, n, w, S->h);
+        } else {
+            reorth(S, n, i, S->V, w);
+            if (S->o->reorth == 2) S->info->reorths++;
+        }
         /* line 6: beta_i = ||v_{i+1}||, v_{i+1} /= beta_i */
         double beta_i = finish_vector(S, n, i, S->V, w, S->V + i * n);
         Tm(S, i - 1, i) = beta_i;
@@ -362,7 +494,12 @@ static void lbp_steps(or_state *S, int64_t i0, double *w, double *z) {
         mat_mul(A, S->V + i * n, z);
         S->info->matvecs++;
         for (int64_t r = 0; r < m; r++) z[r] -= beta_i * S->U[r + (i - 1) * m];
-        reorth(S, m, i, S->U, z);
+        if (S->o->reorth == 1) {
+            if (pro_u(S, i, z)) or_cgs2(m, i, S->U, m, z, S->h);
+        } else {
+            reorth(S, m, i, S->U, z);
+            if (S->o->reorth == 2) S->info->reorths++;
+        }
         /* line 8: alpha_{i+1} = ||u_{i+1}||, u_{i+1} /= alpha_{i+1} */
         double alpha_ip1 = finish_vector(S, m, i, S->U, z, S->U + i * m);
         Tm(S, i, i) = alpha_ip1;
@@ -393,6 +530,9 @@ int or_svds(const or_matrix *A, const or_opts *o, const double *v0,
     S.V = (double *)calloc((size_t)(n * (t + 1)), sizeof(double));
     S.T = (double *)calloc((size_t)((t + 1) * (t + 1)), sizeof(double));
     S.h = (double *)calloc((size_t)(t + 2), sizeof(double));
+    S.mu = (double *)calloc((size_t)(t + 2), sizeof(double));
+    S.nu = (double *)calloc((size_t)(t + 2), sizeof(double));
+    S.tmp = (double *)calloc((size_t)(t + 2), sizeof(double));
     double *w = (double *)calloc((size_t)n, sizeof(double));
     double *z = (double *)calloc((size_t)m, sizeof(double));
     double *Tt = (double *)calloc((size_t)(t * t), sizeof(double));
@@ -403,8 +543,8 @@ int or_svds(const or_matrix *A, const or_opts *o, const double *v0,
     double *Vk = (double *)calloc((size_t)(n * k), sizeof(double));
     double *rho = (double *)calloc((size_t)k, sizeof(double));
     int status = OR_OK;
-    if (!S.U || !S.V || !S.T || !S.h || !w || !z || !Tt || !Uh || !Vh || !Sh ||
-        !Uk || !Vk || !rho) {
+    if (!S.U || !S.V || !S.T || !S.h || !S.mu || !S.nu || !S.tmp || !w || !z || !Tt ||
+        !Uh || !Vh || !Sh || !Uk || !Vk || !rho) {
         status = OR_ENOMEM;
         goto done;
     }
@@ -419,6 +559,8 @@ int or_svds(const or_matrix *A, const or_opts *o, const double *v0,
     mat_mul(A, S.V, z);
     info->matvecs++;
     Tm(&S, 0, 0) = finish_vector(&S, m, 0, S.U, z, S.U);
+    S.mu[0] = 1.0; /* PRO rows of u_0, v_0 */
+    S.nu[0] = 1.0;
 
     int64_t i0 = 1;
     int converged = 0;
@@ -488,6 +630,7 @@ int or_svds(const or_matrix *A, const or_opts *o, const double *v0,
         reorth(&S, m, k, S.U, z);
         /* step 11: alpha_{k+1} = ||u_{k+1}||, u_{k+1} /= alpha_{k+1} */
         Tm(&S, k, k) = finish_vector(&S, m, k, S.U, z, S.U + k * m);
+        if (o->reorth == 1) pro_restart(&S, k, Vh);
         info->restarts++;
         i0 = k + 1; /* step 12 */
     }
@@ -510,7 +653,8 @@ int or_svds(const or_matrix *A, const or_opts *o, const double *v0,
     if (status == OR_OK && !converged) status = OR_NOT_CONVERGED;
 
 done:
-    free(S.U); free(S.V); free(S.T); free(S.h); free(w); free(z); free(Tt);
+    free(S.U); free(S.V); free(S.T); free(S.h); free(S.mu); free(S.nu); free(S.tmp);
+    free(w); free(z); free(Tt);
     free(Uh); free(Vh); free(Sh); free(Uk); free(Vk); free(rho);
     return status;
 }
@@ -531,17 +675,24 @@ int or_lbp(const or_matrix *A, const or_opts *o, int64_t t, const double *v0,
     memset(V, 0, sizeof(double) * (size_t)(n * (t + 1)));
     memset(T, 0, sizeof(double) * (size_t)((t + 1) * (t + 1)));
     S.h = (double *)calloc((size_t)(t + 2), sizeof(double));
+    S.mu = (double *)calloc((size_t)(t + 2), sizeof(double));
+    S.nu = (double *)calloc((size_t)(t + 2), sizeof(double));
     double *w = (double *)calloc((size_t)n, sizeof(double));
     double *z = (double *)calloc((size_t)m, sizeof(double));
-    if (!S.h || !w || !z) { free(S.h); free(w); free(z); return OR_ENOMEM; }
+    if (!S.h || !S.mu || !S.nu || !w || !z) {
+        free(S.h); free(S.mu); free(S.nu); free(w); free(z);
+        return OR_ENOMEM;
+    }
     double nv = or_norm2(n, v0);
     for (int64_t r = 0; r < n; r++) V[r] = v0[r] / nv;
     mat_mul(A, V, z);
     info->matvecs++;
     Tm(&S, 0, 0) = finish_vector(&S, m, 0, U, z, U);
+    S.mu[0] = 1.0;
+    S.nu[0] = 1.0;
     lbp_steps(&S, 1, w, z);
     info->passes = 1;
     info->t_used = (int32_t)t;
-    free(S.h); free(w); free(z);
+    free(S.h); free(S.mu); free(S.nu); free(w); free(z);
     return OR_OK;
 }
