@@ -74,6 +74,9 @@ typedef struct {
     const double *v0;     /* device, length ncols (global), or NULL -> internal N(0,1)  */
     int32_t fixed_passes; /* > 0: run exactly this many passes (parity hook, Q18)        */
     int32_t reorth;       /* 2 = CGS2 (default when 0 is not requested: pass 2);         */
+                          /* 1 = partial: CGS2 only when the omega estimate of the loss  */
+                          /*     of orthogonality exceeds sqrt(eps) (Q20;      */
+                          /*     single GPU; PAPER.md:42 names the class);               */
                           /* 0 = off, test-only                            */
 } svdsc_opts;
 
@@ -86,6 +89,8 @@ typedef struct {
     double seconds_total; /* host wall time of svdsc_solve                                */
     int64_t launches;     /* kernels launched by the library during the solve            */
     int64_t bytes_model;  /* algorithmic HBM bytes of the Lanczos steps */
+                          /* (with reorth = 1: as if every half-step re-orthogonalized)  */
+    int64_t reorths;      /* Lanczos half-steps (A^T u or A v side) re-orthogonalized     */
 } svdsc_info;
 
 /* ---- handles --------------------------------------------------------------- */
@@ -176,7 +181,8 @@ SVDSC_API svdsc_status svdsc_op_lbp(svdsc_matrix *M, const svdsc_opts *o, int32_
  * the handle's stream and accumulates device milliseconds per family (read
  * after the solve).  Families: 0 A v products (a5), 1 A^T u products (a1),
  * 2 CGS sweep p1, 3 p2, 4 p3, 5 normalize, 6 small SVD (a7), 7 residuals,
- * 8 recombination (a8/a9), 9 restart misc, 10 collectives, 11 fused CGS2.
+ * 8 recombination (a8/a9), 9 restart misc, 10 collectives, 11 fused CGS2,
+ * 12 partial re-orthogonalization decisions (reorth = 1).
  * enable: 0 off, 1 every family, < 0 only the families of the bitmask -enable
  * (fewer event records inside a timed region).  enable resets the counters.
  * ms / calls: host arrays of 16 entries. */

@@ -125,6 +125,8 @@ struct Args {
     int wsmem;            // keep the CTA's w rows in shared memory
     unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
     PreReduce pre;        // pending split-K reduction of w (pre.partial != NULL)
+    const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
+    int gate_want;
 };
 
 // out[j] = sum_b partial[b][j] for the columns owned by this CTA
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     qstamp();
     grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the grid
+    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     unsigned int nbar = 0;
     extern __shared__ double sm[];
     __shared__ double sh[32];
@@ -462,6 +465,8 @@ struct SArgs {
     int64_t rpb;  // rows per CTA, multiple of RT
     unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
     int snake;    // stream2 sweep-direction policy (see k_cgs2_stream2)
+    const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
+    int gate_want;
 };
 
 template <int RT>
@@ -570,6 +575,7 @@ __global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
     constexpr int NQ = 1024 / kSThr;  // columns per thread (ncols <= 1024)
     grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
+    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     unsigned int nbar = 0;
     extern __shared__ __align__(16) double smem_s[];
     __shared__ double sh[32];
@@ -757,6 +763,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     constexpr int kSThr = 512, NW = 16, RPW = RT / NW, kCh = RT / 2;
     grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
+    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     unsigned int nbar = 0;
     extern __shared__ __align__(16) double smem_s[];
     __shared__ double sh[32];
@@ -1214,6 +1221,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
     if (a.tdbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
     grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
+    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     unsigned int nbar = 0;
     extern __shared__ __align__(128) double smem_raw[];
     __shared__ __align__(8) uint64_t full[kTmaMaxNS], empty[kTmaMaxNS];
@@ -1655,6 +1663,8 @@ struct CArgs {
     int rpb;  // rows per CTA
     unsigned int *flags;  // grid-barrier slots: this launch zeroes the next launch's slot
     unsigned int epoch;
+    const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
+    int gate_want;
 };
 
 __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
@@ -1662,6 +1672,7 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
     cgx::cluster_group cl = cgx::this_cluster();
     grid_prepare(a.flags, a.epoch);  // keep the barrier-slot chain of the fused launches intact
     if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the cluster
+    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NWc = kClThreads / 32;
     const int ncols = a.ncols, PS = ncols + 2;
@@ -1812,6 +1823,8 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     a.h3 = fs.h3;
     a.flags = fs.flags;
     a.epoch = fs.epoch;
+    a.gate = fs.gate;
+    a.gate_want = fs.gate_want;
     a.ctrl = ctrl;
     a.t_entry = t_entry;
     a.check = check;
@@ -1863,6 +1876,8 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             ca.rpb = (int)rpb;
             ca.flags = fs.flags;
             ca.epoch = fs.epoch;
+            ca.gate = fs.gate;
+            ca.gate_want = fs.gate_want;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(C);
             cfg.blockDim = dim3(kClThreads);
@@ -1931,6 +1946,8 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     sa.h3 = fs.h3;
     sa.flags = fs.flags;
     sa.epoch = fs.epoch;
+    sa.gate = fs.gate;
+    sa.gate_want = fs.gate_want;
     sa.ctrl = ctrl;
     sa.t_entry = t_entry;
     sa.check = check;

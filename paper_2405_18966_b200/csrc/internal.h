@@ -37,6 +37,10 @@ struct Ctrl {
     unsigned int gflags[kMaxBlocks];  // grid-barrier flags of the fused kernels
     unsigned int jprog[16];           // Jacobi rounds logged so far, per cluster CTA (replay role polls)
     unsigned int jdone;               // Jacobi finished: svd_sweeps final
+    // partial re-orthogonalization (reorth = 1, pro.cu)
+    int pro_gate;                     // 1: the current half-step re-orthogonalizes
+    int pro_force[2];                 // V / U side: next vector re-orthogonalized regardless
+    long long pro_reorths;            // half-steps re-orthogonalized so far
 };
 
 // ---- CSR operand (device) prepared by analysis --------------------------------
@@ -139,6 +143,11 @@ struct FusedScratch {
     unsigned int *flags;  // >= 2*nsm grid-barrier flags, zeroed once per solve
     unsigned int epoch;   // unique increasing base per launch (multiple of 16)
     const PreReduce *pre = nullptr;  // pending dense split-K reduction of w (or NULL)
+    // partial re-orthogonalization (reorth = 1): the launch does its work only
+    // if *gate == gate_want (device flag written by pro_decide); else every CTA
+    // returns right after preparing the next barrier slot
+    const int *gate = nullptr;
+    int gate_want = 1;
 };
 // false: the fused path is not applicable (caller uses cgs_p1/p2/p3 + normalize)
 // tmap: optional CUtensorMap (128 B) of Q for the TMA streaming variant
@@ -153,6 +162,15 @@ bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_
 
 
 void ktiming_dump();  // SVDSC_KTIMING=1 debugging aid
+
+// partial re-orthogonalization (pro.cu; Q20).  mu/nu: device rows of
+// length t+2; part: >= nsm doubles of scratch.  pro_decide writes
+// ctrl->pro_gate for the half-step (side 0: v_i from x, side 1: u_i from x);
+// kr is the arrow column of T (k after a restart, -1 in the first pass).
+void pro_init(int t, double *mu, double *nu, cudaStream_t s);
+void pro_decide(int side, int64_t N, const double *x, int i, int kr, const double *T, int ldt, double *mu,
+                double *nu, double *part, Ctrl *ctrl, int nsm, cudaStream_t s);
+void pro_restart(int t, int k, const double *Vh, int ldvh, double *mu, double *nu, Ctrl *ctrl, cudaStream_t s);
 
 // ---- small SVD / restart ---------------------------------------------------------
 // Jacobi SVD of the p x p matrix stored (ld p) in W; outputs Uh, Sh, Vh (ld p),

@@ -227,6 +227,7 @@ struct Ws {
     double *partial = nullptr, *h1 = nullptr, *h2 = nullptr, *nrm = nullptr, *rho = nullptr, *resid = nullptr;
     double *yfull = nullptr, *vfull = nullptr, *vtmp = nullptr;
     double *tlog = nullptr;
+    double *pro_mu = nullptr, *pro_nu = nullptr, *pro_part = nullptr;  // reorth = 1 (pro.cu)
     Ctrl *ctrl = nullptr;
     int64_t ldu = 0, ldv = 0, nv = 0, n_pad = 0;
     int ldt = 0;
@@ -267,6 +268,9 @@ size_t carve(Ws &w, void *base, int64_t m, int64_t n, int t, int k, int P) {
     w.rho = c.take<double>(k);
     w.resid = c.take<double>(k);
     w.tlog = c.take<double>(small_svd_log_doubles(t));
+    w.pro_mu = c.take<double>(t + 2);
+    w.pro_nu = c.take<double>(t + 2);
+    w.pro_part = c.take<double>(kMaxBlocks);
     if (P > 1) {
         w.yfull = c.take<double>(w.n_pad);
         w.vfull = c.take<double>(w.n_pad);
@@ -288,7 +292,7 @@ void check_opts(const svdsc_matrix *M, const svdsc_opts *o) {
     const int t = resolve_t(o, M->m_global, M->n);
     einval(t < o->k + 2, "subspace dimension t = min(max(15,3k), min(m,n)-1) < k+2 (SPEC.md:309)");
     einval(t > 1023, "t > 1023 is not supported");
-    einval(o->reorth != 0 && o->reorth != 2, "reorth must be 0 or 2");
+    einval(o->reorth < 0 || o->reorth > 2, "reorth must be 0, 1 or 2");
 }
 
 // ---------------------------------------------------------------------------
@@ -331,7 +335,7 @@ struct Solver {
     // kernel, which finishes the reduction while staging w (one launch less per
     // half-step); any other consumer calls finish_pending() first
     PreReduce pending;
-    bool defer_reduce() const { return M->kind == 1 && P == 1 && fused_ok && o->reorth != 0; }
+    bool defer_reduce() const { return M->kind == 1 && P == 1 && fused_ok && o->reorth == 2; }
     void finish_pending(int64_t N, double *wv) {
         if (pending.partial) {
             split_reduce(N, pending, wv, abort, s);
@@ -407,6 +411,30 @@ struct Solver {
         H->prof.end(s);
     }
 
+    // partial re-orthogonalization (reorth = 1, Q20): the decision
+    // kernel sets ctrl->pro_gate; the full CGS2 launch runs iff it is 1, the
+    // normalize-only launch (ncols = 0) iff it is 0
+    int pro_kr = -1;        // arrow column of T: k after the first restart
+    int64_t reorth_halves = 0;
+    void orth_norm_pro(int side, int i, int64_t N, const double *Q, int64_t ldq, double *wv, double *t_entry,
+                       int chk) {
+        einval(!fused_ok, "reorth = 1 needs the fused CGS2 kernels (SVDSC_NO_FUSED is set)");
+        finish_pending(N, wv);
+        H->prof.begin(12, s);
+        pro_decide(side, N, wv, i, pro_kr, w.T, w.ldt, w.pro_mu, w.pro_nu, w.pro_part, w.ctrl, nsm, s);
+        H->prof.end(s);
+        H->prof.begin(11, s);
+        const void *tm = have_tmap ? (Q == w.U ? (const void *)tmapU : (Q == w.V ? (const void *)tmapV : nullptr))
+                                   : nullptr;
+        for (int want = 1; want >= 0; want--) {
+            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches), nullptr,
+                            &w.ctrl->pro_gate, want};
+            if (!cgs2_fused(N, want ? i : 0, Q, ldq, wv, nullptr, fs, w.ctrl, t_entry, chk, nsm, s, tm))
+                throw SvdscError(SVDSC_EINVAL, "reorth = 1: fused CGS2 path not applicable");
+        }
+        H->prof.end(s);
+    }
+
     double *Ucol(int j) { return w.U + (int64_t)j * w.ldu; }
     double *Vcol(int j) { return w.V + (int64_t)j * w.ldv; }
     double *Tm(int i, int j) { return w.T + i + (int64_t)j * w.ldt; }
@@ -426,7 +454,12 @@ struct Solver {
             case 1: {  // Alg. 1 lines 5-6 + re-orthogonalization
                 const int i = h.i;
                 Atu(Ucol(i - 1), Vcol(i), Tm(i - 1, i - 1), Vcol(i - 1));
-                orth_norm(nv, i, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk, nullptr);
+                if (o->reorth == 1) {
+                    orth_norm_pro(0, i, nv, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk);
+                } else {
+                    orth_norm(nv, i, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk, nullptr);
+                    reorth_halves += o->reorth == 2;
+                }
                 steps++;
                 bytes_model += bytesA + 8 * nv * (3 * (int64_t)i + 5);
                 break;
@@ -434,7 +467,12 @@ struct Solver {
             case 2: {  // Alg. 1 lines 7-8 + re-orthogonalization
                 const int i = h.i;
                 Av(Vcol(i), Ucol(i), Tm(i - 1, i), Ucol(i - 1));
-                orth_norm(m, i, w.U, w.ldu, Ucol(i), Tm(i, i), chk, nullptr);
+                if (o->reorth == 1) {
+                    orth_norm_pro(1, i, m, w.U, w.ldu, Ucol(i), Tm(i, i), chk);
+                } else {
+                    orth_norm(m, i, w.U, w.ldu, Ucol(i), Tm(i, i), chk, nullptr);
+                    reorth_halves += o->reorth == 2;
+                }
                 bytes_model += bytesA + 8 * m * (3 * (int64_t)i + 5);
                 break;
             }
@@ -523,6 +561,7 @@ struct Solver {
         bytesA = M->kind == 0 ? 12 * M->nnz + 4 * (m + 1) : 8 * m * n;
         ck(cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s), "memset");
         ck(cudaMemsetAsync(w.T, 0, sizeof(double) * (t + 1) * (t + 1), s), "memset");
+        if (o->reorth == 1) pro_init(t, w.pro_mu, w.pro_nu, s);
         if (P > 1) {
             ck(cudaMemsetAsync(w.V, 0, sizeof(double) * w.ldv * (t + 1), s), "memset");
             ck(cudaMemsetAsync(w.yfull, 0, sizeof(double) * w.n_pad, s), "memset");
@@ -579,6 +618,10 @@ struct Solver {
                 H->prof.begin(9, s);
                 copy_col(nv, Vcol(t), Vcol(k), s);  // v_{k+1} = v_{t+1}
                 restart_T(t, k, w.T, w.ldt, w.Uh, w.Sh, w.rho, s);
+                if (o->reorth == 1) {
+                    pro_restart(t, k, w.Vh, t, w.pro_mu, w.pro_nu, w.ctrl, s);
+                    pro_kr = k;
+                }
                 H->prof.end(s);
                 matvecs += 0;
                 c0 += (int)plan.size();
@@ -617,6 +660,7 @@ struct Solver {
             info->breakdowns = breakdowns;
             info->max_resid = lbp_only ? 0.0 : c.max_resid;
             info->bytes_model = bytes_model;
+            info->reorths = o->reorth == 1 ? H->hctrl->pro_reorths : reorth_halves;
         }
         if (!lbp_only && !c.converged) return SVDSC_NOT_CONVERGED;
         return SVDSC_OK;
@@ -632,7 +676,8 @@ svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o, void *ws, size_t w
     auto t0 = std::chrono::steady_clock::now();
     svdsc_status st = guarded(H, [&] {
         if (!lbp_only) check_opts(M, o);
-        einval(o->reorth != 0 && o->reorth != 2, "reorth must be 0 or 2");
+        einval(o->reorth < 0 || o->reorth > 2, "reorth must be 0, 1 or 2");
+        einval(o->reorth == 1 && M->h->comm, "reorth = 1 (partial) is single-GPU only");
         Solver sv{};
         sv.M = M;
         sv.H = H;

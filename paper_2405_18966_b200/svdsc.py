@@ -44,7 +44,7 @@ class Info(ctypes.Structure):
                 ("steps", ctypes.c_int64), ("matvecs", ctypes.c_int64),
                 ("breakdowns", ctypes.c_int64), ("max_resid", ctypes.c_double),
                 ("seconds_total", ctypes.c_double), ("launches", ctypes.c_int64),
-                ("bytes_model", ctypes.c_int64)]
+                ("bytes_model", ctypes.c_int64), ("reorths", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -69,7 +69,7 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
            "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows",
            "svdsc_profile_enable", "svdsc_profile_read"]
 PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",
-                 "recombine", "restart_misc", "collectives", "cgs2_fused"]
+                 "recombine", "restart_misc", "collectives", "cgs2_fused", "pro_decide"]
 
 
 def lib():

@@ -330,7 +330,7 @@ def test_svds_forced_restarts_and_breakdown(S, H):
 def test_svds_contract_errors(S, H):
     wl = W.config(1, scale=10)
     M = S.Matrix.from_host(H, wl.A)
-    for kw in (dict(k=0), dict(k=5, tol=0.0), dict(k=298), dict(k=5, reorth=1)):
+    for kw in (dict(k=0), dict(k=5, tol=0.0), dict(k=298), dict(k=5, reorth=3)):
         with pytest.raises(S.SvdscError) as e:
             S.svds_c(M, **kw)
         assert e.value.status == -1
