@@ -119,6 +119,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--reorth", type=int, default=2, choices=[1, 2],
+                    help="2: full CGS2 every half-step (the paper's method, the headline); "
+                         "1: partial re-orthogonalization (DESIGN.md Q20, SURVEY 8(f4)), an extra line")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -200,7 +203,7 @@ def main():
     ws = torch.empty(S.workspace_size(M, k, t=t), dtype=torch.uint8, device=dev)
 
     def solve():
-        return S.svds_c(M, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0, workspace=ws)
+        return S.svds_c(M, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0, workspace=ws, reorth=args.reorth)
 
     for _ in range(args.warmup):
         solve()
@@ -213,7 +216,9 @@ def main():
     torch.cuda.synchronize()
     prof_all = H.profile_read()
     H.profile(False)
-    fam = max(("Av", "ATu", "cgs2_fused"), key=lambda f: prof_all[f][0])
+    # (reorth = 1: the CGS2 byte model assumes every half-step re-orthogonalizes,
+    # so the roofline line is taken on the products)
+    fam = max(("Av", "ATu", "cgs2_fused") if args.reorth == 2 else ("Av", "ATu"), key=lambda f: prof_all[f][0])
 
     # ---- timed region ----
     clocks = ClockSampler(local_rank)
@@ -225,13 +230,14 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    steps_total, launches, passes, res, bytes_model = 0, 0, [], None, 0
+    steps_total, launches, passes, res, bytes_model, reorths = 0, 0, [], None, 0, 0
     for _ in range(args.steps):
         res = solve()
         steps_total += res.info["steps"]
         launches += res.info["launches"]
         passes.append(res.info["passes"])
         bytes_model += res.info["bytes_model"]
+        reorths += res.info["reorths"]
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -290,12 +296,12 @@ def main():
             h2d = 8 * (Al.m + 1) + 12 * Al.nnz + 8 * Al.n
         d2h = 8 * (k + Al.m * k + Al.n * k + k)
         v0h = torch.from_numpy(wl_full.v0).pin_memory().numpy()
-        S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h)  # warm
+        S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h, reorth=args.reorth)  # warm
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            out = S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h)
+            out = S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h, reorth=args.reorth)
             e1.record(stream)
             torch.cuda.synchronize()
             e2e_ms += e0.elapsed_time(e1)
@@ -324,7 +330,11 @@ def main():
                        "l2": f"inputs larger than L2 (A = {A.bytes_one_pass() >> 20} MB per pass)",
                        "parallelism": f"rows{world}" if world > 1 else "single",
                        "step_hbm_gb_per_s": step_bytes * (steps_total / (ms / 1e3)) / 1e9,
-                       "step_bytes_model": step_bytes},
+                       "step_bytes_model": step_bytes,
+                       "reorth": ("full CGS2 every half-step (PAPER.md:121)" if args.reorth == 2 else
+                                  "partial (omega recurrence, DESIGN.md Q20; not the paper's method; "
+                                  "step_bytes_model still counts every half-step's CGS2)"),
+                       "reorth_half_steps_per_solve": reorths // args.steps},
             "roofline": {"bound": "hbm",
                          "kernel": ("fused CGS2 re-orthogonalization (3 sweeps of U_i / V_i)" if fam == "cgs2_fused"
                                     else f"{fam} product ({'gemv' if A.kind == 'dense' else 'spmv'})"),

@@ -92,8 +92,16 @@ __global__ void __launch_bounds__(kDecThreads) k_pro_decide(int side, int i, int
     if (*(volatile const int *)&ctrl->abort) return;
     __shared__ double sh[32];
     __shared__ int sviol;
+    extern __shared__ double sarrow[];  // the arrow column T(0:kr, kr) and mu(0:kr), staged in parallel
     const int tid = threadIdx.x;
     auto Tm = [&](int p, int l) { return T[p + (int64_t)l * ldt]; };
+    if (kr >= 0) {
+        for (int p = tid; p <= kr; p += kDecThreads) {
+            sarrow[p] = Tm(p, kr);
+            sarrow[kr + 1 + p] = mu[p];
+        }
+        __syncthreads();
+    }
     // ||x||: the partials in a fixed order
     double ps = 0.0;
     for (int b = tid; b < nparts; b += kDecThreads) ps += part[b];
@@ -104,7 +112,7 @@ __global__ void __launch_bounds__(kDecThreads) k_pro_decide(int side, int i, int
         double c;
         if (kr >= 0 && l == kr) {
             c = 0.0;
-            for (int p = 0; p <= kr; p++) c = __dadd_rn(c, fabs(Tm(p, l)));
+            for (int p = 0; p <= kr; p++) c = __dadd_rn(c, fabs(sarrow[p]));
         } else if (kr >= 0 && l < kr) {
             c = fabs(Tm(l, l));
         } else {
@@ -120,7 +128,7 @@ __global__ void __launch_bounds__(kDecThreads) k_pro_decide(int side, int i, int
         for (int l = tid; l < i; l += kDecThreads) {
             double x = 0.0;  // column l of T against mu
             if (kr >= 0 && l == kr) {
-                for (int p = 0; p <= kr; p++) x = tsum_ordered(x, Tm(p, l), mu[p]);
+                for (int p = 0; p <= kr; p++) x = tsum_ordered(x, sarrow[p], sarrow[kr + 1 + p]);
             } else if (kr >= 0 && l < kr) {
                 x = tsum_ordered(x, Tm(l, l), mu[l]);
             } else {
@@ -211,7 +219,8 @@ void pro_decide(int side, int64_t N, const double *x, int i, int kr, const doubl
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (N + 255) / 256));
     k_pro_partial<<<nb, 256, 0, s>>>(N, x, part, &ctrl->abort);
     count_launch();
-    k_pro_decide<<<1, kDecThreads, 0, s>>>(side, i, kr, T, ldt, part, nb, mu, nu, ctrl);
+    const size_t smem = kr >= 0 ? 2 * (size_t)(kr + 1) * sizeof(double) : 0;
+    k_pro_decide<<<1, kDecThreads, smem, s>>>(side, i, kr, T, ldt, part, nb, mu, nu, ctrl);
     count_launch();
 }
 
