@@ -68,6 +68,16 @@ struct CsrOp {
     int64_t n_span = 0;                // rows spanning tile boundaries
     int32_t *span_row = nullptr, *span_t0 = nullptr, *span_t1 = nullptr;  // row, first and last tile
     bool merge = false;                // use the merge schedule for this operand
+    // column-blocked copy (matvec.cu, "cb"): columns split into cb_nb blocks of
+    // kCbW; segment s = b * nrows + r holds row r's entries of block b, in row
+    // order, with 16-bit block-local column indices; x's block is staged in
+    // shared memory, so the gathers never leave the SM
+    int cb_nb = 0, cb_tasks = 0, cb_G = 0;
+    int32_t *cb_ptr = nullptr;         // cb_nb * nrows + 1 segment offsets
+    uint16_t *cb_col = nullptr;        // nnz
+    double *cb_val = nullptr;          // nnz
+    int32_t *cb_tb = nullptr;          // cb_tasks + 1 segment boundaries, one task per CTA
+    double *cb_part = nullptr;         // cb_nb * nrows partial row sums (cb_nb > 1)
     std::vector<void *> owned;         // allocations owned by this operand
 };
 constexpr int kMergeTile = 2048;       // nonzeros per merge tile (256 threads x 8)

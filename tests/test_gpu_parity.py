@@ -76,10 +76,13 @@ def check_products(S, H, A, seed=0):
 
 
 # ---------------------------------------------------------------- a1 / a5
-@pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
-@pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000), (4, 10)])
+@pytest.mark.parametrize("sched", ["auto", "merge", "bins", "cb"])
+@pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000), (4, 10), (3, 2)])
 def test_products_configs(S, H, cid, scale, sched, monkeypatch):
-    """Both SpMV schedules (row-binned and nnz-balanced merge) on every config."""
+    """Every SpMV schedule on every config: "auto" = the merge schedule on
+    power-law operands, else the row bins; "cb" = the opt-in column-blocked
+    kernel where it applies (configs 1, 3: x reused, <= 16 blocks of 24,576
+    columns; config 3 at 1/2 scale has 3 blocks for A v and 5 for A^T u)."""
     if sched != "auto":
         monkeypatch.setenv("SVDSC_SPMV", sched)
     wl = W.config(cid, scale=scale)
@@ -122,6 +125,26 @@ def test_products_edge_cases(S, H, sched, monkeypatch):
     Aa = W.Matrix("csr", m2, n2, row_ptr=rp2, col_idx=col2, values=np.abs(A2.values))
     bud = 2 * gamma(np.bincount(col2, minlength=n2) + 2) * O.spmv_t(Aa, np.abs(u))
     assert np.all(np.abs(yt - O.spmv_t(A2, u)) <= bud + 1e-300)
+
+
+@pytest.mark.parametrize("ncols", [24576, 24577, 49153, 3 * 24576 + 17])
+def test_products_column_blocked_ragged(S, H, ncols, monkeypatch):
+    """Column-blocked SpMV: block edges (a last block of 1 or 17 columns), empty
+    rows, rows with all entries in one block, duplicates, 4..60 nnz per row."""
+    monkeypatch.setenv("SVDSC_SPMV", "cb")
+    rng = np.random.default_rng(ncols)
+    m = 24001
+    lens = rng.integers(4, 60, m)
+    lens[::13] = 0
+    lens[-2:] = 0
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = rng.integers(0, ncols, rp[-1]).astype(np.int32)
+    col[rp[7]:rp[8]] = ncols - 1  # a row living in the last (ragged) block
+    val = rng.standard_normal(rp[-1])
+    A = W.Matrix("csr", m, ncols, row_ptr=rp, col_idx=col, values=val)
+    assert A.nnz >= 8 * ncols  # eligible: x is reused
+    check_products(S, H, A)
 
 
 @pytest.mark.parametrize("m,n", [(5000, 1250), (1001, 333), (20000, 5000)])
