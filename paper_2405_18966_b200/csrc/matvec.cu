@@ -881,7 +881,10 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
                 for (int q = 0; q <= nb; q++)
                     check(cudaMemcpy(&bp[q], op.cb_ptr + (int64_t)q * op.nrows, sizeof(int32_t),
                                      cudaMemcpyDeviceToHost), "D2H");
-                const int T = std::max(nsm, nb);
+#ifndef SVDSC_CB_CPS
+#define SVDSC_CB_CPS 1
+#endif
+                const int T = std::max(nsm * SVDSC_CB_CPS, nb);  // CTAs per SM (1024 threads: 1)
                 std::vector<int32_t> tb(nb + 1);
                 tb[0] = 0;
                 for (int q = 0; q < nb; q++) {
