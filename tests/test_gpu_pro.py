@@ -111,3 +111,27 @@ def test_pro_contract(S, H):
     with pytest.raises(Exception):
         S.svds_c(M, 5, reorth=3)
     M.close()
+
+
+def test_pro_forced_restarts_and_breakdown(S, H):
+    """reorth = 1 through restarts (t = k + 3) and through breakdown repairs
+    (exactly rank-3 matrix, k = 5): the decision kernels are no-ops while a
+    breakdown abort is pending and the replayed half-steps decide again."""
+    A = W.dense_with_spectrum(500, 400, W.spectrum("decay1", 400), seed=5)
+    v0 = W.start_vector(400, 5)
+    r_or = O.svds(A, 10, v0, tol=1e-10, t=13, maxit=500, reorth=1)
+    M = S.Matrix.from_host(H, A)
+    r = S.svds_c(M, 10, tol=1e-10, t=13, maxit=500, v0=dev(v0), fixed_passes=r_or.passes, reorth=1)
+    assert r.info["restarts"] >= 1
+    assert np.abs(r.S.cpu().numpy() - r_or.S).max() <= 1e-10 * r_or.S[0]
+    M.close()
+    rng = np.random.default_rng(3)
+    D = rng.standard_normal((60, 3)) @ rng.standard_normal((3, 40))
+    A2 = W.dense_matrix(D)
+    v2 = rng.standard_normal(40)
+    r_or = O.svds(A2, 5, v2, t=15, maxit=20, reorth=1)
+    M = S.Matrix.from_host(H, A2)
+    r = S.svds_c(M, 5, t=15, maxit=20, v0=dev(v2), fixed_passes=r_or.passes, reorth=1)
+    assert r_or.breakdowns >= 1 and r.info["breakdowns"] >= 1
+    assert np.abs(r.S.cpu().numpy()[:3] - r_or.S[:3]).max() <= 1e-10 * r_or.S[0]
+    M.close()
