@@ -959,7 +959,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         // phase B: w' = w - Q h1 (written back), partial h2, ||w'||^2
 #pragma unroll
         for (int m = 0; m < M; m++) acc[m] = 0.0;
-        if constexpr (RPW * M > 24 || M > 16) {  // wide bases: registers hold acc + hreg only
+        if constexpr (RPW * M > 20 || M > 16) {  // wide bases: registers hold acc + hreg only
             run_tiles([&](int k, const double *T, const double *W) {
                 double part[RPW];
                 rowdots(T, hreg, part);
