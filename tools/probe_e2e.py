@@ -24,6 +24,17 @@ def main():
                   col_idx=torch.from_numpy(A.col_idx).pin_memory().numpy(),
                   values=torch.from_numpy(A.values).pin_memory().numpy())
     v0 = torch.from_numpy(wl.v0).pin_memory().numpy()
+    if os.environ.get("PROBE_DEVICE_FIRST"):  # the bench's order: device-buffer solves first
+        M0 = S.Matrix.from_host(H, A)
+        ws = torch.empty(S.workspace_size(M0, wl.k, t=wl.t), dtype=torch.uint8, device="cuda")
+        x0 = torch.from_numpy(wl.v0).cuda()
+        H.profile(True)
+        S.svds_c(M0, wl.k, tol=wl.tol, maxit=wl.maxit, t=wl.t, v0=x0, workspace=ws)
+        H.profile(True, families=("cgs2_fused",))
+        for _ in range(int(os.environ["PROBE_DEVICE_FIRST"])):
+            S.svds_c(M0, wl.k, tol=wl.tol, maxit=wl.maxit, t=wl.t, v0=x0, workspace=ws)
+        torch.cuda.synchronize()
+        H.profile(False)
     for _ in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
