@@ -35,8 +35,8 @@ struct Ctrl {
     double svd_tiny;      // p eps ||T||_F: numerically zero column norm (reading Q10b)
     unsigned int cnt[16]; // last-block counters (one per reduction site)
     unsigned int gflags[kMaxBlocks];  // grid-barrier flags of the fused kernels
-    unsigned int jprog[16];           // Jacobi rounds logged so far, per cluster CTA (replay role polls)
-    unsigned int jdone;               // Jacobi finished: svd_sweeps final
+
+
     // partial re-orthogonalization (reorth = 1, pro.cu)
     int pro_gate;                     // 1: the current half-step re-orthogonalizes
     int pro_force[2];                 // V / U side: next vector re-orthogonalized regardless

@@ -59,17 +59,6 @@ __global__ void __launch_bounds__(1024) k_copy_T(int p, const double *__restrict
         for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += sh[i];
         ctrl->svd_tiny = (double)p * 2.220446049250313e-16 * sqrt(tot);
     }
-    if (threadIdx.x < 16) ctrl->jprog[threadIdx.x] = 0u;
-    if (threadIdx.x == 16) ctrl->jdone = 0u;
-}
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // round-robin (circle method) pairing: round rnd in [0, pe-1), slot q in [0, pe/2)
@@ -209,13 +198,6 @@ __device__ __forceinline__ double jacobi_tan(double al, double be, double gam) {
 // half-blocks meets once per block sweep.  Every rotation is logged as
 // (t = tan theta, a, b) for k_apply_log; rotations of one local round (all
 // CTAs) touch disjoint columns, so replaying them round by round is exact.
-// debugging aid (SVDSC_KTIMING=1 builds with kJacobiTiming): cross-round section cycles of CTA 0, warp 0
-#ifndef SVDSC_JACOBI_TIMING
-#define SVDSC_JACOBI_TIMING 0
-#endif
-constexpr bool kJacobiTiming = SVDSC_JACOBI_TIMING != 0;  // build with -DSVDSC_JACOBI_TIMING=1 to enable
-__device__ unsigned long long g_jt[8];
-
 struct RotLog {
     double c, s;      // the rotation as applied to W (c = s = 0: no rotation)
     int32_t a, b;     // global column pair, a < b
@@ -289,106 +271,14 @@ constexpr int kJThreads = 640; // 20 warps: one warp per pair, <= 20 pairs per C
 constexpr int kJMaxH = 12;     // preferred half-block width (measured, tools/time_ops.py)
 constexpr int kMaxPairs = kJThreads / 32;
 
-// Replay role of the combined Jacobi launch: replay CTA j owns rows
-// [j R, j R + R) of V (thread (q, i) applies rotation q of a round to row i, as
-// k_apply_log), reading log rounds as soon as every Jacobi CTA has published
-// them (ld.acquire on Ctrl::jprog), and the final round count once jdone is set.
-__device__ void jacobi_replay_role(int p, int per_round, int64_t rps, const RotLog *__restrict__ rlog, Ctrl *ctrl,
-                                   double *V, int R, int lrc, int j, int C) {
-    extern __shared__ __align__(16) double Wsm[];
-    double *rows = Wsm;                                                        // R x p
-    RotLog *buf = reinterpret_cast<RotLog *>(rows + (((int64_t)R * p + 1) & ~1));  // lrc x per_round
-    __shared__ long long s_avail;
-    const int r0 = j * R;
-    if (r0 >= p) return;
-    for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
-        const int i = idx / p, c = idx % p;
-        rows[idx] = (r0 + i == c) ? 1.0 : 0.0;
-    }
-    const int q = threadIdx.x % per_round, i = threadIdx.x / per_round;
-    const bool act = i < R && r0 + i < p;
-    double *row = rows + i * p;
-    int64_t base = 0;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            long long avail;
-            for (;;) {
-                if (ld_acquire_u32(&ctrl->jdone)) {
-                    avail = -1 - (long long)(*(volatile int *)&ctrl->svd_sweeps) * rps;  // encoded: done
-                    break;
-                }
-                unsigned mn = 0xffffffffu;
-                for (int c = 0; c < C; c++) mn = min(mn, ld_acquire_u32(&ctrl->jprog[c]));
-                if ((int64_t)mn >= base + lrc) {
-                    avail = mn;
-                    break;
-                }
-                __nanosleep(200);
-            }
-            s_avail = avail;
-        }
-        __syncthreads();
-        const long long av = s_avail;
-        __syncthreads();
-        const bool done = av < 0;
-        const int64_t upto = done ? (-1 - av) : av;
-        if (base >= upto) {
-            if (done) break;
-            continue;
-        }
-        const int nr = (int)min((int64_t)lrc, upto - base);
-        const int n16 = nr * per_round * 2;
-        const char *src = reinterpret_cast<const char *>(rlog + base * per_round);
-        for (int t = threadIdx.x; t < n16; t += blockDim.x) {
-            const unsigned saddr = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char *>(buf) + 16 * t);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + 16 * t));
-        }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        for (int k = 0; k < nr; k++) {
-            if (act) {
-                const RotLog &e = buf[k * per_round + q];
-                const double c = e.c, s = e.s;
-                if (c != 0.0) {
-                    const double x = row[e.a], y = row[e.b];
-                    row[e.a] = c * x - s * y;
-                    row[e.b] = s * x + c * y;
-                }
-            }
-            __syncthreads();
-        }
-        base += nr;
-    }
-    for (int idx = threadIdx.x; idx < R * p; idx += blockDim.x) {
-        const int ii = idx / p, c = idx % p;
-        if (r0 + ii < p) V[(r0 + ii) + (int64_t)c * p] = rows[idx];
-    }
-}
-
 template <bool CL, int kRPL>
 __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const double *__restrict__ W0, double *Wout,
                                                        RotLog *rlog, int max_sweeps, Ctrl *ctrl, const int *abort,
-                                                       double ctol, int use_bulk, double *Vrep, int rep_R, int rep_lrc) {
+                                                       double ctol, int use_bulk) {
     if (aborted(abort)) return;
     cg::cluster_group cl = cg::this_cluster();
     const int C = CL ? (int)cl.num_blocks() : 1;
     const int me = CL ? (int)cl.block_rank() : 0;
-    if (CL && rep_R > 0 && (int)blockIdx.x >= C) {
-        // replay role (clusters 1..): V rows from the rotation log, following the
-        // Jacobi cluster round by round (co-residency: cooperative launch)
-        jacobi_replay_role(p, C * h, jacobi_rounds_per_sweep(C, h), rlog, ctrl, Vrep, rep_R, rep_lrc,
-                           (int)blockIdx.x - C, C);
-        return;
-    }
-    // publish "rounds logged" for the replay role (after the round's barrier)
-    // (every 8 rounds and at block-round ends: the fence is on the round's
-    // critical path)
-    auto publish = [&](int64_t rounds_done, bool force = false) {
-        if (rep_R > 0 && threadIdx.x == 0 && (force || (rounds_done & 7) == 0)) {
-            __threadfence();
-            st_release_u32(&ctrl->jprog[me], (unsigned)rounds_done);
-        }
-    };
     extern __shared__ __align__(16) double Wsm[];  // slot s, local column i: Wl + (s*h + i)*p
     // bulk-copy exchange: two half-block buffer sets, Wl = the current one
     // (push model: every CTA sends its two half-blocks to their next owners
@@ -488,7 +378,6 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                     }
                 }
                 __syncthreads();
-                publish((int64_t)(sweep - 1) * rps + lr + 1, lr + 1 == lrounds);
             }
             } else {
             // block rounds >= 1: only the h^2 cross pairs of the two half-blocks
@@ -507,9 +396,6 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
             const int64_t rbase = (int64_t)(sweep - 1) * rps + lrounds + (int64_t)(br - 1) * h;
             int jy = wid < h ? wid : 0;  // (wid + rr) mod h, advanced without a division
             for (int rr = 0; rr < h; rr++, jy = (jy + 1 == h) ? 0 : jy + 1) {
-                long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-                const bool prof = kJacobiTiming && me == 0 && threadIdx.x == 0;
-                if (prof) c0 = clock64();
                 if (has) {
                     const int j = h + jy;
                     const int gy = gcol[j];
@@ -522,11 +408,9 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                         yr[u] = (live && r < p) ? py[r] : 0.0;
                     }
                     const bool xlow = gx < gy;
-                    if (prof) c1 = clock64() + (long long)(yr[0] * 0.0);
                     double al, be, gam;
                     if (xlow) pair_sums<kRPL>(xr, yr, al, be, gam);
                     else pair_sums<kRPL>(yr, xr, al, be, gam);
-                    if (prof) c2 = clock64() + (long long)(gam * 0.0);
                     double c = 0.0, s = 0.0;
                     if (live && al > tiny2 && be > tiny2 && gam * gam > ctol2 * (al * be)) {
                         rot_cs(jacobi_tan(al, be, gam), c, s);
@@ -553,17 +437,7 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                         rlog[(rbase + rr) * per_round + (int64_t)me * h + wid] = e;
                     }
                 }
-                if (prof) c3 = clock64();
                 __syncthreads();
-                publish(rbase + rr + 1, rr + 1 == h);
-                if (prof) {
-                    const long long c4 = clock64();
-                    atomicAdd(&g_jt[0], (unsigned long long)(c1 - c0));
-                    atomicAdd(&g_jt[1], (unsigned long long)(c2 - c1));
-                    atomicAdd(&g_jt[2], (unsigned long long)(c3 - c2));
-                    atomicAdd(&g_jt[3], (unsigned long long)(c4 - c3));
-                    atomicAdd(&g_jt[4], 1ull);
-                }
             }
             if (has) {
 #pragma unroll
@@ -575,17 +449,18 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
             __syncthreads();
             }
             if (CL && m > 1 && bulk) {
-                const long long x0 = (kJacobiTiming && me == 0 && threadIdx.x == 0) ? clock64() : 0;
                 const int rn = (br + 1) % m;
                 const int n = h * p;
                 double *Wn = (Wl == Wsm) ? Wsm + 2 * n : Wsm;  // the other buffer set
                 const unsigned bar = (unsigned)__cvta_generic_to_shared(&xbar);
+                // every thread's generic-proxy writes of its half-block columns are
+                // ordered before the async-proxy (bulk copy) reads that follow
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (threadIdx.x == 0) {
                     // two incoming half-blocks; armed before the cluster barrier
                     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                                  "r"((unsigned)(2 * n * 8))
                                  : "memory");
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk reads
                 }
                 cl.sync();  // block round done everywhere; every CTA's barrier is armed
                 if (threadIdx.x < 2) {
@@ -615,13 +490,8 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                 hb[1] = hb_at(C, rn, me, 1);
                 for (int lc = threadIdx.x; lc < H2; lc += blockDim.x) gcol[lc] = hb[lc / h] * h + (lc % h);
                 __syncthreads();
-                if (kJacobiTiming && me == 0 && threadIdx.x == 0) {
-                    atomicAdd(&g_jt[5], (unsigned long long)(clock64() - x0));
-                    atomicAdd(&g_jt[6], 1ull);
-                }
             } else if (CL && m > 1) {
                 // move to round br+1 (after the last block round the circle is back at round 0)
-                const long long x0 = (kJacobiTiming && me == 0 && threadIdx.x == 0) ? clock64() : 0;
                 const int rn = (br + 1) % m;
                 if (threadIdx.x < 2) {
                     int ct, sl;
@@ -654,12 +524,11 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
                 hb[1] = hb_at(C, rn, me, 1);
                 for (int lc = threadIdx.x; lc < H2; lc += blockDim.x) gcol[lc] = hb[lc / h] * h + (lc % h);
                 __syncthreads();
-                if (kJacobiTiming && me == 0 && threadIdx.x == 0) {
-                    atomicAdd(&g_jt[5], (unsigned long long)(clock64() - x0));
-                    atomicAdd(&g_jt[6], 1ull);
-                }
             }
         }
+        // the next sweep's flag is cleared before the barrier: after it, other
+        // warps may already be setting it in the next sweep
+        if (threadIdx.x == 0) rot_flag[(sweep + 1) & 1] = 0;
         if (CL) cl.sync(); else __syncthreads();
         int any = 0;
         if (CL) {
@@ -668,7 +537,6 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
             any = *flag;
         }
         if (CL) cl.sync(); else __syncthreads();
-        if (threadIdx.x == 0) rot_flag[(sweep + 1) & 1] = 0;
         if (!any) {
             conv = true;
             break;
@@ -682,10 +550,6 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
     if (me == 0 && threadIdx.x == 0) {
         ctrl->svd_sweeps = conv ? sweep : max_sweeps;
         ctrl->svd_status = conv ? 0 : (int)SVDSC_ESVD_NOCONV;
-        if (rep_R > 0) {
-            __threadfence();
-            st_release_u32(&ctrl->jdone, 1u);
-        }
     }
     if (CL) cl.sync();
 }
@@ -1076,8 +940,7 @@ void jacobi_geometry(int p, int &C, int &h) {
     // at least h <= kJMaxH columns per half-block (SVDSC_JACOBI_H overrides).
     const int pe = p + (p & 1);
     int hmax = kJThreads / 32;
-    if (const char *e = getenv("SVDSC_JACOBI_H")) hmax = std::max(1, std::min(hmax, atoi(e)));
-    else hmax = std::min(hmax, kJMaxH);
+    hmax = std::min(hmax, kJMaxH);
     for (C = 1; C <= 16; C <<= 1) {
         h = (pe + 2 * C - 1) / (2 * C);
         if (h <= hmax && (size_t)2 * h * p * 8 <= 210 * 1024 && h * p <= kExR * kJThreads &&
@@ -1096,19 +959,16 @@ void jacobi_geometry(int p, int &C, int &h) {
 }
 }  // namespace
 
-// *replayed: set when the V replay ran inside the same (cooperative) launch
 template <int R>
 cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *rlog, Ctrl *ctrl, const int *abort,
-                          double ctol, cudaStream_t s, double *Vw, bool *replayed) {
-    *replayed = false;
+                          double ctol, cudaStream_t s) {
     if (C == 1) {
         cudaFuncSetAttribute(k_jacobi_block<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol, 0, nullptr, 0, 0);
+        k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol, 0);
         return cudaGetLastError();
     }
-    // bulk-copy exchange needs the second buffer set (SVDSC_JACOBI_PULL=1: register pull)
-    const char *pe = getenv("SVDSC_JACOBI_PULL");
-    const int use_bulk = (2 * smem <= 210 * 1024 && !(pe && pe[0] == '1')) ? 1 : 0;
+    // bulk-copy exchange when the second buffer set fits, else a register pull
+    const int use_bulk = (2 * smem <= 210 * 1024) ? 1 : 0;
     if (use_bulk) smem *= 2;
     cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (C > 8) cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1124,38 +984,12 @@ cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *r
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    // combined launch: clusters 1.. replay V from the log while cluster 0 runs the
-    // sweeps (cooperative: every CTA co-resident, else the launch fails and the
-    // replay runs afterwards as k_apply_log; SVDSC_JACOBI_SEPARATE=1 forces that)
-    const char *sep = getenv("SVDSC_JACOBI_SEPARATE");
-    if (!(sep && sep[0] == '1')) {
-        const int per_round = C * h;
-        const int RR = std::max(1, kJThreads / per_round);
-        const int nrep = (p + RR - 1) / RR;
-        const size_t rows_b = ((size_t)RR * p + 2) * 8;
-        const int lrc = (int)std::min<size_t>(16, (200 * 1024 - std::min<size_t>(rows_b, 200 * 1024)) /
-                                                       ((size_t)per_round * sizeof(RotLog)));
-        const int nclus = 1 + (nrep + C - 1) / C;
-        if (lrc >= 1 && rows_b + (size_t)lrc * per_round * sizeof(RotLog) <= 210 * 1024) {
-            cudaLaunchConfig_t c2 = cfg;
-            c2.gridDim = dim3(C * nclus);
-            c2.dynamicSmemBytes = std::max(smem, rows_b + (size_t)lrc * per_round * sizeof(RotLog));
-            cudaLaunchAttribute at2[2];
-            at2[0] = attr[0];
-            at2[1].id = cudaLaunchAttributeCooperative;
-            at2[1].val.cooperative = 1;
-            c2.attrs = at2;
-            c2.numAttrs = 2;
-            if (cudaLaunchKernelEx(&c2, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort,
-                                   ctol, use_bulk, Vw, RR, lrc) == cudaSuccess) {
-                *replayed = true;
-                return cudaSuccess;
-            }
-            cudaGetLastError();
-        }
-    }
+    // V is replayed from the rotation log by k_apply_log after this launch.  (Round 1
+    // replayed it from extra clusters of the same cooperative launch that polled the
+    // Jacobi cluster's progress; that result changed under ncu -- a cross-cluster
+    // spin protocol inside one launch -- so it was removed.)
     return cudaLaunchKernelEx(&cfg, k_jacobi_block<true, R>, p, h, (const double *)W, W, rlog, 50, ctrl, abort, ctol,
-                              use_bulk, (double *)nullptr, 0, 0);
+                              use_bulk);
 }
 
 size_t small_svd_log_doubles(int p) {
@@ -1179,22 +1013,18 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
         const size_t smem = (size_t)2 * h * p * 8;
         cudaError_t e;
         const int rpl = (p + 31) / 32;
-        bool replayed = false;
-        e = rpl <= 1 ? launch_jacobi<1>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 2 ? launch_jacobi<2>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 3 ? launch_jacobi<3>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 4 ? launch_jacobi<4>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 5 ? launch_jacobi<5>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 6 ? launch_jacobi<6>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 8 ? launch_jacobi<8>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 10 ? launch_jacobi<10>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 12 ? launch_jacobi<12>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-          : rpl <= 16 ? launch_jacobi<16>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed)
-                      : launch_jacobi<20>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s, Vw, &replayed);
-        if (e == cudaSuccess && replayed) {
-            count_launch();
-            done = true;
-        } else if (e == cudaSuccess) {
+        e = rpl <= 1 ? launch_jacobi<1>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 2 ? launch_jacobi<2>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 3 ? launch_jacobi<3>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 4 ? launch_jacobi<4>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 5 ? launch_jacobi<5>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 6 ? launch_jacobi<6>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 8 ? launch_jacobi<8>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 10 ? launch_jacobi<10>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 12 ? launch_jacobi<12>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+          : rpl <= 16 ? launch_jacobi<16>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s)
+                      : launch_jacobi<20>(C, p, h, smem, W, rlog, ctrl, abort, ctol, s);
+        if (e == cudaSuccess) {
             count_launch();
             const int per_round = C * h;
             const int rps = (int)jacobi_rounds_per_sweep(C, h);
@@ -1217,17 +1047,6 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
     }
     k_svd_finish<<<1, 1024, 0, s>>>(p, W, Vw, Uh, Sh, Vh, kneed, ctrl, abort);
     count_launch();
-    if (kJacobiTiming && getenv("SVDSC_KTIMING")) {
-        unsigned long long hj[8];
-        cudaStreamSynchronize(s);
-        cudaMemcpyFromSymbol(hj, g_jt, sizeof(hj));
-        const unsigned long long z[8] = {0};
-        cudaMemcpyToSymbol(g_jt, z, sizeof(z));
-        const double n = hj[4] ? (double)hj[4] : 1.0;
-        fprintf(stderr, "[jtiming] p=%d C=%d h=%d cross rounds=%llu  load=%.0f dots=%.0f rot+store=%.0f sync=%.0f cycles/round"
-                "  exchanges=%llu x %.0f cycles\n",
-                p, C, h, hj[4], hj[0] / n, hj[1] / n, hj[2] / n, hj[3] / n, hj[6], hj[6] ? (double)hj[5] / hj[6] : 0.0);
-    }
 }
 
 void residuals(int t, int k, const double *T, int ldt, const double *Uh, const double *Sh, double tol,
