@@ -9,17 +9,24 @@ workload's synthetic input, which is resident in HBM before timing starts.
   value        Lanczos steps per second of the whole job (steps of all timed
                solves / max-over-ranks device time)
   ms_per_step  time-to-k-triplets of one solve (ms)
-  roofline     dominant kernel family (the A / A^T products for dense and
-               sparse inputs), algorithmic bytes per launch
-               over its CUDA-event-timed average duration inside the timed
-               region, against MEASURED_PEAKS.json hbm_gbs
+  roofline     dominant kernel family by device time (the fused CGS2
+               re-orthogonalization on sparse inputs, the A / A^T products on
+               dense ones): algorithmic bytes per launch over
+               its CUDA-event-timed average duration inside the timed region,
+               against MEASURED_PEAKS.json hbm_gbs; `traffic` from the committed
+               ncu capture (profiles/traffic.json)
   e2e          same metric through the C-ABI host-buffer entry point
                (svdsc_solve_host_*), H2D of A and v0 and D2H of S, U, V, resid
                inside the timed region
-  cpu_baseline the CPU oracle (oracle/oracle.c, 1 thread) on a bounded sample
-The default workload is BASELINE.json configs[1] (dense 20,000 x 5,000,
-sigma_i = exp(-i/40), k = 50).  A is 800 MB, larger than the 126 MB L2, so no
-L2 flush is needed between timed solves.
+  cpu_baseline the CPU oracle (oracle/oracle.c, 1 thread pinned to one core):
+               per-step cost t(i) = a + b i fitted on two bounded samples of
+               the first Lanczos steps, extrapolated to the GPU solve's step
+               schedule (labelled "extrapolated")
+The default workload is BASELINE.json configs[3], the largest config that fits
+one GPU (power-law 4,000,000 x 2,000,000, ~150M nnz, k = 100): A is 1.8 GB per
+pass, far larger than the 126 MB L2, so no flush is needed between solves.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, NCCL); every rank generates only its own rows.
 
 --impl reference times the CPU oracle as it stands (the reference arm of this
 tier): each step is a bounded sample (the first Lanczos steps of LBP on the
@@ -93,28 +100,85 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_sample(wl, seconds_target=15.0):
-    """Time the oracle as it stands (1 thread) on the first s Lanczos steps of
-    this workload: returns (steps/s, s, seconds)."""
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+class PinnedCore:
+    """Pin this process to one core while the single-threaded oracle runs."""
+
+    def __enter__(self):
+        self.old = None
+        try:
+            self.old = os.sched_getaffinity(0)
+            self.core = min(self.old)
+            os.sched_setaffinity(0, {self.core})
+        except Exception:
+            self.core = None
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            os.sched_setaffinity(0, self.old)
+
+
+def cpu_fit(wl, seconds_target=15.0):
+    """Time the oracle as it stands (1 thread, one pinned core) on the first s1
+    and s2 Lanczos steps of this workload; fit t(i) = a + b i for the cost of
+    step i (products + CGS2 against i basis vectors): LBP(s) = a s + b s(s+1)/2."""
     import oracle as O
-    # calibrate s with a 2-step probe, then run a bounded sample
-    t0 = time.perf_counter()
-    O.lbp(wl.A, 2, wl.v0)
-    probe = time.perf_counter() - t0
-    per = max(probe / 2.5, 1e-4)
-    s = int(max(2, min(wl.t, seconds_target / per)))
-    t0 = time.perf_counter()
-    O.lbp(wl.A, s, wl.v0)
-    dt = time.perf_counter() - t0
-    return s / dt, s, dt
+    with PinnedCore() as pc:
+        t0 = time.perf_counter()
+        O.lbp(wl.A, 2, wl.v0)
+        probe = max(time.perf_counter() - t0, 1e-4) / 2.0
+        s2 = int(max(4, min(wl.t, 0.75 * seconds_target / probe)))
+        s1 = max(2, s2 // 3)
+        times = {}
+        for s in (s1, s2):
+            t0 = time.perf_counter()
+            O.lbp(wl.A, s, wl.v0)
+            times[s] = time.perf_counter() - t0
+    # solve [s1, s1(s1+1)/2; s2, s2(s2+1)/2] [a; b] = [T1; T2]
+    import numpy as np
+    Mx = np.array([[s1, s1 * (s1 + 1) / 2], [s2, s2 * (s2 + 1) / 2]], dtype=float)
+    a, b = np.linalg.solve(Mx, np.array([times[s1], times[s2]]))
+    if b < 0:  # per-column cost below timing noise at this size
+        a, b = times[s2] / s2, 0.0
+    return {"a": float(a), "b": float(b), "s1": s1, "s2": s2, "t1": times[s1], "t2": times[s2],
+            "core": pc.core, "sample_seconds": times[s1] + times[s2]}
+
+
+def step_schedule(k, t, passes):
+    """Basis sizes i of the Lanczos steps of a solve: 1..t, then k+1..t per restart."""
+    return list(range(1, t + 1)) + list(range(k + 1, t + 1)) * max(0, passes - 1)
+
+
+def relaunch_distributed(args_list, n):
+    """--gpus N without torchrun: one process per GPU via torch.distributed.run."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + args_list
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", type=int, default=2, help="BASELINE.json config id (1-based)")
+    ap.add_argument("--workload", type=int, default=4, help="BASELINE.json config id (1-based)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -127,6 +191,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(sys.argv[1:], args.gpus)
 
     import numpy as np
     import workloads as W
@@ -138,14 +204,16 @@ def main():
         # reference arm = the CPU oracle as it stands, bounded sample per step
         import oracle as O
         O.lib()
-        _, s, _ = cpu_sample(wl, seconds_target=6.0)
+        fit = cpu_fit(wl, seconds_target=6.0)
+        s = fit["s2"]
         times = []
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            O.lbp(wl.A, s, wl.v0)
-            dt = time.perf_counter() - t0
-            if i >= args.warmup:
-                times.append(dt)
+        with PinnedCore():
+            for i in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                O.lbp(wl.A, s, wl.v0)
+                dt = time.perf_counter() - t0
+                if i >= args.warmup:
+                    times.append(dt)
         val = s * len(times) / sum(times)
         line = {
             "impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": args.gpus,
@@ -155,7 +223,10 @@ def main():
             "config": {"workload": wl.name, "m": wl.A.m, "n": wl.A.n, "nnz": wl.A.nnz, "k": wl.k, "t": wl.t,
                        "tol": wl.tol, "l2": "inputs larger than L2 (A is %d MB)" % (wl.A.bytes_one_pass() >> 20)},
             "cpu_baseline": {"value": val, "unit": "steps/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {s} Lanczos steps (Alg. 1 + CGS2) of {wl.name}, plain C, 1 thread"},
+                             "sample": f"each step = the first {s} Lanczos steps (Alg. 1 + CGS2) of {wl.name}, "
+                                       f"plain C, 1 thread pinned to one core (early steps: small bases, so "
+                                       f"this rate overstates the oracle's whole-solve rate)",
+                             "fit_t_i": {"a_s": fit["a"], "b_s": fit["b"]}, **host_info()},
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
@@ -174,22 +245,35 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- workload: rank-local rows of A (row partition) ----
-    wl_full = W.config(args.workload)
-    A = wl_full.A
-    if world > 1:
-        if A.kind == "csr":
-            bounds = S.partition_rows(A.row_ptr, (wl_full.k + wl_full.t) // 2, world)
-        else:
-            bounds = np.linspace(0, A.m, world + 1).astype(np.int64)
+    cid = args.workload
+    deg = W.degrees(cid) if world > 1 else None
+    if world > 1 and deg is not None:
+        # every rank generates only its rows (counter-based per-row streams)
+        rp = np.zeros(deg.size + 1, dtype=np.int64)
+        rp[1:] = np.cumsum(deg)
+        kt = {3: (100, 300), 4: (100, 300), 5: (200, 600)}[cid]  # (k, t) of configs 3-5
+        bounds = S.partition_rows(rp, (kt[0] + kt[1]) // 2, world)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-        if A.kind == "csr":
-            rp = A.row_ptr[r0:r1 + 1] - A.row_ptr[r0]
-            Al = W.Matrix("csr", r1 - r0, A.n, row_ptr=rp, col_idx=A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]],
-                          values=A.values[A.row_ptr[r0]:A.row_ptr[r1]])
-        else:
-            Al = W.dense_matrix(A.dense[r0:r1])
+        wl_full = W.config(cid, r0=r0, r1=r1)
+        Al = wl_full.A
+        m_global = int(deg.size)
+        nnz_global = int(rp[-1])
     else:
-        r0, r1, Al = 0, A.m, A
+        wl_full = W.config(cid)
+        A = wl_full.A
+        m_global, nnz_global = A.m, A.nnz
+        if world > 1:
+            bounds = np.linspace(0, A.m, world + 1).astype(np.int64)
+            r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+            if A.kind == "csr":
+                rpl = A.row_ptr[r0:r1 + 1] - A.row_ptr[r0]
+                Al = W.Matrix("csr", r1 - r0, A.n, row_ptr=rpl, col_idx=A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]],
+                              values=A.values[A.row_ptr[r0]:A.row_ptr[r1]])
+            else:
+                Al = W.dense_matrix(A.dense[r0:r1])
+        else:
+            r0, r1, Al = 0, A.m, A
+    n_cols = Al.n
 
     stream = torch.cuda.current_stream()
     H = S.Handle(stream)
@@ -197,7 +281,7 @@ def main():
         uid = [S.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         H.comm_init(world, rank, uid[0])
-    M = S.Matrix.from_host(H, Al, device=dev, row_offset=r0, m_global=A.m)
+    M = S.Matrix.from_host(H, Al, device=dev, row_offset=r0, m_global=m_global)
     v0 = torch.from_numpy(wl_full.v0).to(dev)
     k, t = wl_full.k, wl_full.t
     ws = torch.empty(S.workspace_size(M, k, t=t), dtype=torch.uint8, device=dev)
@@ -230,14 +314,14 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    steps_total, launches, passes, res, bytes_model, reorths = 0, 0, [], None, 0, 0
+    steps_total, launches, passes, res, bytes_model, bytes_reorth = 0, 0, [], None, 0, 0
     for _ in range(args.steps):
         res = solve()
         steps_total += res.info["steps"]
         launches += res.info["launches"]
         passes.append(res.info["passes"])
         bytes_model += res.info["bytes_model"]
-        reorths += res.info["reorths"]
+        bytes_reorth += res.info["bytes_reorth"]
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -258,21 +342,20 @@ def main():
     bA = Al.bytes_one_pass() if Al.kind == "dense" else 12 * Al.nnz + 4 * (Al.m + 1)
     bAt = Al.bytes_one_pass() if Al.kind == "dense" else 12 * Al.nnz + 4 * (Al.n + 1)
     if fam == "cgs2_fused":
-        # algorithmic CGS2 bytes (8 N (3i + 5) per re-orthogonalization)
-        # = the solves' modelled step bytes minus the products' (one A and one A^T
-        # pass per step, plus the u_1 product)
-        # (the library's model charges bA for both products of a step)
-        cgs_bytes = bytes_model - steps_total * 2 * bA - args.steps * bA
-        bytes_per_launch = cgs_bytes / max(f_calls, 1)
+        # algorithmic CGS2 bytes, 8 N (3 i + 5) per re-orthogonalization (SURVEY.md
+        # 8(d)), counted by the library per call (svdsc_info.bytes_reorth)
+        bytes_per_launch = bytes_reorth / max(f_calls, 1)
     else:
         bytes_per_launch = bA if fam == "Av" else bAt
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # DRAM bytes per launch of this kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        kname = ("k_gemv_t" if fam == "ATu" else "k_gemv_n") if Al.kind == "dense" else None
-        if kname in tj and tj[kname].get("workload") == wl_full.name:
-            traffic = tj[kname]["bytes_per_launch"]
+        ent = tj.get(wl_full.name.split("_div")[0], {}).get(fam)
+        if ent and world == 1:
+            # the capture's DRAM/algorithmic ratio applied to this launch size
+            traffic = ent["dram_bytes"] / ent["algorithmic_bytes"] * bytes_per_launch
+            traffic_src = ent
     except Exception:
         traffic = None
     achieved = bytes_per_launch / (f_ms / f_calls / 1e3) / 1e9 if f_calls else None
@@ -297,6 +380,7 @@ def main():
         d2h = 8 * (k + Al.m * k + Al.n * k + k)
         v0h = torch.from_numpy(wl_full.v0).pin_memory().numpy()
         S.svds_c_host(H, Ahost, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=v0h, reorth=args.reorth)  # warm
+        an = 0.0
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -306,40 +390,50 @@ def main():
             torch.cuda.synchronize()
             e2e_ms += e0.elapsed_time(e1)
             e2e_steps += out[5]["steps"]
+            an += out[5]["seconds_analysis"]
         e2e = {"value": e2e_steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.e2e_steps,
-               "note": "includes per-solve matrix analysis (validation" + (", CSC build" if Al.kind == "csr" else "") + ")"}
+               "analysis_ms_per_step": 1e3 * an / args.e2e_steps,
+               "note": "includes per-solve matrix analysis (validation" + (", row bins, CSC build" if Al.kind == "csr" else "") + ")"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
-        sps, s, dt = cpu_sample(wl_full, seconds_target=15.0)
-        cpu = {"value": sps, "unit": "steps/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {s} Lanczos steps (Alg. 1 + CGS2, LBP first pass) of {wl_full.name}, "
-                         f"{dt:.1f} s, plain C -O2, 1 thread"}
+        fit = cpu_fit(wl_full, seconds_target=15.0)
+        sched = step_schedule(k, t, passes[-1])
+        t_solve = sum(fit["a"] + fit["b"] * i for i in sched)
+        cpu = {"value": len(sched) / t_solve, "unit": "steps/s", "cores": 1, "kind": "oracle",
+               "time_to_k_s": t_solve,
+               "sample": (f"extrapolated: per-step cost t(i) = a + b i fitted on the oracle's first "
+                          f"{fit['s1']} and {fit['s2']} Lanczos steps (Alg. 1 + CGS2) of {wl_full.name} "
+                          f"({fit['sample_seconds']:.1f} s of plain C -O2, 1 thread pinned to core {fit['core']}), "
+                          f"a = {fit['a']:.4g} s, b = {fit['b']:.4g} s, summed over the GPU solve's "
+                          f"{len(sched)} steps ({passes[-1]} passes)"),
+               **host_info()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl_full.name, "m": A.m, "n": A.n, "nnz": A.nnz, "k": k, "t": t,
+            "config": {"workload": wl_full.name, "m": m_global, "n": n_cols, "nnz": nnz_global, "k": k, "t": t,
                        "tol": wl_full.tol, "maxit": wl_full.maxit, "passes_per_solve": passes,
                        "lanczos_steps_per_solve": steps_total // args.steps,
                        "time_to_k_ms": ms / args.steps,
-                       "l2": f"inputs larger than L2 (A = {A.bytes_one_pass() >> 20} MB per pass)",
+                       "l2": f"inputs larger than L2 (A = {(12 * nnz_global if Al.kind == 'csr' else 8 * m_global * n_cols) >> 20} MB per pass)",
                        "parallelism": f"rows{world}" if world > 1 else "single",
+                       "rank0_rows": [r0, r1],
                        "step_hbm_gb_per_s": step_bytes * (steps_total / (ms / 1e3)) / 1e9,
                        "step_bytes_model": step_bytes,
                        "reorth": ("full CGS2 every half-step (PAPER.md:121)" if args.reorth == 2 else
                                   "partial (omega recurrence, DESIGN.md Q20; not the paper's method; "
-                                  "step_bytes_model still counts every half-step's CGS2)"),
-                       "reorth_half_steps_per_solve": reorths // args.steps},
+                                  "step_bytes_model still counts every half-step's CGS2)")},
             "roofline": {"bound": "hbm",
                          "kernel": ("fused CGS2 re-orthogonalization (3 sweeps of U_i / V_i)" if fam == "cgs2_fused"
-                                    else f"{fam} product ({'gemv' if A.kind == 'dense' else 'spmv'})"),
+                                    else f"{fam} product ({'gemv' if Al.kind == 'dense' else 'spmv'})"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "bytes_per_launch": bytes_per_launch, "avg_launch_us": 1e3 * f_ms / max(f_calls, 1),
                          "share_of_step": f_ms / ms if ms else None, "peak_source": peak_src},
             "breakdown_ms_one_solve": {f: round(v[0], 3) for f, v in prof_all.items() if v[1]},

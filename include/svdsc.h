@@ -73,11 +73,13 @@ typedef struct {
     uint64_t seed;        /* seed of the internal start vector / breakdown streams      */
     const double *v0;     /* device, length ncols (global), or NULL -> internal N(0,1)  */
     int32_t fixed_passes; /* > 0: run exactly this many passes (parity hook, Q18)        */
-    int32_t reorth;       /* 2 = CGS2 (default when 0 is not requested: pass 2);         */
+    int32_t reorth;       /* 0 or 2 = CGS2 every half-step, the paper's method           */
+                          /*     (0 so that a zero-initialized struct is   */
+                          /*     the default);                                            */
                           /* 1 = partial: CGS2 only when the omega estimate of the loss  */
                           /*     of orthogonality exceeds sqrt(eps) (Q20;      */
                           /*     single GPU; PAPER.md:42 names the class);               */
-                          /* 0 = off, test-only                            */
+                          /* -1 = off, test-only                           */
 } svdsc_opts;
 
 typedef struct {
@@ -91,6 +93,11 @@ typedef struct {
     int64_t bytes_model;  /* algorithmic HBM bytes of the Lanczos steps */
                           /* (with reorth = 1: as if every half-step re-orthogonalized)  */
     int64_t reorths;      /* Lanczos half-steps (A^T u or A v side) re-orthogonalized     */
+    int64_t bytes_reorth; /* the CGS2 share of bytes_model: 8 N (3 i + 5) per           */
+                          /* re-orthogonalization (+ 8 m k for the restart's U_k rho)    */
+    double seconds_analysis; /* host wall time of the matrix's analysis (svdsc_matrix_*:  */
+                          /* validation, row bins, CSC copy); the host-buffer entry      */
+                          /* points include it in seconds_total                           */
 } svdsc_info;
 
 /* ---- handles --------------------------------------------------------------- */
@@ -152,9 +159,14 @@ SVDSC_API svdsc_status svdsc_solve_host_dense(svdsc_handle *h, int64_t m, int64_
  * the scalar c (may be NULL: c = 0, yprev ignored).  Enqueued on the stream. */
 SVDSC_API svdsc_status svdsc_op_matvec(svdsc_matrix *M, int trans, const double *x, double *y,
                              const double *c_dev, const double *yprev);
-/* a2-a4 / a6: two-pass classical Gram-Schmidt of w (length N) against the first
- * ncols columns of the column-major basis Q (ld >= N), then
- * *norm_dev = ||w|| (device scalar).  w is overwritten.  Enqueued. */
+/* a2-a4 / a6: one re-orthogonalization half-step of the solver: two-pass
+ * classical Gram-Schmidt of w (length N, device, 16-byte aligned for the
+ * streaming kernels) against the first ncols columns of the column-major basis
+ * Q (ld >= N), then beta = ||w|| (Alg. 1 lines 6 / 8) and
+ * w <- w / beta.  *norm_dev (device scalar, may be NULL) = beta; a breakdown
+ * (beta <= 1e-14, reading Q7) gives beta = 0 and leaves w unnormalized.  The
+ * kernel is the one the solver picks for this shape (svdsc_set_policy
+ * SVDSC_POLICY_CGS2 overrides).  Synchronous. */
 SVDSC_API svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const double *Q,
                            int64_t ldq, double *w, double *norm_dev);
 /* a7: SVD of the p x p column-major device matrix Tm (Alg. 2 step 4) by the
@@ -190,6 +202,27 @@ SVDSC_API svdsc_status svdsc_op_lbp(svdsc_matrix *M, const svdsc_opts *o, int32_
 SVDSC_API svdsc_status svdsc_profile_enable(svdsc_handle *h, int enable);
 SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int64_t *calls);
 
+/* ---- kernel-schedule policy --------------------------------------------------
+ * The library picks each kernel from the operand's shape (value 0 = automatic,
+ * the default and the product path).  A policy forces one schedule so that every
+ * kernel the automatic choice can pick is testable at any size; a forced kernel
+ * that cannot run a given shape falls back to the always-applicable path
+ * (split sweeps / one-CTA Jacobi).  Per handle; applies to the handle's later
+ * calls, including matrix analysis (SVDSC_POLICY_SPMV is read there).
+ *   SVDSC_POLICY_SPMV:      0 auto (nnz-balanced tiles when rows > 2048 exist,
+ *                           else row-length bins), 1 row-length bins, 2 nnz tiles
+ *   SVDSC_POLICY_CGS2:      0 auto (cluster for bases <= 2 MB, else Q-resident
+ *                           when the rows fit in shared memory, else streaming),
+ *                           1 split sweeps, 2 Q-resident, 3 cp.async streaming,
+ *                           4 TMA streaming, 5 thread-block cluster
+ *   SVDSC_POLICY_SMALL_SVD: 0 auto (cluster block Jacobi + rotation replay),
+ *                           1 one-CTA Jacobi
+ * EINVAL for an unknown key or value. */
+#define SVDSC_POLICY_SPMV 0
+#define SVDSC_POLICY_CGS2 1
+#define SVDSC_POLICY_SMALL_SVD 2
+SVDSC_API svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t value);
+
 /* ---- multi-GPU (row-partitioned A) -------------------------- */
 /* Rank 0 creates an NCCL unique id (128 bytes, host) that the caller
  * broadcasts (e.g. torch.distributed.broadcast); every rank then calls
@@ -197,6 +230,20 @@ SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int
  * SVDSC_ENCCL if unavailable. */
 SVDSC_API svdsc_status svdsc_comm_unique_id(unsigned char id[128]);
 SVDSC_API svdsc_status svdsc_comm_init(svdsc_handle *h, int nranks, int rank, const unsigned char id[128]);
+/* In-process ("loopback") group: nranks (<= 16) ranks that are threads of this
+ * process, each with its own handle and stream (on one device, or on devices
+ * with peer access enabled by the caller).  Each rank's thread calls
+ * svdsc_comm_init_group(h, g, rank), then every rank calls the same
+ * svdsc_solve concurrently.  Collectives synchronize the rank's stream, meet
+ * the other ranks at a host barrier and sum in rank order (bitwise identical
+ * on every rank); no kernel waits on another rank.  A testing and
+ * single-process backend of the same multi-rank path as NCCL.  The group is
+ * reference counted: svdsc_group_destroy may be called once every rank has
+ * called svdsc_comm_init_group. */
+typedef struct svdsc_group svdsc_group;
+SVDSC_API svdsc_status svdsc_group_create(int nranks, svdsc_group **g);
+SVDSC_API void svdsc_group_destroy(svdsc_group *g);
+SVDSC_API svdsc_status svdsc_comm_init_group(svdsc_handle *h, svdsc_group *g, int rank);
 /* Host-only partitioner (no GPU needed): contiguous row blocks of a CSR
  * matrix (host row_ptr, m+1 entries) balanced by the per-step byte cost
  * w_r = 24 nnz_r + 24 basis_cols.  bounds: host,

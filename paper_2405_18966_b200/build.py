@@ -9,13 +9,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsvdsc.so")
-SOURCES = ["svdsc.cu", "matvec.cu", "cgs.cu", "cgs_fused.cu", "svd.cu", "pro.cu", "paper_api.cpp"]
+SOURCES = ["svdsc.cu", "comm.cu", "matvec.cu", "cgs.cu", "cgs_fused.cu", "svd.cu", "pro.cu", "paper_api.cpp"]
 CLI = os.path.join(HERE, "svdsc-cli")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-FLAGS += os.environ.get("SVDSC_NVCC_EXTRA", "").split()  # tuning experiments only
 
 
 def stale() -> bool:

@@ -29,8 +29,6 @@
 #include "internal.h"
 
 namespace svdsc {
-unsigned long long *g_ktbuf = nullptr;
-unsigned long long *g_qtbuf = nullptr;  // Q-resident kernel phase timers (SVDSC_KTIMING=1)
 namespace {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -123,7 +121,6 @@ struct Args {
     int rpb;              // rows per CTA
     int RT;               // row tile of phase B (streaming mode)
     int wsmem;            // keep the CTA's w rows in shared memory
-    unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
     PreReduce pre;        // pending split-K reduction of w (pre.partial != NULL)
     const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
     int gate_want;
@@ -149,12 +146,6 @@ __device__ __forceinline__ double qval(const Args &a, const double *qsh, int ldq
 
 template <bool QS>
 __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
-    long long tq[12];
-    int ntq = 0;
-    auto qstamp = [&]() {
-        if (a.tdbg && ntq < 12) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq[ntq++]));
-    };
-    qstamp();
     grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the grid
     if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
@@ -196,7 +187,6 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    qstamp();
     if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = a.pre_h[j];
         __syncthreads();
@@ -295,13 +285,11 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
                 __syncthreads();
             }
         }
-        qstamp();
         grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, ncols, a.h1, sh);
         grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
         __syncthreads();
-        qstamp();
 
         // ---------------- phase B: w' = w - Q h1, partial h2, ||w'||^2 ----------------
         if (QS) {
@@ -360,13 +348,11 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
         }
         const double bn = block_sum_all(nrm_wp, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
-        qstamp();
         grid_sync(a.flags, a.epoch + (++nbar));
         reduce_cols(a, ncols + 1, a.h2, sh);
         grid_sync(a.flags, a.epoch + (++nbar));
         for (int j = tid; j <= ncols; j += blockDim.x) hs[j] = __ldcg(a.h2 + j);
         __syncthreads();
-        qstamp();
     } else {
         // plain norm: ||w||^2 into hs[0] (ncols == 0)
         for (int i = tid; i < nr; i += blockDim.x) nrm_wp = fma(wv[i], wv[i], nrm_wp);
@@ -432,11 +418,6 @@ __global__ void __launch_bounds__(256) k_cgs2_fused(Args a) {
     }
     if (!bd)
         for (int i = tid; i < nr; i += blockDim.x) a.w[r0 + i] = wv[i] / beta;
-    qstamp();
-    if (a.tdbg && tid == 0 && blockIdx.x == 0 && ntq == 7) {
-        for (int q = 1; q < 7; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tq[q] - tq[q - 1]));
-        atomicAdd(a.tdbg + 7, 1ull);
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -463,8 +444,14 @@ struct SArgs {
     int check;
     const double *pre_h;
     int64_t rpb;  // rows per CTA, multiple of RT
-    unsigned long long *tdbg;  // optional phase timers (SVDSC_KTIMING=1 debugging aid)
-    int snake;    // stream2 sweep-direction policy (see k_cgs2_stream2)
+    int snake;    // stream2 sweep direction: 1 alternate (default), 2 only with a 2-stage ring
+    // stream2 only: 0 = the whole CGS2 in one launch (single GPU); 1 / 2 / 3 =
+    // one phase of it (multi-GPU: the host all-reduces h1, then [h2; ||w'||^2],
+    // across the ranks between the launches): 1 = [pre_h sweep] + h1 (CTA-reduced
+    // into h1), 2 = w' and h2, ||w'||^2 (into h2[0..ncols]), 3 = w'', beta,
+    // normalization -- where the explicit norm is needed (reading G1) phase 3
+    // leaves w'' unnormalized and raises ctrl->abort with abort_kind = 1
+    int phase;
     const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
     int gate_want;
 };
@@ -509,54 +496,6 @@ __device__ __forceinline__ void issue_tile(const SArgs &a, double *buf, double *
     cp_commit();
 }
 
-// per-row s = sum_j T(rr, j) h[j] for the RT rows of a tile: threads as (row,
-// part), P = kSThr/RT parts (a warp = one part, consecutive rows); returns (on
-// threads < RT) the full sum, parts added in fixed order.
-template <int RT, int kSThr>
-__device__ __forceinline__ double tile_rowdot(const double *T, const double *hs, int ncols, double *red) {
-    constexpr int P = kSThr / RT, kCh = RT / 2;
-    const int rr = threadIdx.x % RT, part = threadIdx.x / RT;
-    const int c = rr >> 1, o = rr & 1;
-    // the swizzle of column j depends on j & (kCh-1); with stride P it cycles with period kCh/gcd
-    double s0 = 0.0, s1 = 0.0;
-    int j = part;
-    const double *tp = T + o;
-    for (; j + P < ncols; j += 2 * P) {
-        const int j1 = j + P;
-        s0 = fma(tp[j * RT + ((c ^ (j & (kCh - 1))) << 1)], hs[j], s0);
-        s1 = fma(tp[j1 * RT + ((c ^ (j1 & (kCh - 1))) << 1)], hs[j1], s1);
-    }
-    if (j < ncols) s0 = fma(tp[j * RT + ((c ^ (j & (kCh - 1))) << 1)], hs[j], s0);
-    red[part * RT + rr] = s0 + s1;
-    __syncthreads();
-    double tot = 0.0;
-    if (threadIdx.x < RT)
-        for (int q = 0; q < P; q++) tot += red[q * RT + threadIdx.x];
-    return tot;
-}
-
-// acc[q] += sum_rr T(rr, j) x[rr] for columns j = tid + kSThr q
-template <int RT, int kSThr, int NQ>
-__device__ __forceinline__ void tile_coldot(const double *T, const double *x, int ncols, double (&acc)[NQ]) {
-    constexpr int kCh = RT / 2;
-#pragma unroll
-    for (int q = 0; q < NQ; q++) {
-        const int j = threadIdx.x + kSThr * q;
-        if (j < ncols) {
-            const double *tj = T + j * RT;
-            const int sw = j & (kCh - 1);
-            double s0 = acc[q], s1 = 0.0;
-#pragma unroll
-            for (int c = 0; c < kCh; c++) {
-                const double2 v = *reinterpret_cast<const double2 *>(tj + ((c ^ sw) << 1));
-                s0 = fma(v.x, x[2 * c], s0);
-                s1 = fma(v.y, x[2 * c + 1], s1);
-            }
-            acc[q] = s0 + s1;
-        }
-    }
-}
-
 // one warp per column (fixed lane-strided order + xor tree: deterministic);
 // a block-wide reduction per column cost ~2 us per column (3 __syncthreads)
 __device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double *) {
@@ -567,188 +506,6 @@ __device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double 
         for (int t = lane; t < nb; t += 32) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
         s = warp_sum(s);
         if (lane == 0) out[j] = s;
-    }
-}
-
-template <int RT, int kSThr, int NS>
-__global__ void __launch_bounds__(kSThr) k_cgs2_stream(SArgs a) {
-    constexpr int NQ = 1024 / kSThr;  // columns per thread (ncols <= 1024)
-    grid_prepare(a.flags, a.epoch);
-    if (*(volatile int *)&a.ctrl->abort) return;
-    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
-    unsigned int nbar = 0;
-    extern __shared__ __align__(16) double smem_s[];
-    __shared__ double sh[32];
-    const int tid = threadIdx.x;
-    const int ncols = a.ncols;
-    const int tile_d = ncols * RT;
-    double *buf = smem_s;                    // NS x ncols x RT (swizzled)
-    double *wt = buf + NS * tile_d;          // NS x RT
-    double *hs = wt + NS * RT;               // ncols + 2
-    double *red = hs + ncols + 2;            // kSThr
-    double *wpt = red + kSThr;               // RT
-    const int64_t rb = (int64_t)blockIdx.x * a.rpb;
-    const int64_t re = min(a.N, rb + a.rpb);
-    const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
-
-    // generic tile loop: body(k, T, W) on tile k (rows rb + k RT ...); NS-stage
-    // cp.async ring (NS-1 tiles in flight while one is consumed); one commit
-    // group per iteration (possibly empty) keeps wait_group<NS-1> exact.
-    auto run_tiles = [&](auto &&body) {
-        if (ntiles == 0) return;
-#pragma unroll
-        for (int p = 0; p < NS - 1; p++) {
-            if (p < ntiles) {
-                const int64_t r1 = rb + (int64_t)p * RT;
-                issue_tile<RT, kSThr>(a, buf + p * tile_d, wt + p * RT, r1, (int)min((int64_t)RT, re - r1));
-            } else {
-                cp_commit();
-            }
-        }
-        for (int k = 0; k < ntiles; k++) {
-            const int kn = k + NS - 1;
-            if (kn < ntiles) {
-                const int64_t r1 = rb + (int64_t)kn * RT;
-                issue_tile<RT, kSThr>(a, buf + (kn % NS) * tile_d, wt + (kn % NS) * RT, r1,
-                                      (int)min((int64_t)RT, re - r1));
-            } else {
-                cp_commit();
-            }
-            cp_wait<NS - 1>();
-            __syncthreads();
-            body(k, buf + (k % NS) * tile_d, wt + (k % NS) * RT);
-            __syncthreads();
-        }
-        cp_wait<0>();
-    };
-
-    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7)), an extra sweep (once per pass)
-        for (int j = tid; j < ncols; j += blockDim.x) hs[j] = a.pre_h[j];
-        __syncthreads();
-        run_tiles([&](int k, const double *T, const double *W) {
-            const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
-            const int64_t r = rb + (int64_t)k * RT + tid;
-            if (tid < RT && r < re) a.w[r] = W[tid] - s;
-        });
-        grid_sync(a.flags, a.epoch + (++nbar));  // make the updated w visible to the cp.async reads below
-    }
-
-    double nrm_wp = 0.0;
-    if (ncols > 0) {
-        // phase A: partial h1 = Q_b^T w_b
-        double acc[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; q++) acc[q] = 0.0;
-        run_tiles([&](int, const double *T, const double *W) { tile_coldot<RT, kSThr, NQ>(T, W, ncols, acc); });
-#pragma unroll
-        for (int q = 0; q < NQ; q++) {
-            const int j = tid + kSThr * q;
-            if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc[q];
-        }
-        grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, ncols, a.h1, sh);
-        grid_sync(a.flags, a.epoch + (++nbar));
-        for (int j = tid; j < ncols; j += blockDim.x) hs[j] = __ldcg(a.h1 + j);
-        __syncthreads();
-        // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
-        double acc2[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; q++) acc2[q] = 0.0;
-        run_tiles([&](int k, const double *T, const double *W) {
-            const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
-            const int64_t r = rb + (int64_t)k * RT + tid;
-            if (tid < RT) {
-                double v = 0.0;
-                if (r < re) {
-                    v = W[tid] - s;
-                    a.w[r] = v;
-                    nrm_wp = fma(v, v, nrm_wp);
-                }
-                wpt[tid] = v;
-            }
-            __syncthreads();
-            tile_coldot<RT, kSThr, NQ>(T, wpt, ncols, acc2);
-        });
-#pragma unroll
-        for (int q = 0; q < NQ; q++) {
-            const int j = tid + kSThr * q;
-            if (j < ncols) a.partial[(int64_t)blockIdx.x * a.PS + j] = acc2[q];
-        }
-    } else {
-        run_tiles([&](int k, const double *, const double *W) {
-            const int64_t r = rb + (int64_t)k * RT + tid;
-            if (tid < RT && r < re) nrm_wp = fma(W[tid], W[tid], nrm_wp);
-        });
-    }
-    {
-        const double bn = block_sum_all(nrm_wp, sh);
-        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
-    }
-    grid_sync(a.flags, a.epoch + (++nbar));
-    sreduce_cols(a, ncols + 1, a.h2, sh);
-    grid_sync(a.flags, a.epoch + (++nbar));
-    for (int j = tid; j <= ncols; j += blockDim.x) hs[j] = __ldcg(a.h2 + j);
-    __syncthreads();
-
-    // phase C: w'' = w' - Q h2, beta, breakdown, normalize
-    const double nrmp = hs[ncols];
-    double hh = 0.0;
-    for (int j = tid; j < ncols; j += blockDim.x) hh = fma(hs[j], hs[j], hh);
-    hh = block_sum_all(hh, sh);
-    double beta2 = nrmp - hh;
-    const bool pyth = beta2 > 0.5 * nrmp;
-    const double amax = a.ctrl->amax[a.check & 1];
-    const double thr = 1e-14 * fmax(amax, 1.0);
-    bool bd = false;
-    double beta = 0.0;
-    if (pyth) {
-        beta = sqrt(beta2);
-        bd = !(beta > thr);
-        if (!bd && ncols > 0) {
-            run_tiles([&](int k, const double *T, const double *W) {
-                const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
-                const int64_t r = rb + (int64_t)k * RT + tid;
-                if (tid < RT && r < re) a.w[r] = (W[tid] - s) / beta;
-            });
-        } else if (!bd) {
-            for (int64_t r = rb + tid; r < re; r += blockDim.x) a.w[r] = a.w[r] / beta;
-        }
-    } else {
-        double nrm2 = 0.0;
-        if (ncols > 0) {
-            run_tiles([&](int k, const double *T, const double *W) {
-                const double s = tile_rowdot<RT, kSThr>(T, hs, ncols, red);
-                const int64_t r = rb + (int64_t)k * RT + tid;
-                if (tid < RT && r < re) {
-                    const double v = W[tid] - s;
-                    a.w[r] = v;
-                    nrm2 = fma(v, v, nrm2);
-                }
-            });
-        } else {
-            for (int64_t r = rb + tid; r < re; r += blockDim.x) nrm2 = fma(a.w[r], a.w[r], nrm2);
-        }
-        const double bn = block_sum_all(nrm2, sh);
-        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
-        grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, 1, a.h3, sh);
-        grid_sync(a.flags, a.epoch + (++nbar));
-        beta = sqrt(fmax(__ldcg(a.h3), 0.0));
-        bd = !(beta > thr);
-        if (!bd)
-            for (int64_t r = rb + tid; r < re; r += blockDim.x) a.w[r] = a.w[r] / beta;
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-        if (bd) {
-            *a.t_entry = 0.0;
-            a.ctrl->amax[(a.check + 1) & 1] = amax;
-            a.ctrl->abort_check = a.check;
-            __threadfence();
-            a.ctrl->abort = 1;
-        } else {
-            *a.t_entry = beta;
-            a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
-        }
     }
 }
 
@@ -905,16 +662,9 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         }
     };
 
-    // phase stamps (SVDSC_KTIMING): thread 0 only, kept in shared memory so
-    // they cost no registers in the streaming loops
-    __shared__ long long tk[8];
-    int ntk = 0;
-    auto stamp = [&]() {
-        if (a.tdbg && threadIdx.x == 0 && ntk < 8) tk[ntk] = clock64();
-        ntk++;
-    };
+    const int ph = a.phase;
     double hreg[M];
-    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
+    if (a.pre_h && ph <= 1) {  // w -= Q pre_h (restart, Eq. (7))
         load_h(a.pre_h, hreg);
         run_tiles([&](int k, const double *T, const double *W) {
             double s[RPW];
@@ -929,11 +679,11 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         grid_sync(a.flags, a.epoch + (++nbar));
     }
 
-    stamp();
     double nrm_wp = 0.0;
-    if (ncols > 0) {
-        // phase A: partial h1
+    if (ncols > 0 && ph <= 2) {
         double acc[M];
+        if (ph <= 1) {
+        // phase A: partial h1
 #pragma unroll
         for (int m = 0; m < M; m++) acc[m] = 0.0;
         run_tiles([&](int, const double *T, const double *W) {
@@ -947,15 +697,16 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             }
         });
         flush_cols(acc);
-        prefetch();  // phase B re-reads the same tiles: start them under the reduction
-        prefetched = true;
-        stamp();
+        if (ph == 0) {
+            prefetch();  // phase B re-reads the same tiles: start them under the reduction
+            prefetched = true;
+        }
         grid_sync(a.flags, a.epoch + (++nbar));
-        stamp();
         sreduce_cols(a, ncols, a.h1, sh);
+        if (ph == 1) return;  // the host all-reduces h1 across the ranks
         grid_sync(a.flags, a.epoch + (++nbar));
+        }
         load_h(a.h1, hreg);
-        stamp();
         // phase B: w' = w - Q h1 (written back), partial h2, ||w'||^2
 #pragma unroll
         for (int m = 0; m < M; m++) acc[m] = 0.0;
@@ -1010,7 +761,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             });
         }
         flush_cols(acc);
-    } else {
+    } else if (ph == 0 || ph == 2) {
         run_tiles([&](int k, const double *, const double *W) {
 #pragma unroll
             for (int q = 0; q < RPW; q++) {
@@ -1020,22 +771,23 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             }
         });
     }
-    {
-        const double bn = block_sum_all(nrm_wp, sh);
-        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+    if (ph == 0 || ph == 2) {
+        {
+            const double bn = block_sum_all(nrm_wp, sh);
+            if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+        }
+        if (ncols > 0 && ph == 0) {  // phase C reads w' written above by this CTA
+            __threadfence();
+            __syncthreads();
+            prefetch();
+            prefetched = true;
+        }
+        grid_sync(a.flags, a.epoch + (++nbar));
+        sreduce_cols(a, ncols + 1, a.h2, sh);
+        if (ph == 2) return;  // the host all-reduces [h2; ||w'||^2] across the ranks
+        grid_sync(a.flags, a.epoch + (++nbar));
     }
-    if (ncols > 0) {  // phase C reads w' written above by this CTA
-        __threadfence();
-        __syncthreads();
-        prefetch();
-        prefetched = true;
-    }
-    stamp();
-    grid_sync(a.flags, a.epoch + (++nbar));
-    sreduce_cols(a, ncols + 1, a.h2, sh);
-    grid_sync(a.flags, a.epoch + (++nbar));
     load_h(a.h2, hreg);
-    stamp();
     const double nrmp = __ldcg(a.h2 + ncols);
     double hh = 0.0;
     for (int j = tid; j < ncols; j += kSThr) {
@@ -1069,6 +821,28 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         } else if (!bd) {
             for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
         }
+    } else if (ph == 3) {
+        // multi-GPU: the explicit norm of w'' needs one more cross-rank reduction;
+        // form w'' and hand the norm to the host (pass-end repair, svdsc.cu)
+        if (ncols > 0)
+            run_tiles([&](int k, const double *T, const double *W) {
+                double s[RPW];
+                rowdots(T, hreg, s);
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    if (lane == q * kHalf && r < re) a.w[r] = W[rr] - s[q];
+                }
+            });
+        if (blockIdx.x == 0 && tid == 0) {
+            a.ctrl->abort_check = a.check;
+            a.ctrl->abort_kind = 1;
+            __threadfence();
+            a.ctrl->abort = 1;
+        }
+        cp_wait<0>();
+        return;
     } else {
         double nrm2 = 0.0;
         if (ncols > 0) {
@@ -1098,13 +872,6 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         bd = !(beta > thr);
         if (!bd)
             for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
-    }
-    stamp();
-    if (a.tdbg && threadIdx.x == 0 && ntk == 7 && a.N >= (int64_t)a.tdbg[15] && ncols >= (int)a.tdbg[14]) {
-        // phases: A | wait1 | reduce1+bar2+load | B | red2 | C
-        for (int q = 1; q < 7; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
-        atomicAdd(a.tdbg + 10, 1ull);
-        atomicAdd(a.tdbg + 11, (unsigned long long)ntiles);
     }
     cp_wait<0>();  // a prefetch may be pending if phase C was skipped
     if (blockIdx.x == 0 && tid == 0) {
@@ -1231,8 +998,6 @@ template <int M>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_constant__ CUtensorMap tq, SArgs a, int ns,
                                                              int nsplit) {
     constexpr int RT = kTmaRT, NW = kTmaNW, J = M;
-    unsigned long long g_entry = 0;
-    if (a.tdbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
     grid_prepare(a.flags, a.epoch);
     if (*(volatile int *)&a.ctrl->abort) return;
     if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
@@ -1375,12 +1140,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         grid_sync(a.flags, a.epoch + (++nbar));
     }
 
-    long long tk[8];
-    int ntk = 0;
-    auto stamp = [&]() {
-        if (a.tdbg && ntk < 8) tk[ntk++] = clock64();
-    };
-    stamp();
     double nrm_wp = 0.0;
     if (ncols > 0) {
         double acc[J];
@@ -1396,14 +1155,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         });
         flush_cols(acc);
         prefetch();
-        stamp();
         grid_sync(a.flags, a.epoch + (++nbar));
-        stamp();
         sreduce_cols(a, ncols, a.h1, sh);
-        stamp();
         grid_sync(a.flags, a.epoch + (++nbar));
         load_h(a.h1);
-        stamp();
 #pragma unroll
         for (int j = 0; j < J; j++) acc[j] = 0.0;
         // phase B: w' = w - Q h1 (written back), partial h2 = Q^T w', ||w'||^2
@@ -1437,12 +1192,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         __syncthreads();
         prefetch();
     }
-    stamp();
     grid_sync(a.flags, a.epoch + (++nbar));
     sreduce_cols(a, ncols + 1, a.h2, sh);
     grid_sync(a.flags, a.epoch + (++nbar));
     load_h(a.h2);
-    stamp();
     const double nrmp = __ldcg(a.h2 + ncols);
     double hh = 0.0;
     for (int j = tid; j < ncols; j += kTmaThreads) hh = fma(hs[j], hs[j], hh);
@@ -1494,20 +1247,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         if (!bd)
             for (int64_t r = rb + tid; r < re; r += kTmaThreads) a.w[r] = a.w[r] / beta;
     }
-    stamp();
-    const char *kfilter = nullptr;  // (device: filter set via a.tdbg[15] = min N)
-    (void)kfilter;
-    if (a.tdbg && tid == 0 && ntk == 8 && a.N >= (int64_t)a.tdbg[15] && ncols >= (int)a.tdbg[14]) {
-        for (int q = 1; q < 8; q++) atomicAdd(a.tdbg + q - 1, (unsigned long long)(tk[q] - tk[q - 1]));
-        atomicAdd(a.tdbg + 10, 1ull);
-        atomicAdd(a.tdbg + 11, (unsigned long long)ntiles);
-        if (blockIdx.x == 0) {
-            unsigned long long g_exit;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
-            atomicAdd(a.tdbg + 8, g_exit - g_entry);  // ns, CTA 0 entry -> exit
-            atomicAdd(a.tdbg + 9, (unsigned long long)(tk[0] - 0));
-        }
-    }
     // phase C prefetched but skipped (breakdown): wait for those copies so
     // that no bulk copy is in flight when the CTA exits
     if (tid == ptid && ncols > 0 && pyth && bd) {
@@ -1532,12 +1271,9 @@ template <int M>
 bool launch_tma(const CUtensorMap &tq, const SArgs &a0, int nsm, cudaStream_t s) {
     SArgs a = a0;
     if (a.ncols > kTmaNW * M) return false;
-    // column groups per tile: smallest split with units <= ~48 KB (deeper ring)
-    int nsplit = 1;
-    int unit_kb = 1024;  // SVDSC_TMA_UNIT_KB: split tiles into column groups of at most this many KB
-    if (const char *e = getenv("SVDSC_TMA_UNIT_KB")) unit_kb = atoi(e);
-    while (nsplit < 4 && (kTmaNW / nsplit) * M * 32 * 8 > unit_kb * 1024 && (M * (kTmaNW / (2 * nsplit))) % 16 == 0)
-        nsplit *= 2;
+    // one column group per tile (splitting tiles into column-group units for a
+    // deeper ring measured slower)
+    const int nsplit = 1;
     const int gbox = (kTmaNW / nsplit) * M / 16;
     const size_t stage_b = ((size_t)gbox * 512 + kTmaRT) * sizeof(double);
     const size_t fixed = ((size_t)2 * kTmaNW * kTmaRT + a.ncols + 2) * sizeof(double) + 128;
@@ -1579,33 +1315,6 @@ bool launch_tma_any(const CUtensorMap &tq, const SArgs &a, int nsm, cudaStream_t
     return false;  // wider bases: cp.async variants
 }
 
-template <int RT, int NT, int NS>
-bool launch_stream(const SArgs &a0, int nsm, cudaStream_t s) {
-    SArgs a = a0;
-    const size_t smem = ((size_t)NS * a.ncols * RT + NS * RT + a.ncols + 2 + NT + RT) * sizeof(double);
-    if (smem > 220 * 1024) return false;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_cgs2_stream<RT, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr = true;
-    }
-    int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_stream<RT, NT, NS>, NT, smem);
-    if (bps < 1) return false;
-    const int nb = nsm;
-    int64_t rpb = (a.N + nb - 1) / nb;
-    rpb = (rpb + RT - 1) / RT * RT;
-    a.rpb = rpb;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (a.N + rpb - 1) / rpb));
-    void *args[] = {&a};
-    if (cudaLaunchCooperativeKernel((void *)k_cgs2_stream<RT, NT, NS>, grid, NT, args, smem, s) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    count_launch();
-    return true;
-}
-
 }  // namespace
 
 bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_total, int64_t ld) {
@@ -1630,27 +1339,6 @@ bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
-}
-
-// debugging aid (SVDSC_KTIMING=1): per-phase cycle counters of the TMA kernel
-void ktiming_dump() {
-    if (g_qtbuf) {
-        unsigned long long q[16];
-        cudaMemcpy(q, g_qtbuf, sizeof(q), cudaMemcpyDeviceToHost);
-        cudaMemset(g_qtbuf, 0, sizeof(q));
-        const double n = q[7] ? (double)q[7] : 1.0;
-        fprintf(stderr, "[qtiming] calls=%llu  loadQ=%.0f phaseA=%.0f red1=%.0f phaseB=%.0f red2=%.0f phaseC=%.0f ns (CTA 0)\n",
-                q[7], q[0] / n, q[1] / n, q[2] / n, q[3] / n, q[4] / n, q[5] / n);
-    }
-    if (!g_ktbuf) return;
-    unsigned long long h[16];
-    cudaMemcpy(h, g_ktbuf, sizeof(h), cudaMemcpyDeviceToHost);
-    cudaMemset(g_ktbuf, 0, 14 * sizeof(unsigned long long));  // keep the filter in [14], [15]
-    const double n = h[10] ? (double)h[10] : 1.0;
-    fprintf(stderr,
-            "[ktiming] calls(x CTAs)=%llu avg tiles/CTA=%.1f  phaseA=%.0f wait1=%.0f reduce1=%.0f bar2+load=%.0f "
-            "phaseB=%.0f red2=%.0f phaseC=%.0f cycles  CTA0 entry->exit total %.3f ms\n",
-            h[10], h[11] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[8] * 1e-6);
 }
 
 // ---------------------------------------------------------------------------
@@ -1822,6 +1510,13 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
                 const void *tmap) {
+    // kernel choice (SVDSC_POLICY_CGS2): 0 automatic by size -- one thread-block
+    // cluster for bases <= 2 MB, else the Q-resident cooperative kernel when the
+    // CTA's rows of Q fit in shared memory, else the cp.async streaming kernel;
+    // 2 / 3 / 4 / 5 force Q-resident / streaming / TMA streaming / cluster;
+    // 1 (split kernels) and an inapplicable forced kernel return false
+    const int pol = g_policy.cgs2;
+    if (pol == 1) return false;
     constexpr int kThreads = 256;
     const size_t smem_cap = 200 * 1024;
     Args a{};
@@ -1843,33 +1538,16 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     a.t_entry = t_entry;
     a.check = check;
     a.pre_h = pre_h;
-    a.tdbg = nullptr;
-    if (const char *kt = getenv("SVDSC_KTIMING")) {
-        if (kt[0] == '1') {
-            if (!g_qtbuf) {
-                cudaMalloc(&g_qtbuf, 16 * sizeof(unsigned long long));
-                cudaMemset(g_qtbuf, 0, 16 * sizeof(unsigned long long));
-            }
-            a.tdbg = g_qtbuf;
-        }
-    }
-    // small bases: one thread-block cluster, DSMEM reductions (SVDSC_CLUSTER_CGS2:
-    // 0 off, else the byte threshold of N x ncols x 8 below which it is used)
-    {
-        static size_t cl_max = 0;
-        static bool cl_init = false;
-        if (!cl_init) {
-            cl_init = true;
-            cl_max = (size_t)2 << 20;  // measured: 12.7 vs 17.2 us per call at config 1 (1.2 MB);
-                                       // slower than the Q-resident kernel at 6 MB (config 2 V side)
-            if (const char *e = getenv("SVDSC_CLUSTER_CGS2")) cl_max = (size_t)strtoull(e, nullptr, 10);
-        }
-        const char *fse0 = getenv("SVDSC_FORCE_STREAM");
+    // small bases: one thread-block cluster, DSMEM reductions (measured: 12.7 vs
+    // 17.2 us per call at config 1 (1.2 MB); slower than the Q-resident kernel
+    // at 6 MB, the config 2 V side)
+    if (pol == 0 || pol == 5) {
+        const size_t cl_max = (size_t)2 << 20;
         const int C = 16;
         const int64_t rpb = (N + C - 1) / C;
         const size_t smem = ((size_t)rpb + 4 * ((size_t)ncols + 2)) * sizeof(double);
-        if ((size_t)N * (size_t)std::max(ncols, 1) * 8 <= cl_max && smem <= 200 * 1024 && ncols <= 1022 &&
-            !(fse0 && fse0[0] == '1')) {
+        if ((pol == 5 || (size_t)N * (size_t)std::max(ncols, 1) * 8 <= cl_max) && smem <= 200 * 1024 &&
+            ncols <= 1022) {
             static bool attr = false;
             if (!attr) {
                 cudaFuncSetAttribute(k_cgs2_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1910,17 +1588,15 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             }
             cudaGetLastError();
         }
+        if (pol == 5) return false;
     }
-    // try Q-resident mode: 2 CTAs per SM, then 1 (SVDSC_FORCE_STREAM=1 skips it: test hook)
-    const char *fse = getenv("SVDSC_FORCE_STREAM");
-    const bool force_stream = fse && fse[0] == '1';
-    int qs_first = 1;  // CTAs per SM tried first: 1 measured faster (fewer CTAs in each grid barrier / reduction); SVDSC_QS_PER_SM overrides
-    if (const char *e = getenv("SVDSC_QS_PER_SM")) qs_first = std::max(1, std::min(2, atoi(e)));
-    for (int per_sm = qs_first; per_sm >= 1 && !force_stream; per_sm--) {
-        const int nb = nsm * per_sm;
+    // Q-resident mode: the CTA's rows of Q staged once in shared memory (1 CTA
+    // per SM measured faster than 2: fewer CTAs in each grid barrier / reduction)
+    if (pol == 0 || pol == 2) {
+        const int nb = nsm;
         const int64_t rpb = (N + nb - 1) / nb;
         const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1) + std::max<int64_t>(256, rpb)) * sizeof(double);
-        if (ncols > 0 && smem * per_sm <= 220 * 1024 && smem <= smem_cap && rpb >= 1) {
+        if (ncols > 0 && smem <= smem_cap && rpb >= 1) {
             a.rpb = (int)rpb;
             a.RT = 1;
             a.wsmem = 1;
@@ -1932,17 +1608,21 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             }
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cgs2_fused<true>, kThreads, smem);
-            if (bps < per_sm) continue;
-            const int grid = (int)std::min<int64_t>(nb, (N + rpb - 1) / rpb);
-            void *args[] = {&a};
-            if (cudaLaunchCooperativeKernel((void *)k_cgs2_fused<true>, grid, kThreads, args, smem, s) != cudaSuccess)
-                return false;
-            count_launch();
-            return true;
+            if (bps >= 1) {
+                const int grid = (int)std::min<int64_t>(nb, (N + rpb - 1) / rpb);
+                void *args[] = {&a};
+                if (cudaLaunchCooperativeKernel((void *)k_cgs2_fused<true>, grid, kThreads, args, smem, s) ==
+                    cudaSuccess) {
+                    count_launch();
+                    return true;
+                }
+                cudaGetLastError();  // clear, fall through to the streaming kernel
+            }
         }
+        if (pol == 2) return false;
     }
-    // streaming mode (tall bases): cp.async row tiles through shared memory;
-    // a pending dense reduction is finished first (the tiles read w from HBM)
+    // streaming mode (tall bases): row tiles through shared memory; a pending
+    // dense reduction is finished first (the tiles read w from HBM)
     if (fs.pre) split_reduce(N, *fs.pre, w, ctrl ? &ctrl->abort : nullptr, s);
     const bool aligned = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
@@ -1967,34 +1647,61 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     sa.check = check;
     sa.pre_h = pre_h;
     sa.snake = 1;
-    if (const char *e = getenv("SVDSC_SNAKE")) sa.snake = atoi(e);
-    {
-        const char *kt = getenv("SVDSC_KTIMING");
-        if (kt && kt[0] == '1') {
-            if (!g_ktbuf) {
-                cudaMalloc(&g_ktbuf, 16 * sizeof(unsigned long long));
-                cudaMemset(g_ktbuf, 0, 16 * sizeof(unsigned long long));
-                // SVDSC_KTIMING_MIN_N / _MIN_COLS: only calls at least this large are timed
-                unsigned long long flt[2] = {0, 0};
-                if (const char *e = getenv("SVDSC_KTIMING_MIN_COLS")) flt[0] = strtoull(e, nullptr, 10);
-                if (const char *e = getenv("SVDSC_KTIMING_MIN_N")) flt[1] = strtoull(e, nullptr, 10);
-                cudaMemcpy(g_ktbuf + 14, flt, sizeof(flt), cudaMemcpyHostToDevice);
-            }
-            sa.tdbg = g_ktbuf;
-        }
+    sa.phase = 0;
+    if (pol == 4) return tmap && launch_tma_any(*reinterpret_cast<const CUtensorMap *>(tmap), sa, nsm, s);
+    // cp.async register-blocked streaming (measured faster than the TMA variant
+    // by 5-10 %); bases wider than its shared-memory ring (about
+    // 860 columns) fall back to the split kernels
+    return launch_stream2_any(sa, nsm, s);
+}
+
+// Multi-GPU CGS2 (P > 1): the streaming kernel in three launches, split at its
+// two reductions, with the cross-rank all-reduces of h1 and [h2; ||w'||^2]
+// between them (SURVEY.md 8(e) collectives 2-3 / 5-6).  Each CTA reduction is
+// finished on the device, so the all-reduce moves ncols (+1) doubles per rank.
+// false: not applicable (caller uses the split sweeps).
+bool cgs2_phased(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
+                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
+                 Comm *comm, unsigned int *launches) {
+    if (g_policy.cgs2 == 1) return false;
+    const bool aligned = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    if (!aligned || N < 1) return false;
+    if (ncols > 840) return false;  // wider than the streaming kernel's shared-memory ring
+    SArgs sa{};
+    sa.N = N;
+    sa.ncols = ncols;
+    sa.Q = Q;
+    sa.ldq = ldq;
+    sa.w = w;
+    sa.partial = fs.partial;
+    sa.PS = ncols + 2;
+    sa.h1 = fs.h1;
+    sa.h2 = fs.h2;
+    sa.h3 = fs.h3;
+    sa.flags = fs.flags;
+    sa.gate = nullptr;
+    sa.ctrl = ctrl;
+    sa.t_entry = t_entry;
+    sa.check = check;
+    sa.snake = 1;
+    auto launch = [&](int phase) {
+        sa.phase = phase;
+        sa.epoch = 16u * (++*launches);
+        sa.pre_h = phase == 1 ? pre_h : nullptr;
+        if (!launch_stream2_any(sa, nsm, s))
+            throw CommError(SVDSC_ECUDA, "multi-GPU CGS2: streaming kernel launch failed");
+    };
+    if (ncols > 0) {
+        launch(1);
+        comm->allreduce_sum(fs.h1, (size_t)ncols, s);
+    } else if (pre_h) {
+        return false;
     }
-    // deepest pipeline that fits: RT = 32 rows with 4, 3, 2 stages, then 16 and 8 rows
-    const char *sv = getenv("SVDSC_STREAM_VARIANT");
-    const int var = sv ? atoi(sv) : 2;  // default: register-blocked cp.async (measured fastest, tools/time_ops.py)
-    if (var == 0 && tmap && launch_tma_any(*reinterpret_cast<const CUtensorMap *>(tmap), sa, nsm, s)) return true;
-    if ((var == 0 || var == 2) && launch_stream2_any(sa, nsm, s)) return true;
-    if (var == 1 && launch_stream<16, 512, 4>(sa, nsm, s)) return true;
-    if (launch_stream<32, 512, 4>(sa, nsm, s)) return true;
-    if (launch_stream<32, 512, 3>(sa, nsm, s)) return true;
-    if (launch_stream<32, 512, 2>(sa, nsm, s)) return true;
-    if (launch_stream<16, 512, 2>(sa, nsm, s)) return true;
-    if (launch_stream<8, 512, 2>(sa, nsm, s)) return true;
-    return false;
+    launch(2);
+    comm->allreduce_sum(fs.h2, (size_t)ncols + 1, s);
+    launch(3);
+    return true;
 }
 
 }  // namespace svdsc

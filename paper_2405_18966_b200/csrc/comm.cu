@@ -1,0 +1,283 @@
+// comm.cu -- collectives of the row-partitioned multi-GPU solve (SURVEY.md
+// 8(e); BASELINE.json north_star (e): all-gather of v, reduce of the partial
+// A^T u, all-reduce of the Gram-Schmidt coefficient vectors).
+//
+// Two backends behind one interface (internal.h `Comm`):
+//   * NCCL (one process per GPU, NVLink / NVSwitch), loaded with dlopen so the
+//     library has no link-time NCCL dependency; every collective is enqueued on
+//     the solve's stream.
+//   * loopback: the ranks are threads of ONE process, each with its own handle
+//     and stream (same or different devices).  Every collective synchronizes
+//     the caller's stream, meets the other ranks at a host barrier and moves
+//     the data with plain copies / a fixed-order summation kernel, so the
+//     library's multi-rank host logic (partition, slicing, collective order,
+//     status agreement) runs on a single GPU.  No kernel ever waits on another
+//     rank's kernel.  Sums are over ranks 0..P-1 in order: every rank gets
+//     bitwise identical results.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace svdsc {
+
+// ---------------------------------------------------------------------------
+// NCCL (runtime-loaded)
+namespace {
+typedef struct ncclComm *ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0, kNcclMin = 3;
+
+struct Nccl {
+    bool tried = false, ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+bool nccl_load() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+#define SYM(name, field) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(lib, name))
+    SYM("ncclGetUniqueId", GetUniqueId);
+    SYM("ncclCommInitRank", CommInitRank);
+    SYM("ncclCommDestroy", CommDestroy);
+    SYM("ncclCommAbort", CommAbort);
+    SYM("ncclAllReduce", AllReduce);
+    SYM("ncclReduceScatter", ReduceScatter);
+    SYM("ncclAllGather", AllGather);
+    SYM("ncclGetErrorString", GetErrorString);
+#undef SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
+                g_nccl.AllGather;
+    return g_nccl.ok;
+}
+
+void ckn(ncclResult_t r, const char *what) {
+    if (r != 0)
+        throw CommError(SVDSC_ENCCL, std::string(what) + ": " +
+                                         (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
+}
+void ckc(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw CommError(SVDSC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct NcclComm : Comm {
+    ncclComm_t c = nullptr;
+    int *dint = nullptr;
+    ~NcclComm() override {
+        if (dint) cudaFree(dint);
+        if (c && g_nccl.CommDestroy) g_nccl.CommDestroy(c);
+    }
+    void allreduce_sum(double *buf, size_t n, cudaStream_t s) override {
+        ckn(g_nccl.AllReduce(buf, buf, n, kNcclFloat64, kNcclSum, c, s), "ncclAllReduce");
+    }
+    void reduce_scatter_sum(const double *in, double *out, size_t n_each, cudaStream_t s) override {
+        ckn(g_nccl.ReduceScatter(in, out, n_each, kNcclFloat64, kNcclSum, c, s), "ncclReduceScatter");
+    }
+    void allgather(const double *in, double *out, size_t n_each, cudaStream_t s) override {
+        ckn(g_nccl.AllGather(in, out, n_each, kNcclFloat64, c, s), "ncclAllGather");
+    }
+    int allreduce_min_int(int v, cudaStream_t s) override {
+        if (!dint) ckc(cudaMalloc(&dint, sizeof(int)), "cudaMalloc");
+        ckc(cudaMemcpyAsync(dint, &v, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+        ckn(g_nccl.AllReduce(dint, dint, 1, kNcclInt32, kNcclMin, c, s), "ncclAllReduce(min)");
+        int r = 0;
+        ckc(cudaMemcpyAsync(&r, dint, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+        ckc(cudaStreamSynchronize(s), "sync");
+        return r;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// loopback
+constexpr int kMaxLoopRanks = 16;
+struct RankPtrs {
+    const double *p[kMaxLoopRanks];
+};
+
+// out[i] = sum_{q < P} p[q][off + i], q ascending (fixed order)
+__global__ void k_sum_ranks(RankPtrs rp, int P, size_t off, size_t n, double *out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < P; q++) s += rp.p[q][off + i];
+        out[i] = s;
+    }
+}
+}  // namespace
+
+struct LoopbackGroup {
+    int P = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool failed = false;
+    int refs = 1;  // the creator's reference + one per attached rank
+    std::vector<const double *> ptr;
+    std::vector<int> ival;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (failed) throw CommError(SVDSC_ECUDA, "loopback group: another rank failed");
+        const uint64_t g = gen;
+        if (++arrived == P) {
+            arrived = 0;
+            gen++;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g || failed; });
+            if (failed && gen == g) throw CommError(SVDSC_ECUDA, "loopback group: another rank failed");
+        }
+    }
+    void fail() {
+        std::lock_guard<std::mutex> lk(mu);
+        failed = true;
+        cv.notify_all();
+    }
+};
+
+namespace {
+struct LoopbackComm : Comm {
+    LoopbackGroup *g;
+    double *tmp = nullptr;
+    size_t tmp_n = 0;
+    explicit LoopbackComm(LoopbackGroup *grp) : g(grp) {}
+    ~LoopbackComm() override {
+        if (tmp) cudaFree(tmp);
+        loopback_group_release(g);
+    }
+    RankPtrs ptrs() const {
+        RankPtrs r{};
+        for (int q = 0; q < nranks; q++) r.p[q] = g->ptr[q];
+        return r;
+    }
+    void sum_into(size_t off, size_t n, double *out, cudaStream_t s) {
+        if (n == 0) return;
+        const int blocks = (int)std::min<size_t>(1184, (n + 255) / 256);
+        k_sum_ranks<<<blocks, 256, 0, s>>>(ptrs(), nranks, off, n, out);
+        count_launch();
+        ckc(cudaGetLastError(), "k_sum_ranks");
+    }
+    void publish(const double *p, cudaStream_t s) {
+        ckc(cudaStreamSynchronize(s), "sync");  // p's producer is complete
+        g->ptr[rank] = p;
+        g->barrier();
+    }
+    void allreduce_sum(double *buf, size_t n, cudaStream_t s) override {
+        if (n > tmp_n) {
+            if (tmp) cudaFree(tmp);
+            tmp = nullptr;
+            ckc(cudaMalloc(&tmp, n * sizeof(double)), "cudaMalloc");
+            tmp_n = n;
+        }
+        publish(buf, s);
+        sum_into(0, n, tmp, s);
+        ckc(cudaStreamSynchronize(s), "sync");
+        g->barrier();  // every rank has read every buffer
+        ckc(cudaMemcpyAsync(buf, tmp, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
+    }
+    void reduce_scatter_sum(const double *in, double *out, size_t n_each, cudaStream_t s) override {
+        publish(in, s);
+        sum_into((size_t)rank * n_each, n_each, out, s);
+        ckc(cudaStreamSynchronize(s), "sync");
+        g->barrier();
+    }
+    void allgather(const double *in, double *out, size_t n_each, cudaStream_t s) override {
+        publish(in, s);
+        for (int q = 0; q < nranks; q++)
+            ckc(cudaMemcpyAsync(out + (size_t)q * n_each, g->ptr[q], n_each * sizeof(double), cudaMemcpyDefault, s),
+                "allgather copy");
+        ckc(cudaStreamSynchronize(s), "sync");
+        g->barrier();
+    }
+    int allreduce_min_int(int v, cudaStream_t) override {
+        g->ival[rank] = v;
+        g->barrier();
+        int m = v;
+        for (int q = 0; q < nranks; q++) m = std::min(m, g->ival[q]);
+        g->barrier();
+        return m;
+    }
+    void abort() override { g->fail(); }
+};
+}  // namespace
+
+bool comm_nccl_available() { return nccl_load(); }
+
+void comm_nccl_unique_id(unsigned char id[128]) {
+    if (!nccl_load()) throw CommError(SVDSC_ENCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId u;
+    ckn(g_nccl.GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, u.internal, 128);
+}
+
+Comm *comm_nccl_create(const unsigned char id[128], int nranks, int rank) {
+    if (!nccl_load()) throw CommError(SVDSC_ENCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    NcclComm *c = new NcclComm();
+    c->nranks = nranks;
+    c->rank = rank;
+    const ncclResult_t r = g_nccl.CommInitRank(&c->c, nranks, u, rank);
+    if (r != 0) {
+        c->c = nullptr;
+        delete c;
+        ckn(r, "ncclCommInitRank");
+    }
+    return c;
+}
+
+LoopbackGroup *loopback_group_create(int nranks) {
+    if (nranks < 1 || nranks > kMaxLoopRanks) return nullptr;
+    LoopbackGroup *g = new LoopbackGroup();
+    g->P = nranks;
+    g->ptr.assign(nranks, nullptr);
+    g->ival.assign(nranks, 0);
+    return g;
+}
+
+void loopback_group_release(LoopbackGroup *g) {
+    if (!g) return;
+    bool del = false;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        del = --g->refs == 0;
+    }
+    if (del) delete g;
+}
+
+Comm *comm_loopback_create(LoopbackGroup *g, int rank) {
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->refs++;
+    }
+    LoopbackComm *c = new LoopbackComm(g);
+    c->nranks = g->P;
+    c->rank = rank;
+    return c;
+}
+
+}  // namespace svdsc

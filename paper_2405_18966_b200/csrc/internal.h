@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -27,6 +28,7 @@ struct Ctrl {
     double inv;           // 1 / norm of the vector being normalized
     int abort;            // != 0: breakdown pending; step kernels are no-ops
     int abort_check;      // check index that broke down
+    int abort_kind;       // 0 breakdown (reading Q7); 1 explicit norm needed (multi-GPU CGS2, reading G1)
     int svd_status;       // 0 ok, SVDSC_ESVD_NOCONV
     int svd_sweeps;
     int converged;
@@ -35,8 +37,6 @@ struct Ctrl {
     double svd_tiny;      // p eps ||T||_F: numerically zero column norm (reading Q10b)
     unsigned int cnt[16]; // last-block counters (one per reduction site)
     unsigned int gflags[kMaxBlocks];  // grid-barrier flags of the fused kernels
-
-
     // partial re-orthogonalization (reorth = 1, pro.cu)
     int pro_gate;                     // 1: the current half-step re-orthogonalizes
     int pro_force[2];                 // V / U side: next vector re-orthogonalized regardless
@@ -68,16 +68,6 @@ struct CsrOp {
     int64_t n_span = 0;                // rows spanning tile boundaries
     int32_t *span_row = nullptr, *span_t0 = nullptr, *span_t1 = nullptr;  // row, first and last tile
     bool merge = false;                // use the merge schedule for this operand
-    // column-blocked copy (matvec.cu, "cb"): columns split into cb_nb blocks of
-    // kCbW; segment s = b * nrows + r holds row r's entries of block b, in row
-    // order, with 16-bit block-local column indices; x's block is staged in
-    // shared memory, so the gathers never leave the SM
-    int cb_nb = 0, cb_tasks = 0, cb_G = 0;
-    int32_t *cb_ptr = nullptr;         // cb_nb * nrows + 1 segment offsets
-    uint16_t *cb_col = nullptr;        // nnz
-    double *cb_val = nullptr;          // nnz
-    int32_t *cb_tb = nullptr;          // cb_tasks + 1 segment boundaries, one task per CTA
-    double *cb_part = nullptr;         // cb_nb * nrows partial row sums (cb_nb > 1)
     std::vector<void *> owned;         // allocations owned by this operand
 };
 constexpr int kMergeTile = 2048;       // nonzeros per merge tile (256 threads x 8)
@@ -165,13 +155,18 @@ struct FusedScratch {
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
                 const void *tmap);
+struct Comm;
+// P > 1: the streaming CGS2 in three launches with the cross-rank all-reduces of
+// h1 and [h2; ||w'||^2] between them; *launches is the per-solve fused-launch
+// counter (grid-barrier slot chain).  false: not applicable.
+bool cgs2_phased(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
+                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
+                 Comm *comm, unsigned int *launches);
 // TMA descriptor of a column-major basis (N rows, ncols_total columns, ld):
 // 16 x 16 boxes, SWIZZLE_128B, zero fill beyond N.  Returns false if the
 // driver entry point is unavailable.
 bool make_basis_tmap(void *map128, const double *base, int64_t N, int64_t ncols_total, int64_t ld);
 
-
-void ktiming_dump();  // SVDSC_KTIMING=1 debugging aid
 
 // partial re-orthogonalization (pro.cu; Q20).  mu/nu: device rows of
 // length t+2; part: >= nsm doubles of scratch.  pro_decide writes
@@ -201,6 +196,41 @@ void recombine(int64_t N, int t, int k, const double *Q, int64_t ldq, const doub
                double *Qout, int64_t ldo, int nsm, cudaStream_t s);
 void copy_col(int64_t N, const double *src, double *dst, cudaStream_t s);
 void fill_zero(double *p, int64_t n, cudaStream_t s);
+
+// ---- collectives of the row-partitioned solve (comm.cu) ---------
+struct CommError : std::runtime_error {
+    svdsc_status st;
+    CommError(svdsc_status s, const std::string &m) : std::runtime_error(m), st(s) {}
+};
+struct Comm {
+    int nranks = 1, rank = 0;
+    virtual ~Comm() {}
+    // enqueued on s (NCCL) or completed before return (loopback)
+    virtual void allreduce_sum(double *buf, size_t n, cudaStream_t s) = 0;
+    virtual void reduce_scatter_sum(const double *in, double *out, size_t n_each, cudaStream_t s) = 0;
+    virtual void allgather(const double *in, double *out, size_t n_each, cudaStream_t s) = 0;
+    // blocking: the minimum of v over the ranks (status agreement before compute)
+    virtual int allreduce_min_int(int v, cudaStream_t s) = 0;
+    virtual void abort() {}  // a rank failed mid-solve: release the others (loopback)
+};
+bool comm_nccl_available();
+void comm_nccl_unique_id(unsigned char id[128]);
+Comm *comm_nccl_create(const unsigned char id[128], int nranks, int rank);
+struct LoopbackGroup;
+LoopbackGroup *loopback_group_create(int nranks);
+void loopback_group_release(LoopbackGroup *g);
+Comm *comm_loopback_create(LoopbackGroup *g, int rank);
+
+// ---- kernel-schedule policy (svdsc_set_policy, include/svdsc.h) -----------------
+// 0 everywhere = automatic choice by shape (the product default).  Set per call
+// from the handle (thread-local: distinct handles on distinct threads are
+// independent); tests use it to run every schedule the automatic choice may pick.
+struct Policy {
+    int spmv = 0;       // SVDSC_POLICY_SPMV
+    int cgs2 = 0;       // SVDSC_POLICY_CGS2
+    int small_svd = 0;  // SVDSC_POLICY_SMALL_SVD
+};
+extern thread_local Policy g_policy;
 
 // ---- launch bookkeeping ----------------------------------------------------------
 extern thread_local int64_t g_launches;

@@ -29,6 +29,7 @@
 namespace svdsc {
 
 thread_local int64_t g_launches = 0;
+thread_local Policy g_policy;
 
 namespace {
 
@@ -520,176 +521,6 @@ __global__ void k_csc_gather(int64_t nnz, const uint64_t *__restrict__ key, cons
     }
 }
 
-// ---- column-blocked SpMV ("cb", opt-in: SVDSC_SPMV=cb) --------------------
-// For operands whose x is reused (nnz / ncols >= 8) and spans at most
-// kCbMaxBlocks blocks of kCbW columns: the random gathers x[col] of the row
-// kernels go to L2 in 32-byte sectors for 8 useful bytes (ncu, config 3: DRAM
-// 27 %, L2 59 %, L1 72 % busy).  Here each CTA stages one block of x (192 KB)
-// in shared memory and streams the block's row segments: gathers are shared-
-// memory loads, the matrix is read once with 10 B per nonzero (16-bit local
-// column), and the per-block partial row sums are added in block order by
-// k_cb_reduce (deterministic; the epilogue - c yprev is fused there, or in the
-// main kernel when there is a single block).
-#ifndef SVDSC_CB_W
-#define SVDSC_CB_W 24576
-#define SVDSC_CB_MB 16
-#endif
-#ifndef SVDSC_CB_THREADS
-#define SVDSC_CB_THREADS 1024
-#endif
-#ifndef SVDSC_CB_LD
-#define SVDSC_CB_LD 0
-#endif
-constexpr int kCbW = SVDSC_CB_W;
-constexpr int kCbMaxBlocks = SVDSC_CB_MB;
-constexpr int kCbThreads = SVDSC_CB_THREADS;
-template <typename T>
-__device__ __forceinline__ T cb_ld(const T *p) {
-#if SVDSC_CB_LD == 1
-    return __ldg(p);
-#elif SVDSC_CB_LD == 2
-    return __ldcg(p);
-#else
-    return __ldcs(p);
-#endif
-}
-
-// warp per row: per-block counts of the row's entries (ballot + popc)
-__global__ void k_cb_count(int64_t nrows, int nb, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                           int32_t *len /* nb * nrows + 1, entry b * nrows + r + 1 */) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = w0; r < nrows; r += nw) {
-        int cnt[kCbMaxBlocks];
-#pragma unroll
-        for (int b = 0; b < kCbMaxBlocks; b++) cnt[b] = 0;
-        for (int64_t p = rp[r]; p < rp[r + 1]; p += 32) {
-            const int64_t q = p + lane;
-            const int blk = q < rp[r + 1] ? col[q] / kCbW : -1;
-#pragma unroll
-            for (int b = 0; b < kCbMaxBlocks; b++) cnt[b] += __popc(__ballot_sync(0xffffffffu, blk == b));
-        }
-        if (lane < nb) {
-            int c = 0;
-#pragma unroll
-            for (int b = 0; b < kCbMaxBlocks; b++) c = (b == lane) ? cnt[b] : c;
-            len[(int64_t)lane * nrows + r + 1] = c;
-        }
-    }
-}
-
-// warp per row: scatter the row's entries to their block segments, keeping
-// the row order inside every segment
-__global__ void k_cb_fill(int64_t nrows, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                          const double *__restrict__ val, const int32_t *__restrict__ ptr, uint16_t *ccol,
-                          double *cval) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int64_t r = w0; r < nrows; r += nw) {
-        int base[kCbMaxBlocks];
-#pragma unroll
-        for (int b = 0; b < kCbMaxBlocks; b++) base[b] = 0;
-        for (int64_t p = rp[r]; p < rp[r + 1]; p += 32) {
-            const int64_t q = p + lane;
-            const bool ok = q < rp[r + 1];
-            const int c = ok ? col[q] : 0;
-            const int blk = ok ? c / kCbW : -1;
-#pragma unroll
-            for (int b = 0; b < kCbMaxBlocks; b++) {
-                const unsigned m = __ballot_sync(0xffffffffu, blk == b);
-                if (blk == b) {
-                    const int64_t pos = (int64_t)ptr[(int64_t)b * nrows + r] + base[b] + __popc(m & lt);
-                    ccol[pos] = (uint16_t)(c - b * kCbW);
-                    cval[pos] = val[q];
-                }
-                base[b] += __popc(m);
-            }
-        }
-    }
-}
-
-struct CbArgs {
-    int64_t nrows, ncols;
-    int nb;
-    const int32_t *ptr;
-    const uint16_t *col;
-    const double *val;
-    const int32_t *tb;
-    const double *x;
-    double *y;      // nb == 1: the output (epilogue fused)
-    double *part;   // nb > 1: per-segment partial sums
-    const double *c_dev, *yprev;
-    const int *abort;
-};
-
-template <int G, int kU>
-__global__ void __launch_bounds__(kCbThreads) k_spmv_cb(CbArgs a) {
-    if (aborted(a.abort)) return;
-    extern __shared__ double xs[];
-    constexpr int GPW = 32 / G;
-    constexpr int NWARP = kCbThreads / 32;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane % G;
-    // CTAs [tb[b], tb[b+1]) serve column block b (counts proportional to its
-    // nonzeros); their warps interleave over the block's row segments, so the
-    // whole grid streams neighbouring addresses (as the row kernels do)
-    int b = 0;
-    while (b + 1 < a.nb && (int)blockIdx.x >= a.tb[b + 1]) b++;
-    const int c_first = a.tb[b], nct = a.tb[b + 1] - c_first;
-    if (nct <= 0) return;
-    const double c = a.c_dev ? *a.c_dev : 0.0;
-    const int64_t c0 = (int64_t)b * kCbW;
-    const int w = (int)min((int64_t)kCbW, a.ncols - c0);
-    for (int j = threadIdx.x; j < w; j += kCbThreads) xs[j] = __ldg(a.x + c0 + j);
-    __syncthreads();
-    const int64_t seg0 = (int64_t)b * a.nrows, seg1 = seg0 + a.nrows;
-    const int64_t gw = (int64_t)(blockIdx.x - c_first) * NWARP + wid, nw = (int64_t)nct * NWARP;
-    for (int64_t base = seg0 + gw * GPW; base < seg1; base += nw * GPW) {
-        const int64_t seg = base + lane / G;
-        double s0 = 0.0, s1 = 0.0;
-        if (seg < seg1) {
-            const int64_t p0 = a.ptr[seg], p1 = a.ptr[seg + 1];
-            for (int64_t p = p0 + sub; p < p1; p += G * kU) {
-                int ci[kU];
-                double vv[kU];
-#pragma unroll
-                for (int u = 0; u < kU; u++) {
-                    const int64_t q = p + (int64_t)u * G;
-                    const bool ok = q < p1;
-                    ci[u] = ok ? (int)cb_ld(a.col + q) : 0;
-                    vv[u] = ok ? cb_ld(a.val + q) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < kU; u++) {
-                    if (u & 1) s1 = fma(vv[u], xs[ci[u]], s1);
-                    else s0 = fma(vv[u], xs[ci[u]], s0);
-                }
-            }
-        }
-        double sum = s0 + s1;
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, G);
-        if (sub == 0 && seg < seg1) {
-            if (a.nb == 1) epilogue_store(a.y, seg - seg0, sum, c, a.yprev);
-            else a.part[seg] = sum;
-        }
-    }
-}
-
-// y[r] = sum_b part[b * nrows + r] (b ascending) - c yprev[r]
-__global__ void k_cb_reduce(int64_t nrows, int nb, const double *__restrict__ part, double *y, const double *c_dev,
-                            const double *__restrict__ yprev, const int *abort) {
-    if (aborted(abort)) return;
-    const double c = c_dev ? *c_dev : 0.0;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nb; b++) s += __ldcs(part + (int64_t)b * nrows + r);
-        epilogue_store(y, r, s, c, yprev);
-    }
-}
-
 inline void check(cudaError_t e, const char *what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -783,13 +614,14 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
     // nnz-balanced merge schedule for operands with long rows (CTA-per-row and
     // chunked bins non-empty: power-law rows), where the binned launches
     // serialize and imbalance; measured 21% faster there (config 4), 35% slower
-    // on uniform rows (config 3).  SVDSC_SPMV=merge|bins forces either.
+    // on uniform rows (config 3).  Policy SVDSC_POLICY_SPMV (1 bins, 2 merge)
+    // forces either.
     {
-        const char *sv = getenv("SVDSC_SPMV");
         const bool aligned = ((reinterpret_cast<uintptr_t>(op.col) & 31) == 0) &&
                              ((reinterpret_cast<uintptr_t>(op.val) & 63) == 0);
         const bool long_rows = off[7] > off[5];
-        const bool want = sv ? std::string(sv) == "merge" : long_rows;
+        const int pol = g_policy.spmv;
+        const bool want = pol == 2 ? true : (pol == 1 ? false : long_rows);
         if (op.nnz > 0 && op.nrows < (int64_t)INT32_MAX && aligned && want) {
             const int64_t nt = (op.nnz + kMergeTile - 1) / kMergeTile;
             op.n_tiles = nt;
@@ -839,64 +671,6 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
             }
             check(cudaMemcpyAsync(op.tile_r1, r1.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
             op.merge = true;
-        }
-    }
-    // column-blocked copy (k_spmv_cb), opt-in with SVDSC_SPMV=cb where x is
-    // reused and spans few blocks: correct (parity-tested) but measured 5x
-    // SLOWER than the row bins at config 3 -- kept for the
-    // investigation, not used by default
-    {
-        const char *sv = getenv("SVDSC_SPMV");
-        const bool want = sv && std::string(sv) == "cb";
-        const int nb = (int)((op.ncols + kCbW - 1) / kCbW);
-        const bool ok = want && !op.merge && off[7] == off[5] && op.nrows > 0 && op.ncols > 0 &&
-                        nb <= kCbMaxBlocks && op.nnz >= 8 * op.ncols && op.nnz < (int64_t)INT32_MAX &&
-                        (int64_t)nb * op.nrows < (int64_t)INT32_MAX;
-        if (ok) {
-            int dev = 0, nsm = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            const int64_t nseg = (int64_t)nb * op.nrows;
-            op.cb_nb = nb;
-            op.cb_tasks = nsm;
-            op.cb_ptr = dev_alloc<int32_t>(op, nseg + 1);
-            op.cb_col = dev_alloc<uint16_t>(op, op.nnz);
-            op.cb_val = dev_alloc<double>(op, op.nnz);
-            op.cb_tb = dev_alloc<int32_t>(op, nb + 1);
-            if (nb > 1) op.cb_part = dev_alloc<double>(op, nseg);
-            check(cudaMemsetAsync(op.cb_ptr, 0, (nseg + 1) * sizeof(int32_t), s), "memset");
-            k_cb_count<<<grid_for(op.nrows * 32, 256), 256, 0, s>>>(op.nrows, nb, op.row_ptr, op.col, op.cb_ptr);
-            void *tmp = nullptr;
-            size_t tmp_bytes = 0;
-            check(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, op.cb_ptr, op.cb_ptr, (int)(nseg + 1), s),
-                  "scan size");
-            check(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)), "cudaMalloc");
-            check(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, op.cb_ptr, op.cb_ptr, (int)(nseg + 1), s), "scan");
-            k_cb_fill<<<grid_for(op.nrows * 32, 256), 256, 0, s>>>(op.nrows, op.row_ptr, op.col, op.val, op.cb_ptr,
-                                                                   op.cb_col, op.cb_val);
-            check(cudaStreamSynchronize(s), "sync");
-            cudaFree(tmp);
-            {  // CTAs per column block, proportional to its nonzeros, >= 1 each
-                std::vector<int32_t> bp(nb + 1);
-                for (int q = 0; q <= nb; q++)
-                    check(cudaMemcpy(&bp[q], op.cb_ptr + (int64_t)q * op.nrows, sizeof(int32_t),
-                                     cudaMemcpyDeviceToHost), "D2H");
-#ifndef SVDSC_CB_CPS
-#define SVDSC_CB_CPS 1
-#endif
-                const int T = std::max(nsm * SVDSC_CB_CPS, nb);  // CTAs per SM (1024 threads: 1)
-                std::vector<int32_t> tb(nb + 1);
-                tb[0] = 0;
-                for (int q = 0; q < nb; q++) {
-                    const int64_t want = (int64_t)llround((double)T * bp[q + 1] / std::max<int64_t>(op.nnz, 1));
-                    tb[q + 1] = (int32_t)std::max<int64_t>(tb[q] + 1, std::min<int64_t>(want, T - (nb - 1 - q)));
-                }
-                tb[nb] = T;
-                op.cb_tasks = T;
-                check(cudaMemcpy(op.cb_tb, tb.data(), (nb + 1) * sizeof(int32_t), cudaMemcpyHostToDevice), "H2D");
-            }
-            const double L = (double)op.nnz / (double)nseg;  // mean segment length
-            op.cb_G = L <= 16.0 ? 4 : (L <= 48.0 ? 8 : 16);
         }
     }
     check(cudaStreamSynchronize(s), "sync");
@@ -968,33 +742,8 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
     csr_analyze(at, s);
 }
 
-namespace {
-template <int G>
-void launch_cb(const CsrOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
-               const int *abort, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_spmv_cb<G, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbW * 8);
-        attr = true;
-    }
-    CbArgs a{A.nrows, A.ncols, A.cb_nb, A.cb_ptr, A.cb_col, A.cb_val, A.cb_tb, x, y, A.cb_part, c_dev, yprev, abort};
-    k_spmv_cb<G, 4><<<A.cb_tasks, kCbThreads, kCbW * 8, s>>>(a);
-    count_launch();
-}
-}  // namespace
-
 void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
               const int *abort, cudaStream_t s) {
-    if (A.cb_nb > 0) {
-        if (A.cb_G == 4) launch_cb<4>(A, x, y, c_dev, yprev, abort, s);
-        else if (A.cb_G == 8) launch_cb<8>(A, x, y, c_dev, yprev, abort, s);
-        else launch_cb<16>(A, x, y, c_dev, yprev, abort, s);
-        if (A.cb_nb > 1) {
-            k_cb_reduce<<<grid_for(A.nrows, 256), 256, 0, s>>>(A.nrows, A.cb_nb, A.cb_part, y, c_dev, yprev, abort);
-            count_launch();
-        }
-        return;
-    }
     if (A.merge) {
         k_spmv_merge<<<(unsigned)A.n_tiles, 256, 0, s>>>(A.nnz, A.tile_r0, A.tile_r1, A.row_ptr, A.col, A.val, x, y,
                                                          c_dev, yprev, A.tile_head, A.tile_tail, abort);
@@ -1024,8 +773,6 @@ void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, c
             int bps = 0, dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            if (const char *co = getenv("SVDSC_CARVEOUT"))  // experiment: shared-memory carveout of the SpMV
-                cudaFuncSetAttribute(k_spmv_bins, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_bins, 256, 0);
             wave = std::max(1, bps) * nsm;
         }
@@ -1122,64 +869,6 @@ __global__ void __launch_bounds__(256) k_gemv_n(int64_t m, int64_t n, const doub
     }
 }
 
-// y_partial[split][c] = sum over rows of split of A[r,c] x[r]; each warp owns
-// 4 adjacent columns, so every x value loaded (128-bit, L1) serves 4 columns of
-// A (one 128-bit streaming load each): x traffic per A byte drops 4x.
-__global__ void __launch_bounds__(256) k_gemv_t4(int64_t m, int64_t n, const double *__restrict__ A, int64_t ld,
-                                                 const double *__restrict__ x, double *partial, int64_t rows_per_split,
-                                                 const int *abort) {
-    if (aborted(abort)) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t c0 = (blockIdx.x * 8ll + w) * 4;
-    const int64_t r0 = blockIdx.y * rows_per_split;
-    const int64_t r1 = min(m, r0 + rows_per_split);
-    if (c0 >= n) return;
-    const int nc = (int)min((int64_t)4, n - c0);
-    const double *col[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) col[q] = A + min(c0 + q, n - 1) * ld;  // clamped: extra columns unused
-    double acc[4][2];
-#pragma unroll
-    for (int q = 0; q < 4; q++) acc[q][0] = acc[q][1] = 0.0;
-    int64_t r = r0 + 2 * lane;
-    for (; r + 64 * 3 + 1 < r1; r += 64 * 4) {
-        double2 v[4][4], xv[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            xv[u] = __ldg(reinterpret_cast<const double2 *>(x + r + 64 * u));
-#pragma unroll
-            for (int q = 0; q < 4; q++) v[q][u] = __ldcs(reinterpret_cast<const double2 *>(col[q] + r + 64 * u));
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                acc[q][0] = fma(v[q][u].x, xv[u].x, acc[q][0]);
-                acc[q][1] = fma(v[q][u].y, xv[u].y, acc[q][1]);
-            }
-    }
-    for (; r + 1 < r1; r += 64) {
-        const double2 xv = __ldg(reinterpret_cast<const double2 *>(x + r));
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const double2 v = __ldcs(reinterpret_cast<const double2 *>(col[q] + r));
-            acc[q][0] = fma(v.x, xv.x, acc[q][0]);
-            acc[q][1] = fma(v.y, xv.y, acc[q][1]);
-        }
-    }
-    if (r < r1) {
-#pragma unroll
-        for (int q = 0; q < 4; q++) acc[q][0] = fma(col[q][r], x[r], acc[q][0]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-        double s = acc[q][0] + acc[q][1];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0 && q < nc) partial[blockIdx.y * n + c0 + q] = s;
-    }
-}
-
 // y_partial[split][c] = sum over rows of split of A[r,c] x[r]; warp per column.
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_gemv_t(int64_t m, int64_t n, const double *__restrict__ A, int64_t ld,
@@ -1265,13 +954,7 @@ void gemv_t(const DenseOp &A, const double *x, double *y, const double *c_dev, c
     rps = (rps + 1) & ~1ll;  // even, keeps 16-byte alignment of every split start
     const bool vec = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.data) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    // k_gemv_t4 (4 columns per warp) measured slower at config 2 (153 vs 127 us):
-    // opt-in experiment only (SVDSC_GEMV_T4=1)
-    const char *g4 = getenv("SVDSC_GEMV_T4");
-    if (vec && g4 && g4[0] == '1') {
-        dim3 grid((unsigned)((n + 31) / 32), (unsigned)splits);
-        k_gemv_t4<<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
-    } else {
+    {
         dim3 grid((unsigned)((n + 7) / 8), (unsigned)splits);
         if (vec) k_gemv_t<true><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);
         else k_gemv_t<false><<<grid, 256, 0, s>>>(m, n, A.data, A.ld, x, A.partial, rps, abort);

@@ -1004,6 +1004,7 @@ void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double
                int kneed, Ctrl *ctrl, const int *abort, double *tlog, cudaStream_t s) {
     k_copy_T<<<1, 1024, 0, s>>>(p, Tsrc, ldt, W, Vw, ctrl, abort);
     count_launch();
+    if (g_policy.small_svd == 1) tlog = nullptr;  // one-CTA Jacobi (SVDSC_POLICY_SMALL_SVD = 1)
     const double ctol = 2.0 * (double)p * 2.220446049250313e-16;  // reading Q10a
     bool done = false;
     int C, h;

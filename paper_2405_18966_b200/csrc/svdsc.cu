@@ -9,9 +9,11 @@
 //
 // Multi-GPU: A is row-partitioned; U rows follow A's rows;
 // V is split into equal slices of n_pad / P rows.  Per Lanczos step:
-// reduce-scatter of the partial A^T u, all-gather of v_{i+1}, and all-reduces
-// of the CGS2 coefficient vectors and of the squared norms (NCCL, loaded with
-// dlopen so the library itself has no link-time NCCL dependency).
+// reduce-scatter of the partial A^T u, all-gather of v_{i+1}, and two
+// all-reduces per re-orthogonalization (h1, then [h2; ||w'||^2]) between the
+// three launches of the streaming CGS2 kernel (comm.cu: NCCL, or the
+// in-process loopback backend).  Every rank agrees on the call's status
+// (all-reduce of min) before any compute.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdint.h>
@@ -30,48 +32,7 @@
 
 using namespace svdsc;
 
-// ---------------------------------------------------------------------------
-// NCCL (runtime-loaded)
 namespace {
-typedef struct ncclComm *ncclComm_t;
-typedef struct {
-    char internal[128];
-} ncclUniqueId;
-typedef int ncclResult_t;
-constexpr int kNcclFloat64 = 8, kNcclSum = 0;
-
-struct Nccl {
-    bool tried = false, ok = false;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*ReduceScatter)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    const char *(*GetErrorString)(ncclResult_t) = nullptr;
-};
-Nccl g_nccl;
-
-bool nccl_load() {
-    if (g_nccl.tried) return g_nccl.ok;
-    g_nccl.tried = true;
-    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) return false;
-#define SYM(name, field) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(lib, name))
-    SYM("ncclGetUniqueId", GetUniqueId);
-    SYM("ncclCommInitRank", CommInitRank);
-    SYM("ncclCommDestroy", CommDestroy);
-    SYM("ncclAllReduce", AllReduce);
-    SYM("ncclReduceScatter", ReduceScatter);
-    SYM("ncclAllGather", AllGather);
-    SYM("ncclGetErrorString", GetErrorString);
-#undef SYM
-    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
-                g_nccl.AllGather;
-    return g_nccl.ok;
-}
-
 struct SvdscError : std::runtime_error {
     svdsc_status st;
     SvdscError(svdsc_status s, const std::string &m) : std::runtime_error(m), st(s) {}
@@ -79,11 +40,6 @@ struct SvdscError : std::runtime_error {
 
 inline void ck(cudaError_t e, const char *what) {
     if (e != cudaSuccess) throw SvdscError(SVDSC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-inline void ckn(ncclResult_t r, const char *what) {
-    if (r != 0)
-        throw SvdscError(SVDSC_ENCCL, std::string(what) + ": " +
-                                          (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
 }
 inline void einval(bool bad, const std::string &m) {
     if (bad) throw SvdscError(SVDSC_EINVAL, m);
@@ -152,11 +108,19 @@ struct svdsc_handle {
     int device = 0, nsm = 148;
     cudaStream_t stream = nullptr;
     std::string err;
-    ncclComm_t comm = nullptr;
+    Comm *comm = nullptr;        // multi-rank collectives (comm.cu); NULL: single rank
     int nranks = 1, rank = 0;
+    Policy policy;               // kernel-schedule policy (svdsc_set_policy)
+    cudaMemPool_t pool = nullptr;  // private pool of the library's stream-ordered allocations
     Ctrl *hctrl = nullptr;       // pinned host mirror of the control block
     void *scratch = nullptr;     // op-level scratch
     size_t scratch_bytes = 0;
+};
+
+struct svdsc_group {
+    LoopbackGroup *g;
+    int P;
+    int nranks() const { return P; }
 };
 
 struct svdsc_matrix {
@@ -166,16 +130,21 @@ struct svdsc_matrix {
     CsrOp A, At;
     DenseOp D;
     double *dense_partial = nullptr;
+    double seconds_analysis = 0.0;  // host wall time of svdsc_matrix_* (validation, bins, CSC)
 };
 
 namespace {
 
 template <typename F>
 svdsc_status guarded(svdsc_handle *h, F &&f) {
+    if (h) g_policy = h->policy;
     try {
         f();
         return SVDSC_OK;
     } catch (const SvdscError &e) {
+        if (h) h->err = e.what();
+        return e.st;
+    } catch (const CommError &e) {
         if (h) h->err = e.what();
         return e.st;
     } catch (const std::exception &e) {
@@ -292,7 +261,14 @@ void check_opts(const svdsc_matrix *M, const svdsc_opts *o) {
     const int t = resolve_t(o, M->m_global, M->n);
     einval(t < o->k + 2, "subspace dimension t = min(max(15,3k), min(m,n)-1) < k+2 (SPEC.md:309)");
     einval(t > 1023, "t > 1023 is not supported");
-    einval(o->reorth < 0 || o->reorth > 2, "reorth must be 0, 1 or 2");
+    einval(o->reorth < -1 || o->reorth > 2, "reorth must be -1, 0, 1 or 2");
+}
+
+// stream-ordered allocation from the handle's private pool
+void *pool_alloc(svdsc_handle *H, size_t bytes, cudaStream_t s) {
+    void *p = nullptr;
+    ck(cudaMallocFromPoolAsync(&p, std::max<size_t>(bytes, 8), H->pool, s), "cudaMallocFromPoolAsync");
+    return p;
 }
 
 // ---------------------------------------------------------------------------
@@ -307,21 +283,21 @@ struct Solver {
     int t, k, P, rank, nsm;
     int64_t m, nv, n;
     const int *abort;
-    int64_t matvecs = 0, steps = 0, breakdowns = 0, bytes_model = 0;
+    int64_t matvecs = 0, steps = 0, breakdowns = 0, bytes_model = 0, bytes_reorth = 0;
     uint64_t bd_stream = 0;
     int check = 0;
     int64_t bytesA = 0;
 
     // ---- collectives (no-ops for P = 1) ----
     void allreduce(double *buf, size_t count) {
-        if (P > 1) ckn(g_nccl.AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, H->comm, s), "ncclAllReduce");
+        if (P > 1) H->comm->allreduce_sum(buf, count, s);
     }
 
     // z = A x - c zprev on the local rows (x = V column slice)
     void Av(const double *vcol, double *z, const double *c_dev, const double *zprev) {
         const double *x = vcol;
         if (P > 1) {
-            ckn(g_nccl.AllGather(vcol, w.vfull, (size_t)nv, kNcclFloat64, H->comm, s), "ncclAllGather");
+            H->comm->allgather(vcol, w.vfull, (size_t)nv, s);
             x = w.vfull;
         }
         H->prof.begin(0, s);
@@ -353,8 +329,7 @@ struct Solver {
         } else {
             if (M->kind == 0) spmv_csr(M->At, u, w.yfull, nullptr, nullptr, abort, s);
             else gemv_t(M->D, u, w.yfull, nullptr, nullptr, abort, s);
-            ckn(g_nccl.ReduceScatter(w.yfull, wcol, (size_t)nv, kNcclFloat64, kNcclSum, H->comm, s),
-                "ncclReduceScatter");
+            H->comm->reduce_scatter_sum(w.yfull, wcol, (size_t)nv, s);
             if (c_dev) axpy_dev(nv, wcol, c_dev, wprev, abort, s);
         }
         matvecs++;
@@ -401,6 +376,15 @@ struct Solver {
                 pending = PreReduce{};
                 return;
             }
+            fused_ok = false;
+        }
+        if (P > 1 && o->reorth != 0 && fused_ok) {
+            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 0u, nullptr};
+            H->prof.begin(11, s);
+            const bool ok = cgs2_phased(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s, H->comm,
+                                        &fused_launches);
+            H->prof.end(s);
+            if (ok) return;
             fused_ok = false;
         }
         finish_pending(N, wv);
@@ -450,6 +434,7 @@ struct Solver {
                 Av(Vcol(0), Ucol(0), nullptr, nullptr);
                 orth_norm(m, 0, w.U, w.ldu, Ucol(0), Tm(0, 0), chk, nullptr);
                 bytes_model += bytesA + 8 * m * 5;
+                bytes_reorth += 8 * m * 5;
                 break;
             case 1: {  // Alg. 1 lines 5-6 + re-orthogonalization
                 const int i = h.i;
@@ -462,6 +447,7 @@ struct Solver {
                 }
                 steps++;
                 bytes_model += bytesA + 8 * nv * (3 * (int64_t)i + 5);
+                if (o->reorth == 2) bytes_reorth += 8 * nv * (3 * (int64_t)i + 5);
                 break;
             }
             case 2: {  // Alg. 1 lines 7-8 + re-orthogonalization
@@ -474,11 +460,15 @@ struct Solver {
                     reorth_halves += o->reorth == 2;
                 }
                 bytes_model += bytesA + 8 * m * (3 * (int64_t)i + 5);
+                if (o->reorth == 2) bytes_reorth += 8 * m * (3 * (int64_t)i + 5);
                 break;
             }
             case 3: {  // Alg. 2 steps 10-11: u_{k+1} = A v_{k+1} - Uk rho, re-orth
                 Av(Vcol(k), Ucol(k), nullptr, nullptr);
                 orth_norm(m, k, w.U, w.ldu, Ucol(k), Tm(k, k), chk, w.rho);
+                // the product, the Ũ_k rho sweep and the CGS2 against Ũ_k
+                bytes_model += bytesA + 8 * m * (4 * (int64_t)k + 5);
+                if (o->reorth != 0) bytes_reorth += 8 * m * (4 * (int64_t)k + 5);
                 break;
             }
         }
@@ -504,6 +494,22 @@ struct Solver {
         breakdowns++;
     }
 
+    // multi-GPU CGS2 whose second pass removed more than half of ||w'||^2 (reading
+    // G1): w'' is formed; its explicit norm (one more all-reduce), the breakdown
+    // test, the T entry and the normalization, as the single-GPU kernel does
+    void fix_norm(const Half &h, int chk) {
+        double *col, *tent;
+        int64_t N;
+        if (h.kind == 1) {
+            col = Vcol(h.i), N = nv, tent = Tm(h.i - 1, h.i);
+        } else {
+            const int j = h.kind == 0 ? 0 : (h.kind == 2 ? h.i : k);
+            col = Ucol(j), N = m, tent = Tm(j, j);
+        }
+        cgs2(N, 0, nullptr, 0, col, false);
+        normalize(N, col, rb, w.ctrl, tent, chk, 0, nsm, s);
+    }
+
     Ctrl read_ctrl() {
         ck(cudaMemcpyAsync(H->hctrl, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H ctrl");
         ck(cudaStreamSynchronize(s), "sync");
@@ -526,20 +532,14 @@ struct Solver {
                 H->prof.end(s);
             }
             Ctrl c = read_ctrl();
-            if (const char *dump = getenv("SVDSC_DEBUG_DUMP")) {  // debugging aid: append T per pass
-                std::vector<double> hT((size_t)(t + 1) * (t + 1));
-                ck(cudaMemcpy(hT.data(), w.T, hT.size() * sizeof(double), cudaMemcpyDeviceToHost), "dump");
-                if (FILE *f = fopen(dump, "ab")) {
-                    fwrite(hT.data(), sizeof(double), hT.size(), f);
-                    fclose(f);
-                }
-            }
             if (!c.abort) return;
             const int idx = c.abort_check - c0;
             if (idx < 0 || idx >= (int)plan.size()) throw SvdscError(SVDSC_ECUDA, "breakdown bookkeeping");
-            const int zero = 0;
-            ck(cudaMemcpyAsync(&w.ctrl->abort, &zero, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-            fix(plan[idx]);
+            const int zero[2] = {0, 0};
+            ck(cudaMemcpyAsync(&w.ctrl->abort, &zero[0], sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+            ck(cudaMemcpyAsync(&w.ctrl->abort_kind, &zero[1], sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+            if (c.abort_kind == 1) fix_norm(plan[idx], c0 + idx);
+            else fix(plan[idx]);
             pos = idx + 1;
         }
     }
@@ -550,13 +550,11 @@ struct Solver {
         carve(w, ws_base, m, n, t, k, P);
         nv = w.nv;
         rb = RedBuf{w.partial, kMaxBlocks, w.h1, w.h2, w.nrm, w.ctrl->cnt};
-        {
-            const char *e = getenv("SVDSC_NO_FUSED");
-            fused_ok = !(e && e[0] == '1');
-            const char *nt = getenv("SVDSC_NO_TMA");
-            have_tmap = !(nt && nt[0] == '1') && make_basis_tmap(tmapU, w.U, m, t + 1, w.ldu) &&
-                        make_basis_tmap(tmapV, w.V, nv, t + 1, w.ldv);
-        }
+        fused_ok = true;
+        // TMA descriptors of the bases (used by the TMA streaming CGS2 kernel,
+        // SVDSC_POLICY_CGS2 = 4)
+        have_tmap = g_policy.cgs2 == 4 && make_basis_tmap(tmapU, w.U, m, t + 1, w.ldu) &&
+                    make_basis_tmap(tmapV, w.V, nv, t + 1, w.ldv);
         abort = &w.ctrl->abort;
         bytesA = M->kind == 0 ? 12 * M->nnz + 4 * (m + 1) : 8 * m * n;
         ck(cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s), "memset");
@@ -642,14 +640,12 @@ struct Solver {
                 recombine(nv, t, k, w.V, w.ldv, w.Vh, t, Vout, ldv_out, nsm, s);
             } else {
                 recombine(nv, t, k, w.V, w.ldv, w.Vh, t, w.vtmp + (int64_t)rank * nv * k, nv, nsm, s);
-                ckn(g_nccl.AllGather(w.vtmp + (int64_t)rank * nv * k, w.vtmp, (size_t)nv * k, kNcclFloat64, H->comm, s),
-                    "ncclAllGather");
+                H->comm->allgather(w.vtmp + (int64_t)rank * nv * k, w.vtmp, (size_t)nv * k, s);
                 copy_gathered(w.vtmp, nv, k, P, n, Vout, ldv_out, s);
             }
             ck(cudaStreamSynchronize(s), "sync");
             ck(cudaGetLastError(), "final");
         }
-        if (getenv("SVDSC_KTIMING")) ktiming_dump();
         if (info) {
             info->passes = passes;
             info->restarts = std::max(0, passes - 1);
@@ -660,6 +656,7 @@ struct Solver {
             info->breakdowns = breakdowns;
             info->max_resid = lbp_only ? 0.0 : c.max_resid;
             info->bytes_model = bytes_model;
+            info->bytes_reorth = bytes_reorth;
             info->reorths = o->reorth == 1 ? H->hctrl->pro_reorths : reorth_halves;
         }
         if (!lbp_only && !c.converged) return SVDSC_NOT_CONVERGED;
@@ -667,24 +664,32 @@ struct Solver {
     }
 };
 
-svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o, void *ws, size_t ws_bytes, double *S, double *U,
+svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o_in, void *ws, size_t ws_bytes, double *S, double *U,
                         int64_t ldu, double *V, int64_t ldv, double *resid, svdsc_info *info, bool lbp_only,
                         int t_override, double *Tout) {
     svdsc_handle *H = M->h;
     svdsc_status ret = SVDSC_OK;
     const int64_t l0 = g_launches;
     auto t0 = std::chrono::steady_clock::now();
+    svdsc_opts oo{};
+    Solver sv{};
+    size_t need = 0;
+    // contract checks (no device work), then every rank agrees on the status
     svdsc_status st = guarded(H, [&] {
-        if (!lbp_only) check_opts(M, o);
-        einval(o->reorth < 0 || o->reorth > 2, "reorth must be 0, 1 or 2");
-        einval(o->reorth == 1 && M->h->comm, "reorth = 1 (partial) is single-GPU only");
-        Solver sv{};
+        einval(!o_in, "opts is NULL");
+        oo = *o_in;
+        if (!lbp_only) check_opts(M, &oo);
+        einval(oo.reorth < -1 || oo.reorth > 2, "reorth must be -1, 0, 1 or 2");
+        // 0 (a zero-initialized struct) = the paper's method, CGS2 every half-step;
+        // -1 = re-orthogonalization off (test only); internally 2 / 1 / 0
+        oo.reorth = oo.reorth == 0 ? 2 : (oo.reorth < 0 ? 0 : oo.reorth);
+        einval(oo.reorth == 1 && H->nranks > 1, "reorth = 1 (partial) is single-GPU only");
         sv.M = M;
         sv.H = H;
-        sv.o = o;
+        sv.o = &oo;
         sv.s = H->stream;
-        sv.k = o->k;
-        sv.t = t_override > 0 ? t_override : resolve_t(o, M->m_global, M->n);
+        sv.k = oo.k;
+        sv.t = t_override > 0 ? t_override : resolve_t(&oo, M->m_global, M->n);
         sv.P = H->nranks;
         sv.rank = H->rank;
         sv.nsm = H->nsm;
@@ -694,18 +699,33 @@ svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o, void *ws, size_t w
         einval(!lbp_only && ldu < std::max<int64_t>(1, M->m_local), "ldu < m_local");
         einval(!lbp_only && ldv < std::max<int64_t>(1, M->n), "ldv < ncols");
         Ws probe;
-        const size_t need = carve(probe, nullptr, M->m_local, M->n, sv.t, sv.k, sv.P);
-        void *base = ws;
-        bool own = false;
-        if (!base) {
-            ck(cudaMallocAsync(&base, need, sv.s), "cudaMallocAsync workspace");
-            own = true;
-        } else {
-            einval(ws_bytes < need, "workspace too small (see svdsc_workspace_size)");
+        need = carve(probe, nullptr, M->m_local, M->n, sv.t, sv.k, sv.P);
+        einval(ws && ws_bytes < need, "workspace too small (see svdsc_workspace_size)");
+    });
+    if (H->nranks > 1) {
+        int agreed = (int)st;
+        const std::string local_err = H->err;
+        const svdsc_status sa = guarded(H, [&] { agreed = H->comm->allreduce_min_int((int)st, H->stream); });
+        if (sa != SVDSC_OK) return sa;
+        if (st != SVDSC_OK) {
+            H->err = local_err;
+            return st;
         }
+        if (agreed != SVDSC_OK) {
+            H->err = "another rank rejected the call (status " + std::to_string(agreed) + ")";
+            return (svdsc_status)agreed;
+        }
+    } else if (st != SVDSC_OK) {
+        return st;
+    }
+    st = guarded(H, [&] {
+        void *base = ws;
+        const bool own = !base;
+        if (own) base = pool_alloc(H, need, sv.s);
         try {
             ret = sv.solve(base, S, U, ldu, V, ldv, resid, info, lbp_only, Tout);
         } catch (...) {
+            if (H->comm) H->comm->abort();
             if (own) {
                 cudaFreeAsync(base, sv.s);
                 cudaStreamSynchronize(sv.s);
@@ -719,6 +739,7 @@ svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o, void *ws, size_t w
     });
     if (info) {
         info->seconds_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        info->seconds_analysis = M->seconds_analysis;
         info->launches = g_launches - l0;
     }
     return st != SVDSC_OK ? st : ret;
@@ -735,8 +756,6 @@ void matrix_common_dense_setup(svdsc_matrix *M) {
     // ~2500 CTAs (2.8 waves at 6 CTAs/SM): measured best at config 2 (splits 4-5:
     // 120 us vs 127 us at 2 splits; tools/timeline.py sweep)
     D.splits_t = (int)std::max<int64_t>(1, std::min<int64_t>({64, (2500 + cb / 2) / cb, std::max<int64_t>(1, m / 1024)}));
-    if (const char *e = getenv("SVDSC_SPLITS_T")) D.splits_t = std::max(1, atoi(e));  // experiment
-    if (const char *e = getenv("SVDSC_SPLITS_N")) D.splits_n = std::max(1, atoi(e));  // experiment
     const size_t need = std::max<size_t>((size_t)D.splits_n * m, (size_t)D.splits_t * n);
     ck(cudaMalloc(&M->dense_partial, need * sizeof(double)), "cudaMalloc");
     D.partial = M->dense_partial;
@@ -760,17 +779,21 @@ svdsc_status svdsc_create(svdsc_handle **h, void *stream) {
         H->stream = reinterpret_cast<cudaStream_t>(stream);
         ck(cudaMallocHost(&H->hctrl, sizeof(Ctrl)), "cudaMallocHost");
         // stream-ordered allocations (NULL workspace, host-buffer entry points)
-        // come from the device's default pool: keep its memory mapped between
-        // solves instead of returning it at every synchronization (re-mapping
-        // the 800 MB operand of BASELINE config 2 cost ~40 ms per solve)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, H->device) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        cudaGetLastError();
+        // come from a private pool that keeps its memory mapped between solves
+        // instead of returning it at every synchronization (re-mapping the
+        // 800 MB operand of BASELINE config 2 cost ~40 ms per solve); the
+        // device's default pool, which the host application may use, is untouched
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = H->device;
+        ck(cudaMemPoolCreate(&H->pool, &props), "cudaMemPoolCreate");
+        uint64_t keep = UINT64_MAX;
+        ck(cudaMemPoolSetAttribute(H->pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool attribute");
     });
     if (st != SVDSC_OK) {
+        if (H->hctrl) cudaFreeHost(H->hctrl);
+        if (H->pool) cudaMemPoolDestroy(H->pool);
         delete H;
         return st;
     }
@@ -786,10 +809,11 @@ svdsc_status svdsc_set_stream(svdsc_handle *h, void *stream) {
 
 void svdsc_destroy(svdsc_handle *h) {
     if (!h) return;
-    if (getenv("SVDSC_KTIMING")) ktiming_dump();  // op-level calls (tools/probe_cgs2.py)
-    if (h->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm);
+    cudaStreamSynchronize(h->stream);
+    delete h->comm;
     if (h->hctrl) cudaFreeHost(h->hctrl);
     if (h->scratch) cudaFree(h->scratch);
+    if (h->pool) cudaMemPoolDestroy(h->pool);
     delete h;
 }
 
@@ -801,6 +825,7 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
     if (!h || !Mout) return SVDSC_EINVAL;
     *Mout = nullptr;
     svdsc_matrix *M = new svdsc_matrix();
+    const auto t0 = std::chrono::steady_clock::now();
     svdsc_status st = guarded(h, [&] {
         einval(nrows < 0 || ncols < 1 || nnz < 0, "bad dimensions");
         einval(!row_ptr || (nnz > 0 && (!col_idx || !values)), "NULL array");
@@ -816,7 +841,7 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
         M->m_global = m_global;
         cudaStream_t s = h->stream;
         int *bad = nullptr;
-        ck(cudaMallocAsync((void **)&bad, sizeof(int), s), "alloc");
+        bad = (int *)pool_alloc(h, sizeof(int), s);
         ck(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
         k_validate_csr<<<148 * 4, 256, 0, s>>>(nrows, ncols, nnz, row_ptr, col_idx, values, bad);
         int hb = 0;
@@ -835,6 +860,7 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
         M->A.val = values;
         csr_analyze(M->A, s);
         csr_transpose(M->A, M->At, s);
+        M->seconds_analysis = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
     if (st != SVDSC_OK) {
         csr_free(M->A);
@@ -851,6 +877,7 @@ svdsc_status svdsc_matrix_dense(svdsc_handle *h, int64_t nrows, int64_t ncols, i
     if (!h || !Mout) return SVDSC_EINVAL;
     *Mout = nullptr;
     svdsc_matrix *M = new svdsc_matrix();
+    const auto t0 = std::chrono::steady_clock::now();
     svdsc_status st = guarded(h, [&] {
         einval(nrows < 1 || ncols < 1 || ld < nrows, "bad dimensions");
         einval(!data, "NULL data");
@@ -864,7 +891,7 @@ svdsc_status svdsc_matrix_dense(svdsc_handle *h, int64_t nrows, int64_t ncols, i
         M->nnz = nrows * ncols;
         cudaStream_t s = h->stream;
         int *bad = nullptr;
-        ck(cudaMallocAsync((void **)&bad, sizeof(int), s), "alloc");
+        bad = (int *)pool_alloc(h, sizeof(int), s);
         ck(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
         k_validate_dense<<<148 * 4, 256, 0, s>>>(nrows, ncols, ld, data, bad);
         int hb = 0;
@@ -877,6 +904,7 @@ svdsc_status svdsc_matrix_dense(svdsc_handle *h, int64_t nrows, int64_t ncols, i
         M->D.ld = ld;
         M->D.data = data;
         matrix_common_dense_setup(M);
+        M->seconds_analysis = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
     if (st != SVDSC_OK) {
         if (M->dense_partial) cudaFree(M->dense_partial);
@@ -936,8 +964,7 @@ svdsc_status svdsc_solve_host_csr(svdsc_handle *h, int64_t m, int64_t n, int64_t
         einval(m < 1 || n < 1 || nnz < 0 || !row_ptr || !S || !U || !V, "bad arguments");
         cudaStream_t s = h->stream;
         auto dalloc = [&](size_t b) {
-            void *p = nullptr;
-            ck(cudaMallocAsync(&p, std::max<size_t>(b, 8), s), "cudaMallocAsync");
+            void *p = pool_alloc(h, b, s);
             bufs.push_back(p);
             return p;
         };
@@ -982,8 +1009,7 @@ svdsc_status svdsc_solve_host_dense(svdsc_handle *h, int64_t m, int64_t n, const
         einval(m < 1 || n < 1 || !data || !S || !U || !V, "bad arguments");
         cudaStream_t s = h->stream;
         auto dalloc = [&](size_t b) {
-            void *p = nullptr;
-            ck(cudaMallocAsync(&p, std::max<size_t>(b, 8), s), "cudaMallocAsync");
+            void *p = pool_alloc(h, b, s);
             bufs.push_back(p);
             return p;
         };
@@ -1074,35 +1100,22 @@ svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const doub
         OpScratch sc = op_scratch(h, (int)ncols, 1);
         RedBuf rb{sc.partial, kMaxBlocks, sc.h1, sc.h2, sc.nrm, sc.ctrl->cnt};
         cudaStream_t s = h->stream;
-        const char *fp = getenv("SVDSC_OPCGS_FUSED");  // test hook: run the solver's fused kernel
-        if (fp && fp[0] == '1') {
-            // fused path normalizes w; norm_dev receives the norm (the T entry)
-            alignas(64) unsigned char tm[128];
-            const bool have = (fp[1] == 't') && ncols > 0 && make_basis_tmap(tm, Q, N, ncols, ldq);
-            FusedScratch fs{sc.partial, sc.h1, sc.h2, sc.nrm, sc.ctrl->gflags, 16u};
-            double *tent = sc.nrm + 2;
-            if (!cgs2_fused(N, (int)ncols, Q, ldq, w, nullptr, fs, sc.ctrl, tent, 0, h->nsm, s, have ? tm : nullptr))
-                throw SvdscError(SVDSC_EINVAL, "fused CGS2 path not applicable");
-            if (norm_dev) ck(cudaMemcpyAsync(norm_dev, tent, sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
-            ck(cudaStreamSynchronize(s), "sync");
-            ck(cudaGetLastError(), "cgs2 fused");
-            return;
+        double *tent = sc.nrm + 2;  // the T entry (beta / alpha) of this half-step
+        // the solver's kernel for this shape (SVDSC_POLICY_CGS2), else the split sweeps
+        alignas(64) unsigned char tm[128];
+        const bool have = g_policy.cgs2 == 4 && ncols > 0 && make_basis_tmap(tm, Q, N, ncols, ldq);
+        FusedScratch fs{sc.partial, sc.h1, sc.h2, sc.nrm, sc.ctrl->gflags, 16u};
+        if (!cgs2_fused(N, (int)ncols, Q, ldq, w, nullptr, fs, sc.ctrl, tent, 0, h->nsm, s, have ? tm : nullptr)) {
+            if (ncols > 0) {
+                cgs_p1(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
+                cgs_p2(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
+                cgs_p3(N, (int)ncols, Q, ldq, w, sc.h2, rb, nullptr, h->nsm, s);
+            } else {
+                cgs_p3(N, 0, Q, ldq, w, nullptr, rb, nullptr, h->nsm, s);
+            }
+            normalize(N, w, rb, sc.ctrl, tent, 0, 0, h->nsm, s);
         }
-        if (ncols > 0) {
-            cgs_p1(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
-            cgs_p2(N, (int)ncols, Q, ldq, w, rb, nullptr, h->nsm, s);
-            cgs_p3(N, (int)ncols, Q, ldq, w, sc.h2, rb, nullptr, h->nsm, s);
-        } else {
-            cgs_p3(N, 0, Q, ldq, w, nullptr, rb, nullptr, h->nsm, s);
-        }
-        if (norm_dev) {
-            // norm = sqrt(nrm2) via a 1-element normalize-free copy
-            double hv = 0.0;
-            ck(cudaMemcpyAsync(&hv, sc.nrm, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-            ck(cudaStreamSynchronize(s), "sync");
-            hv = std::sqrt(hv);
-            ck(cudaMemcpyAsync(norm_dev, &hv, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
-        }
+        if (norm_dev) ck(cudaMemcpyAsync(norm_dev, tent, sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
         ck(cudaStreamSynchronize(s), "sync");
         ck(cudaGetLastError(), "cgs2");
     });
@@ -1116,7 +1129,7 @@ svdsc_status svdsc_op_small_svd(svdsc_handle *h, int32_t p, const double *Tm, do
         einval(p < 1 || p > 1023 || !Tm || !U || !S || !V, "bad arguments");
         OpScratch sc = op_scratch(h, 0, p);
         cudaStream_t s = h->stream;
-        small_svd(p, Tm, p, sc.W, sc.Vw, U, S, V, p, sc.ctrl, nullptr, getenv("SVDSC_NO_CLUSTER_SVD") ? nullptr : sc.tlog, s);
+        small_svd(p, Tm, p, sc.W, sc.Vw, U, S, V, p, sc.ctrl, nullptr, sc.tlog, s);
         Ctrl c;
         ck(cudaMemcpyAsync(&c, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H");
         ck(cudaStreamSynchronize(s), "sync");
@@ -1162,28 +1175,61 @@ svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int64_t *call
 
 svdsc_status svdsc_comm_unique_id(unsigned char id[128]) {
     if (!id) return SVDSC_EINVAL;
-    if (!nccl_load()) return SVDSC_ENCCL;
-    ncclUniqueId u;
-    if (g_nccl.GetUniqueId(&u) != 0) return SVDSC_ENCCL;
-    std::memcpy(id, u.internal, 128);
-    return SVDSC_OK;
+    return guarded(nullptr, [&] { comm_nccl_unique_id(id); });
 }
 
 svdsc_status svdsc_comm_init(svdsc_handle *h, int nranks, int rank, const unsigned char id[128]) {
     if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks) return SVDSC_EINVAL;
-    if (nranks == 1) {
+    return guarded(h, [&] {
+        delete h->comm;
+        h->comm = nullptr;
         h->nranks = 1;
         h->rank = 0;
-        return SVDSC_OK;
-    }
-    return guarded(h, [&] {
-        if (!nccl_load()) throw SvdscError(SVDSC_ENCCL, "libnccl.so.2 not loadable");
-        ncclUniqueId u;
-        std::memcpy(u.internal, id, 128);
-        ckn(g_nccl.CommInitRank(&h->comm, nranks, u, rank), "ncclCommInitRank");
+        if (nranks == 1) return;
+        h->comm = comm_nccl_create(id, nranks, rank);
         h->nranks = nranks;
         h->rank = rank;
     });
+}
+
+svdsc_status svdsc_group_create(int nranks, svdsc_group **g) {
+    if (!g || nranks < 1 || nranks > 16) return SVDSC_EINVAL;
+    *g = new svdsc_group{loopback_group_create(nranks), nranks};
+    return SVDSC_OK;
+}
+
+void svdsc_group_destroy(svdsc_group *g) {
+    if (!g) return;
+    loopback_group_release(g->g);
+    delete g;
+}
+
+svdsc_status svdsc_comm_init_group(svdsc_handle *h, svdsc_group *g, int rank) {
+    if (!h || !g || !g->g) return SVDSC_EINVAL;
+    return guarded(h, [&] {
+        einval(rank < 0 || rank >= g->nranks(), "rank out of range");
+        delete h->comm;
+        h->comm = nullptr;
+        h->nranks = 1;
+        h->rank = 0;
+        if (g->nranks() == 1) return;
+        h->comm = comm_loopback_create(g->g, rank);
+        h->nranks = g->nranks();
+        h->rank = rank;
+    });
+}
+
+svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t value) {
+    if (!h) return SVDSC_EINVAL;
+    const int maxv[3] = {2, 5, 1};
+    if (key < 0 || key > 2 || value < 0 || value > maxv[key]) {
+        h->err = "svdsc_set_policy: unknown key or value";
+        return SVDSC_EINVAL;
+    }
+    if (key == SVDSC_POLICY_SPMV) h->policy.spmv = value;
+    else if (key == SVDSC_POLICY_CGS2) h->policy.cgs2 = value;
+    else h->policy.small_svd = value;
+    return SVDSC_OK;
 }
 
 svdsc_status svdsc_partition_rows(int64_t m, const int64_t *row_ptr, int64_t basis_cols, int nparts, int64_t *bounds) {

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, os.environ.get("SVDSC_LIB_VARIANT", "libsvdsc.so"))  # variant: tuning experiments
+_SO = os.path.join(_HERE, "libsvdsc.so")
 _lib = None
 
 OK, NOT_CONVERGED = 0, 1
@@ -44,7 +44,8 @@ class Info(ctypes.Structure):
                 ("steps", ctypes.c_int64), ("matvecs", ctypes.c_int64),
                 ("breakdowns", ctypes.c_int64), ("max_resid", ctypes.c_double),
                 ("seconds_total", ctypes.c_double), ("launches", ctypes.c_int64),
-                ("bytes_model", ctypes.c_int64), ("reorths", ctypes.c_int64)]
+                ("bytes_model", ctypes.c_int64), ("reorths", ctypes.c_int64),
+                ("bytes_reorth", ctypes.c_int64), ("seconds_analysis", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -67,7 +68,13 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
            "svdsc_solve", "svdsc_solve_host_csr", "svdsc_solve_host_dense", "svdsc_op_matvec",
            "svdsc_op_cgs2", "svdsc_op_small_svd", "svdsc_op_recombine", "svdsc_op_lbp",
            "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows",
-           "svdsc_profile_enable", "svdsc_profile_read"]
+           "svdsc_profile_enable", "svdsc_profile_read", "svdsc_set_policy",
+           "svdsc_group_create", "svdsc_group_destroy", "svdsc_comm_init_group"]
+# svdsc_set_policy keys / values (include/svdsc.h)
+POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD = 0, 1, 2
+SPMV = {"auto": 0, "bins": 1, "merge": 2}
+CGS2 = {"auto": 0, "split": 1, "qs": 2, "stream": 3, "tma": 4, "cluster": 5}
+SMALL_SVD = {"auto": 0, "one_cta": 1}
 PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",
                  "recombine", "restart_misc", "collectives", "cgs2_fused", "pro_decide"]
 
@@ -109,6 +116,11 @@ def lib():
         L.svdsc_partition_rows.argtypes = [I64, P, I64, ctypes.c_int, P]
         L.svdsc_profile_enable.argtypes = [P, ctypes.c_int]
         L.svdsc_profile_read.argtypes = [P, P, P]
+        L.svdsc_set_policy.argtypes = [P, I32, I32]
+        L.svdsc_group_create.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+        L.svdsc_group_destroy.argtypes = [P]
+        L.svdsc_group_destroy.restype = None
+        L.svdsc_comm_init_group.argtypes = [P, P, ctypes.c_int]
         # the paper's interface (include/svdsc_paper.h)
         PM, PC = ctypes.POINTER(PaperMat), ctypes.POINTER(PaperCsr)
         for f in ("svds_C", "svds_C_opt"):
@@ -170,6 +182,18 @@ class Handle:
         self._check(lib().svdsc_comm_init(self.ptr, nranks, rank, uid))
         self.nranks, self.rank = nranks, rank
 
+    def comm_init_group(self, group: "Group", rank):
+        """Join an in-process loopback group (svdsc_comm_init_group)."""
+        self._check(lib().svdsc_comm_init_group(self.ptr, group.ptr, rank))
+        self.nranks, self.rank = group.nranks, rank
+
+    def set_policy(self, spmv=None, cgs2=None, small_svd=None):
+        """Force a kernel schedule (svdsc_set_policy); names from SPMV / CGS2 / SMALL_SVD."""
+        for key, table, v in ((POLICY_SPMV, SPMV, spmv), (POLICY_CGS2, CGS2, cgs2),
+                              (POLICY_SMALL_SVD, SMALL_SVD, small_svd)):
+            if v is not None:
+                self._check(lib().svdsc_set_policy(self.ptr, key, table[v] if isinstance(v, str) else int(v)))
+
     def profile(self, enable=True, families=None):
         """CUDA-event timing per operation family; `families`: names to record
         (None: all) -- fewer events inside a timed region."""
@@ -187,6 +211,28 @@ class Handle:
     def close(self):
         if self.ptr:
             lib().svdsc_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Group:
+    """In-process loopback group of nranks ranks (svdsc_group_create)."""
+
+    def __init__(self, nranks):
+        self.ptr = ctypes.c_void_p()
+        self.nranks = nranks
+        st = lib().svdsc_group_create(nranks, ctypes.byref(self.ptr))
+        if st < 0:
+            raise SvdscError(st, "svdsc_group_create")
+
+    def close(self):
+        if self.ptr:
+            lib().svdsc_group_destroy(self.ptr)
             self.ptr = ctypes.c_void_p()
 
     def __del__(self):

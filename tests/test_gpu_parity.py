@@ -38,6 +38,15 @@ def H(S):
     return S.Handle()
 
 
+@pytest.fixture
+def Hp(S):
+    """A fresh handle per test, for tests that force a kernel schedule
+    (svdsc_set_policy applies to the handle's later calls)."""
+    h = S.Handle()
+    yield h
+    h.close()
+
+
 def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
@@ -76,23 +85,20 @@ def check_products(S, H, A, seed=0):
 
 
 # ---------------------------------------------------------------- a1 / a5
-@pytest.mark.parametrize("sched", ["auto", "merge", "bins", "cb"])
+@pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
 @pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000), (4, 10), (3, 2)])
-def test_products_configs(S, H, cid, scale, sched, monkeypatch):
+def test_products_configs(S, Hp, cid, scale, sched):
     """Every SpMV schedule on every config: "auto" = the merge schedule on
-    power-law operands, else the row bins; "cb" = the opt-in column-blocked
-    kernel where it applies (configs 1, 3: x reused, <= 16 blocks of 24,576
-    columns; config 3 at 1/2 scale has 3 blocks for A v and 5 for A^T u)."""
-    if sched != "auto":
-        monkeypatch.setenv("SVDSC_SPMV", sched)
+    power-law operands, else the row bins (svdsc_set_policy SVDSC_POLICY_SPMV)."""
+    Hp.set_policy(spmv=sched)
     wl = W.config(cid, scale=scale)
-    check_products(S, H, wl.A)
+    check_products(S, Hp, wl.A)
 
 
 @pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
-def test_products_edge_cases(S, H, sched, monkeypatch):
-    if sched != "auto":
-        monkeypatch.setenv("SVDSC_SPMV", sched)
+def test_products_edge_cases(S, Hp, sched):
+    H = Hp
+    H.set_policy(spmv=sched)
     rng = np.random.default_rng(7)
     m, n = 3001, 777
     rows = []
@@ -127,26 +133,6 @@ def test_products_edge_cases(S, H, sched, monkeypatch):
     assert np.all(np.abs(yt - O.spmv_t(A2, u)) <= bud + 1e-300)
 
 
-@pytest.mark.parametrize("ncols", [24576, 24577, 49153, 3 * 24576 + 17])
-def test_products_column_blocked_ragged(S, H, ncols, monkeypatch):
-    """Column-blocked SpMV: block edges (a last block of 1 or 17 columns), empty
-    rows, rows with all entries in one block, duplicates, 4..60 nnz per row."""
-    monkeypatch.setenv("SVDSC_SPMV", "cb")
-    rng = np.random.default_rng(ncols)
-    m = 24001
-    lens = rng.integers(4, 60, m)
-    lens[::13] = 0
-    lens[-2:] = 0
-    rp = np.zeros(m + 1, np.int64)
-    rp[1:] = np.cumsum(lens)
-    col = rng.integers(0, ncols, rp[-1]).astype(np.int32)
-    col[rp[7]:rp[8]] = ncols - 1  # a row living in the last (ragged) block
-    val = rng.standard_normal(rp[-1])
-    A = W.Matrix("csr", m, ncols, row_ptr=rp, col_idx=col, values=val)
-    assert A.nnz >= 8 * ncols  # eligible: x is reused
-    check_products(S, H, A)
-
-
 @pytest.mark.parametrize("m,n", [(5000, 1250), (1001, 333), (20000, 5000)])
 def test_products_dense(S, H, m, n):
     rng = np.random.default_rng(m)
@@ -155,48 +141,30 @@ def test_products_dense(S, H, m, n):
 
 
 # ---------------------------------------------------------------- a2-a4 / a6
-@pytest.mark.parametrize("N,c", [(10007, 37), (200000, 300), (3, 1), (50000, 0), (4096, 600)])
-def test_cgs2(S, H, N, c):
-    rng = np.random.default_rng(N + c)
+@pytest.mark.parametrize("variant", ["auto", "split", "qs", "stream", "tma", "cluster"])
+@pytest.mark.parametrize("N,c", [(10007, 37), (200000, 300), (4096, 150), (1250, 64), (333, 5), (4096, 65),
+                                 (4096, 96), (4096, 128), (4096, 129), (65536, 150), (70001, 257),
+                                 (4096, 600), (30011, 17), (70001, 9), (40000, 30), (3, 1), (50000, 0)])
+def test_cgs2_variants(S, Hp, N, c, variant):
+    """One re-orthogonalization half-step (svdsc_op_cgs2: CGS2 + norm +
+    normalize) through every kernel the solver may pick (svdsc_set_policy
+    SVDSC_POLICY_CGS2; a forced kernel that cannot run the shape falls back to
+    the split sweeps) against the oracle's CGS2 and norm."""
+    Hp.set_policy(cgs2=variant)
+    rng = np.random.default_rng(N * 7 + c)
     Q = np.linalg.qr(rng.standard_normal((N, max(c, 1))))[0][:, :c]
     w = rng.standard_normal(N)
     if c:
-        w += Q @ rng.standard_normal(c) * 10  # mostly inside span(Q)
-    Qd = S.colmajor(N, max(c, 1))
-    if c:
-        Qd.copy_(dev(np.asfortranarray(Q)))
-    wg, nrm = S.cgs2(H, Qd if c else None, dev(w))
-    w_or = O.cgs2(Q, w) if c else w.copy()
-    scale = np.linalg.norm(w)
-    assert np.abs(wg.cpu().numpy() - w_or).max() <= 1e-12 * scale
-    assert abs(nrm.item() - O.norm2(w_or)) <= 1e-12 * scale
-
-
-@pytest.mark.parametrize("variant", ["qs", "stream", "stream2", "tma"])
-@pytest.mark.parametrize("N,c", [(10007, 37), (200000, 300), (4096, 150), (1250, 64), (333, 5), (4096, 65),
-                                 (4096, 96), (4096, 128), (4096, 129), (65536, 150), (70001, 257),
-                                 (4096, 600), (30011, 17), (70001, 9), (40000, 30)])
-def test_cgs2_fused_variants(S, H, N, c, variant, monkeypatch):
-    """The solver's fused CGS2 + normalize kernels (Q-resident, cp.async
-    streaming, register-blocked streaming, TMA streaming) against the oracle."""
-    env = {"qs": ("1", "0", None), "stream": ("1t", "1", "1"), "stream2": ("1t", "1", "2"),
-           "tma": ("1t", "1", "0")}[variant]
-    monkeypatch.setenv("SVDSC_OPCGS_FUSED", env[0])
-    if env[1] == "1":
-        monkeypatch.setenv("SVDSC_FORCE_STREAM", "1")
-    if env[2] is not None:
-        monkeypatch.setenv("SVDSC_STREAM_VARIANT", env[2])
-    rng = np.random.default_rng(N * 7 + c)
-    Q = np.linalg.qr(rng.standard_normal((N, c)))[0]
-    w = rng.standard_normal(N) + Q @ rng.standard_normal(c) * 3
+        w += Q @ rng.standard_normal(c) * 3
     ld = -(-N // 32) * 32
     Qd = torch.zeros((c + 1, ld), dtype=torch.float64, device="cuda")  # column-major, ld % 32 == 0
-    Qd[:c, :N] = dev(np.ascontiguousarray(Q.T))
+    if c:
+        Qd[:c, :N] = dev(np.ascontiguousarray(Q.T))
     wd = torch.zeros(ld, dtype=torch.float64, device="cuda")
     wd[:N] = dev(w)
-    Qv = Qd.t()[:N, :c]
-    wg, nrm = S.cgs2(H, Qv, wd[:N])
-    w_or = O.cgs2(Q, w)
+    Qv = Qd.t()[:N, :c] if c else None
+    wg, nrm = S.cgs2(Hp, Qv, wd[:N])
+    w_or = O.cgs2(Q, w) if c else w.copy()
     nor = O.norm2(w_or)
     assert abs(nrm.item() - nor) <= 1e-12 * np.linalg.norm(w)
     assert np.abs(wg.cpu().numpy() - w_or / nor).max() <= 1e-12 * np.linalg.norm(w) / nor
@@ -219,11 +187,12 @@ def _arrow(rng, p, k):
 @pytest.mark.parametrize("cluster", [True, False])
 @pytest.mark.parametrize("p,kind", [(30, "bidiag"), (150, "arrow"), (300, "arrow"), (31, "bidiag"), (1, "bidiag"),
                                     (601, "arrow")])
-def test_small_svd(S, H, p, kind, cluster, monkeypatch):
+def test_small_svd(S, Hp, p, kind, cluster):
+    H = Hp
     if not cluster:
         if p > 300:
             pytest.skip("one-CTA fallback is slow at this size")
-        monkeypatch.setenv("SVDSC_NO_CLUSTER_SVD", "1")
+        H.set_policy(small_svd="one_cta")
     rng = np.random.default_rng(p)
     T = _bidiag(rng, p) if kind == "bidiag" or p < 3 else _arrow(rng, p, p // 3)
     Td = S.colmajor(p, p)
@@ -301,13 +270,14 @@ def _e2e(S, H, wl, fixed=True, **kw):
 
 @pytest.mark.parametrize("mode", ["fused", "stream", "split"])
 @pytest.mark.parametrize("cid,scale", [(1, 1), (2, 4), (3, 20), (6, 10), (7, 10), (8, 10)])
-def test_svds_parity(S, H, cid, scale, mode, monkeypatch):
+def test_svds_parity(S, Hp, cid, scale, mode):
+    H = Hp
     if mode == "split":
-        monkeypatch.setenv("SVDSC_NO_FUSED", "1")
+        H.set_policy(cgs2="split")
     if mode == "stream":
         if cid == 1:
             pytest.skip("covered by the other configs")
-        monkeypatch.setenv("SVDSC_FORCE_STREAM", "1")
+        H.set_policy(cgs2="stream")
     wl = W.config(cid, scale=scale)
     r, r_or, U, V, s = _e2e(S, H, wl)
     k = wl.k
@@ -353,7 +323,7 @@ def test_svds_forced_restarts_and_breakdown(S, H):
 def test_svds_contract_errors(S, H):
     wl = W.config(1, scale=10)
     M = S.Matrix.from_host(H, wl.A)
-    for kw in (dict(k=0), dict(k=5, tol=0.0), dict(k=298), dict(k=5, reorth=3)):
+    for kw in (dict(k=0), dict(k=5, tol=0.0), dict(k=298), dict(k=5, reorth=3), dict(k=5, reorth=-2)):
         with pytest.raises(S.SvdscError) as e:
             S.svds_c(M, **kw)
         assert e.value.status == -1

@@ -247,6 +247,21 @@ CONFIG_NAMES = {
 }
 
 
+def degrees(cid: int, seed: int = 0, scale: int = 1) -> np.ndarray | None:
+    """Row lengths of a sparse config's generator, without generating the rows
+    (for the row partition of a multi-GPU run: every rank then
+    generates only its own rows with config(cid, r0=..., r1=...)).  None for
+    configs generated as a whole (1: uniform cells; dense)."""
+    f = scale
+    if cid == 3:
+        return np.full(200_000 // f, 50, dtype=np.int64)
+    if cid == 4:
+        return zipf_degrees(4_000_000 // f, 2_000_000 // f, 150_000_000 // f, 100_000, seed)[0]
+    if cid == 5:
+        return np.full(30_000_000 // f, 20, dtype=np.int64)
+    return None
+
+
 def config(cid: int, seed: int = 0, scale: int = 1, r0: int = 0, r1: int | None = None,
            keep_factors: bool = False) -> Workload:
     f = scale
