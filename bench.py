@@ -132,29 +132,38 @@ class PinnedCore:
 
 
 def cpu_fit(wl, seconds_target=15.0):
-    """Time the oracle as it stands (1 thread, one pinned core) on the first s1
-    and s2 Lanczos steps of this workload; fit t(i) = a + b i for the cost of
-    step i (products + CGS2 against i basis vectors): LBP(s) = a s + b s(s+1)/2."""
+    """Time the oracle as it stands (1 thread, one pinned core) and fit the cost
+    of Lanczos step i as t(i) = a + b i:
+      b: the oracle's CGS2 (or_cgs2) of one U-side and one V-side vector against
+         a c-column basis block (synthetic, the workload's row counts), / c;
+      a: the first s Lanczos steps of LBP on the workload (its products and
+         norms), minus their CGS2 share b * s(s+1)/2, / s."""
+    import numpy as np
+
     import oracle as O
+    rng = np.random.default_rng(0)
     with PinnedCore() as pc:
         t0 = time.perf_counter()
         O.lbp(wl.A, 2, wl.v0)
         probe = max(time.perf_counter() - t0, 1e-4) / 2.0
-        s2 = int(max(4, min(wl.t, 0.75 * seconds_target / probe)))
-        s1 = max(2, s2 // 3)
-        times = {}
-        for s in (s1, s2):
+        s = int(max(2, min(wl.t, 0.4 * seconds_target / probe)))
+        t0 = time.perf_counter()
+        O.lbp(wl.A, s, wl.v0)
+        t_lbp = time.perf_counter() - t0
+        # CGS2 per basis column, both sides (bounded: c columns of each side)
+        c = max(2, min(wl.t, 64, int(2e9 // (8 * (wl.A.m + wl.A.n)))))  # <= 2 GB of host basis
+        t_cgs = 0.0
+        for N in (wl.A.m, wl.A.n):
+            Q = np.asfortranarray(rng.standard_normal((N, c)))
+            w = rng.standard_normal(N)
             t0 = time.perf_counter()
-            O.lbp(wl.A, s, wl.v0)
-            times[s] = time.perf_counter() - t0
-    # solve [s1, s1(s1+1)/2; s2, s2(s2+1)/2] [a; b] = [T1; T2]
-    import numpy as np
-    Mx = np.array([[s1, s1 * (s1 + 1) / 2], [s2, s2 * (s2 + 1) / 2]], dtype=float)
-    a, b = np.linalg.solve(Mx, np.array([times[s1], times[s2]]))
-    if b < 0:  # per-column cost below timing noise at this size
-        a, b = times[s2] / s2, 0.0
-    return {"a": float(a), "b": float(b), "s1": s1, "s2": s2, "t1": times[s1], "t2": times[s2],
-            "core": pc.core, "sample_seconds": times[s1] + times[s2]}
+            O.cgs2(Q, w)
+            t_cgs += time.perf_counter() - t0
+            del Q
+    b = t_cgs / c
+    a = max(0.0, (t_lbp - b * s * (s + 1) / 2) / s)
+    return {"a": float(a), "b": float(b), "s": s, "c": c, "t_lbp": t_lbp, "t_cgs": t_cgs,
+            "core": pc.core, "sample_seconds": t_lbp + t_cgs}
 
 
 def step_schedule(k, t, passes):
@@ -205,7 +214,7 @@ def main():
         import oracle as O
         O.lib()
         fit = cpu_fit(wl, seconds_target=6.0)
-        s = fit["s2"]
+        s = fit["s"]
         times = []
         with PinnedCore():
             for i in range(args.warmup + args.steps):
@@ -404,11 +413,12 @@ def main():
         t_solve = sum(fit["a"] + fit["b"] * i for i in sched)
         cpu = {"value": len(sched) / t_solve, "unit": "steps/s", "cores": 1, "kind": "oracle",
                "time_to_k_s": t_solve,
-               "sample": (f"extrapolated: per-step cost t(i) = a + b i fitted on the oracle's first "
-                          f"{fit['s1']} and {fit['s2']} Lanczos steps (Alg. 1 + CGS2) of {wl_full.name} "
-                          f"({fit['sample_seconds']:.1f} s of plain C -O2, 1 thread pinned to core {fit['core']}), "
-                          f"a = {fit['a']:.4g} s, b = {fit['b']:.4g} s, summed over the GPU solve's "
-                          f"{len(sched)} steps ({passes[-1]} passes)"),
+               "sample": (f"extrapolated: per-step cost t(i) = a + b i of the oracle on {wl_full.name}, "
+                          f"b from its CGS2 of one U- and one V-side vector against a {fit['c']}-column basis "
+                          f"block, a from its first {fit['s']} Lanczos steps (Alg. 1 + CGS2) minus their CGS2 "
+                          f"share ({fit['sample_seconds']:.1f} s of plain C -O2, 1 thread pinned to core "
+                          f"{fit['core']}): a = {fit['a']:.4g} s, b = {fit['b']:.4g} s per basis column, "
+                          f"summed over the GPU solve's {len(sched)} steps ({passes[-1]} passes)"),
                **host_info()}
 
     if rank == 0:
