@@ -209,8 +209,9 @@ SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int
  * that cannot run a given shape falls back to the always-applicable path
  * (split sweeps / one-CTA Jacobi).  Per handle; applies to the handle's later
  * calls, including matrix analysis (SVDSC_POLICY_SPMV is read there).
- *   SVDSC_POLICY_SPMV:      0 auto (nnz-balanced tiles when rows > 2048 exist,
- *                           else row-length bins), 1 row-length bins, 2 nnz tiles
+ *   SVDSC_POLICY_SPMV:      0 auto (row-length bins for small operands and
+ *                           near-uniform rows of >= 48 nonzeros, else register-
+ *                           segmented chunks), 1 row-length bins, 2 segmented chunks
  *   SVDSC_POLICY_CGS2:      0 auto (cluster for bases <= 2 MB, else Q-resident
  *                           when the rows fit in shared memory, else streaming),
  *                           1 split sweeps, 2 Q-resident, 3 cp.async streaming,

@@ -59,18 +59,24 @@ struct CsrOp {
     int32_t *chunk_row = nullptr;      // long-row slot per chunk
     int64_t n_long = 0, n_chunks = 0;
     double *chunk_partial = nullptr;   // n_chunks
-    // nnz-balanced ("merge") schedule: tile t = nonzeros [t*kMergeTile, (t+1)*kMergeTile)
-    int64_t n_tiles = 0;
-    int32_t *tile_r0 = nullptr;        // first row of tile t (row holding nonzero t*kMergeTile; 0 for t = 0)
-    int32_t *tile_r1 = nullptr;        // last row of tile t (inclusive; trailing empty rows belong to the last tile)
-    double *tile_head = nullptr;       // partial sum of tile t's first row when it began before the tile
-    double *tile_tail = nullptr;       // partial sum of tile t's last row when it continues after the tile
-    int64_t n_span = 0;                // rows spanning tile boundaries
-    int32_t *span_row = nullptr, *span_t0 = nullptr, *span_t1 = nullptr;  // row, first and last tile
-    bool merge = false;                // use the merge schedule for this operand
+    // register-segmented schedule ("seg", matvec.cu k_spmv_seg): chunks of
+    // kSegChunk consecutive nonzeros, a contiguous run of chunks per warp
+    uint32_t *seg_bits = nullptr;      // ceil(nnz/32) words: bit j of word w set <=> nonzero 32w+j starts its row
+    int32_t *seg_rows = nullptr;       // the non-empty rows, ascending (row of the k-th row start)
+    int32_t *seg_cstart = nullptr;     // per chunk: row starts among the nonzeros before it
+    int32_t *seg_empty = nullptr;      // the empty rows (y = -c yprev)
+    int64_t seg_nempty = 0, seg_nchunks = 0;
+    int seg_cpw = 0, seg_nranges = 0, seg_grid = 0;  // chunks per warp, warp ranges, CTAs
+    double *seg_head = nullptr, *seg_tail = nullptr;  // per warp range partial row sums
+    unsigned int *seg_flag = nullptr;  // per warp range: 1 once its partial is published (reset by the joiner)
+    bool seg = false;                  // use the seg schedule for this operand
     std::vector<void *> owned;         // allocations owned by this operand
 };
-constexpr int kMergeTile = 2048;       // nonzeros per merge tile (256 threads x 8)
+#ifndef SVDSC_SEG_K
+#define SVDSC_SEG_K 4
+#endif
+constexpr int kSegK = SVDSC_SEG_K;     // consecutive nonzeros per lane of a seg chunk (4 or 8)
+constexpr int kSegChunk = 32 * kSegK;  // nonzeros per seg chunk
 
 struct DenseOp {
     int64_t nrows = 0, ncols = 0, ld = 0;

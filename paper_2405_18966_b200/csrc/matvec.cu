@@ -51,15 +51,24 @@ __host__ __device__ __forceinline__ int row_bin(int64_t L) {
     return 6;
 }
 
+// row counts per bin (cnt[0..7]) and the longest row (cnt[8])
 __global__ void k_bin_count(int64_t nrows, const int64_t *__restrict__ rp, unsigned long long *cnt) {
     __shared__ unsigned int sc[8];
+    __shared__ unsigned long long smax;
     if (threadIdx.x < 8) sc[threadIdx.x] = 0;
+    if (threadIdx.x == 0) smax = 0;
     __syncthreads();
+    unsigned long long mx = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
-         r += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&sc[row_bin(rp[r + 1] - rp[r])], 1u);
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t L = rp[r + 1] - rp[r];
+        atomicAdd(&sc[row_bin(L)], 1u);
+        mx = max(mx, (unsigned long long)L);
+    }
+    atomicMax(&smax, mx);
     __syncthreads();
     if (threadIdx.x < 8 && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
+    if (threadIdx.x == 0) atomicMax(&cnt[8], smax);
 }
 
 // bin key and row id per row; a stable radix sort by key then lists every bin's
@@ -218,141 +227,6 @@ __global__ void __launch_bounds__(256) k_spmv_cta(const int32_t *__restrict__ ro
     }
 }
 
-// ---------------------------------------------------------------------------
-// nnz-balanced ("merge") SpMV: every CTA takes kMergeTile consecutive nonzeros
-// whatever the row lengths (power-law rows, CSC columns), so the A stream is
-// perfectly balanced and fully coalesced.  Phase 1: thread j computes the 8
-// products val[p] * x[col[p]] of p = e0 + 8j .. 8j+7 (128-bit loads, 8 gathers
-// in flight) into shared memory.  Phase 2: the tile's rows [r0, r1] are summed
-// from shared memory -- one thread per row for slices <= 32, one warp per row
-// (lane-strided + xor tree) for longer ones.  Rows wholly inside the tile are
-// finished (y = sum - c yprev); a row that began before the tile leaves its
-// part in tile_head[t], one that continues after it in tile_tail[t]; a fixup
-// kernel adds those in tile order.  Deterministic.
-__global__ void __launch_bounds__(256) k_spmv_merge(int64_t nnz, const int32_t *__restrict__ tile_r0,
-                                                    const int32_t *__restrict__ tile_r1,
-                                                    const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                                    const double *__restrict__ val, const double *__restrict__ x,
-                                                    double *__restrict__ y, const double *c_dev,
-                                                    const double *__restrict__ yprev, double *head, double *tail,
-                                                    const int *abort) {
-    if (aborted(abort)) return;
-    __shared__ __align__(16) double prod[kMergeTile];
-    __shared__ int32_t longq[256];
-    __shared__ int nlong;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t t = blockIdx.x;
-    const int64_t e0 = t * kMergeTile, e1 = min(nnz, e0 + kMergeTile);
-    const double c = c_dev ? *c_dev : 0.0;
-    if (tid == 0) nlong = 0;
-    {
-        const int64_t p = e0 + 8 * tid;
-        double v[8];
-        int ci[8];
-        if (p + 8 <= e1) {
-            const int4 *cp = reinterpret_cast<const int4 *>(col + p);
-            const double2 *vp = reinterpret_cast<const double2 *>(val + p);
-            const int4 c0 = __ldcs(cp), c1 = __ldcs(cp + 1);
-            ci[0] = c0.x; ci[1] = c0.y; ci[2] = c0.z; ci[3] = c0.w;
-            ci[4] = c1.x; ci[5] = c1.y; ci[6] = c1.z; ci[7] = c1.w;
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const double2 d = __ldcs(vp + u);
-                v[2 * u] = d.x;
-                v[2 * u + 1] = d.y;
-            }
-        } else {
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const bool ok = p + u < e1;
-                ci[u] = ok ? __ldcs(col + p + u) : 0;
-                v[u] = ok ? __ldcs(val + p + u) : 0.0;
-            }
-        }
-        double xv[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) xv[u] = __ldg(x + ci[u]);
-#pragma unroll
-        for (int u = 0; u < 8; u++) prod[8 * tid + u] = v[u] * xv[u];
-    }
-    __syncthreads();
-    const int r0 = tile_r0[t], r1 = tile_r1[t];
-    auto finish = [&](int r, int64_t a, int64_t b, double sum) {
-        if (rp[r] >= e0) {  // row began inside this tile
-            if (rp[r + 1] <= e1) {
-                if (yprev) sum -= c * yprev[r];
-                y[r] = sum;
-            } else {
-                tail[t] = sum;
-            }
-        } else {
-            head[t] = sum;
-        }
-    };
-    for (int r = r0 + tid; r <= r1; r += 256) {
-        const int64_t a = max(rp[r], e0), b = min(rp[r + 1], e1);
-        if (b - a > 32) {
-            const int q = atomicAdd(&nlong, 1);
-            if (q < 256) longq[q] = r;
-            continue;
-        }
-        double s0 = 0.0, s1 = 0.0;
-        int64_t i = a;
-        for (; i + 1 < b; i += 2) {
-            s0 += prod[i - e0];
-            s1 += prod[i + 1 - e0];
-        }
-        if (i < b) s0 += prod[i - e0];
-        finish(r, a, b, s0 + s1);
-    }
-    __syncthreads();
-    const int nl = min(nlong, 256);  // a tile holds at most kMergeTile / 33 < 256 long slices
-    for (int q = wid; q < nl; q += 8) {
-        const int r = longq[q];
-        const int64_t a = max(rp[r], e0), b = min(rp[r + 1], e1);
-        double s = 0.0;
-        for (int64_t i = a + lane; i < b; i += 32) s += prod[i - e0];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) finish(r, a, b, s);
-    }
-}
-
-// rows spanning tiles: y = tail[t0] + head[t0+1] + ... + head[t1] - c yprev
-__global__ void k_spmv_merge_fix(int64_t n_span, const int32_t *__restrict__ span_row,
-                                 const int32_t *__restrict__ span_t0, const int32_t *__restrict__ span_t1,
-                                 const double *__restrict__ head, const double *__restrict__ tail, double *y,
-                                 const double *c_dev, const double *__restrict__ yprev, const int *abort) {
-    if (aborted(abort)) return;
-    const double c = c_dev ? *c_dev : 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_span; i += (int64_t)gridDim.x * blockDim.x) {
-        const int r = span_row[i];
-        double s = tail[span_t0[i]];
-        for (int t = span_t0[i] + 1; t <= span_t1[i]; t++) s += head[t];
-        if (yprev) s -= c * yprev[r];
-        y[r] = s;
-    }
-}
-
-// tile_r0[t] = row holding nonzero t * kMergeTile (largest r with rp[r] <= e0 and rp[r+1] > e0)
-__global__ void k_merge_tiles(int64_t nrows, int64_t nnz, int64_t n_tiles, const int64_t *__restrict__ rp,
-                              int32_t *r0) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles; t += (int64_t)gridDim.x * blockDim.x) {
-        if (t == 0) {
-            r0[0] = 0;
-            continue;
-        }
-        const int64_t e0 = t * kMergeTile;
-        int64_t lo = 0, hi = nrows;  // find largest r with rp[r] <= e0 (rp[nrows] = nnz > e0)
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) / 2;
-            if (rp[mid] <= e0) lo = mid;
-            else hi = mid;
-        }
-        r0[t] = (int32_t)lo;
-    }
-}
-
 // chunks of long rows: partial[ch] = sum over the chunk
 __global__ void __launch_bounds__(256) k_spmv_chunks(int64_t n_chunks, const int32_t *__restrict__ chunk_row,
                                                      const int64_t *__restrict__ chunk_first,
@@ -387,6 +261,306 @@ __global__ void k_spmv_chunks_fix(int64_t n_long, const int32_t *__restrict__ lo
         double sum = 0.0;
         for (int64_t ch = chunk_first[s]; ch < chunk_first[s + 1]; ch++) sum += partial[ch];
         epilogue_store(y, long_rows[s], sum, c, yprev);
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Register-segmented SpMV ("seg", the default schedule for every CSR operand:
+// A and its CSC copy, uniform and power-law rows alike).  The nonzeros are cut
+// into chunks of kSegChunk = 32 lanes x 8 consecutive nonzeros; each warp of a
+// persistent grid owns a contiguous run of chunks (nnz-balanced, whatever the
+// row lengths).  Per chunk a lane loads its 8 column indices and values with
+// 128-bit streaming loads, issues its 8 independent x gathers, and sums its
+// products in order, splitting them at row starts read from a bitmap (1 bit per
+// nonzero, built at analysis): rows wholly inside the lane are finished there;
+// the pieces that cross lanes are joined by a segmented suffix sum over the
+// warp (5 shuffles), the piece that crosses chunks is carried in a register.
+// Rows crossing warp ranges leave partial sums (head / tail per range) that the
+// last CTA to finish adds in range order.  No shared memory, no barriers in
+// the loop (round 1's nnz-tile kernel spent ~1/3 of its L1 cycles on shared-
+// memory staging and bank conflicts); every sum has a fixed order, so the
+// result is bitwise reproducible.  The row index of the k-th row start is
+// rows[k] (non-empty rows, ascending); cstart[ch] = row starts before chunk ch.
+struct SegArgs {
+    int64_t nnz;
+    int nchunks, cpw, nranges;
+    const int32_t *col;
+    const double *val;
+    const double *x;
+    const uint32_t *bits;
+    const int32_t *rows, *cstart, *empty;
+    int64_t nempty;
+    double *y;
+    const double *c_dev, *yprev;
+    double *head, *tail;
+    unsigned int *flag;  // per warp range: 1 once its head / tail piece is published (the joiner resets it)
+    const int *abort;
+};
+constexpr int kSegThreads = 256;
+constexpr unsigned kFull = 0xffffffffu;
+#ifndef SVDSC_SEG_MINB
+#define SVDSC_SEG_MINB 5
+#endif
+#ifndef SVDSC_SEG_FULLPF
+#define SVDSC_SEG_FULLPF 0
+#endif
+constexpr bool kSegFullPf = SVDSC_SEG_FULLPF != 0;
+constexpr int kSegMinBlocks = SVDSC_SEG_MINB;
+
+// the first nonzero of warp range w continues a row that began before it
+__device__ __forceinline__ bool seg_mid(const SegArgs &a, int w) {
+    const int64_t b = (int64_t)w * a.cpw * kSegChunk;
+    return b < a.nnz && !((__ldg(a.bits + (b >> 5)) >> (b & 31)) & 1u);
+}
+
+__device__ __forceinline__ void seg_store(const SegArgs &a, int k, double s, double c) {
+    const int r = __ldg(a.rows + k);
+    if (a.yprev) s -= c * a.yprev[r];
+    a.y[r] = s;
+}
+
+__device__ __forceinline__ void seg_publish(const SegArgs &a, int w) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.flag + w), "r"(1u) : "memory");
+}
+
+// Row k began in an earlier warp range and ends in range w with the piece
+// `own`: wait for the earlier ranges' pieces (decoupled look-back: only
+// lower-numbered ranges, i.e. warps of CTAs dispatched no later than this
+// one, are waited for) and add them in range order: tail of the range where
+// the row began, heads of the ranges it spans whole, then own.  One lane.
+__device__ __forceinline__ void seg_join(const SegArgs &a, int w, int k, double own, double c) {
+    int wf = w;
+    for (;;) {
+        const int wp = wf - 1;
+        unsigned f;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flag + wp) : "memory");
+            if (f == 1u) break;
+            __nanosleep(64);
+        }
+        if (wp > 0 && seg_mid(a, wp) && __ldg(a.cstart + wp * a.cpw) - 1 == k) {
+            wf = wp;  // range wp lies wholly inside row k: its piece is head[wp]
+            continue;
+        }
+        break;  // row k began in range wp = wf - 1: its piece is tail[wp]
+    }
+    double s = __ldcg(a.tail + wf - 1);
+    for (int j = wf; j < w; j++) s += __ldcg(a.head + j);
+    seg_store(a, k, s + own, c);
+    // every published piece has exactly one joiner: reset its flag for the
+    // next launch (stream order), so no launch counter is needed (graph-safe)
+    for (int j = wf - 1; j < w; j++) a.flag[j] = 0u;
+}
+
+// one lane's kSegK consecutive nonzeros of a chunk: column indices, row-start
+// bits and the chunk's row-start offset (seg_load_ci), values (seg_load_v)
+__device__ __forceinline__ void seg_load_ci(const SegArgs &a, int ch, int lane, int (&ci)[kSegK], uint32_t &bits,
+                                            int &kb) {
+    constexpr uint32_t kMask = (1u << kSegK) - 1u;
+    const int64_t e = (int64_t)ch * kSegChunk + kSegK * lane;
+    bits = 0;
+    kb = __ldg(a.cstart + ch);
+    if (e + kSegK <= a.nnz) {
+        const int4 *cp = reinterpret_cast<const int4 *>(a.col + e);
+#pragma unroll
+        for (int q = 0; q < kSegK / 4; q++) {
+            const int4 t = __ldcs(cp + q);
+            ci[4 * q] = t.x;
+            ci[4 * q + 1] = t.y;
+            ci[4 * q + 2] = t.z;
+            ci[4 * q + 3] = t.w;
+        }
+        bits = (__ldg(a.bits + (e >> 5)) >> (e & 31)) & kMask;
+    } else {
+#pragma unroll
+        for (int u = 0; u < kSegK; u++) ci[u] = e + u < a.nnz ? __ldcs(a.col + e + u) : 0;
+        if (e < a.nnz) bits = (__ldg(a.bits + (e >> 5)) >> (e & 31)) & kMask;
+    }
+}
+__device__ __forceinline__ void seg_load_v(const SegArgs &a, int ch, int lane, double (&v)[kSegK]) {
+    const int64_t e = (int64_t)ch * kSegChunk + kSegK * lane;
+    if (e + kSegK <= a.nnz) {
+        const double2 *vp = reinterpret_cast<const double2 *>(a.val + e);
+#pragma unroll
+        for (int u = 0; u < kSegK / 2; u++) {
+            const double2 t = __ldcs(vp + u);
+            v[2 * u] = t.x;
+            v[2 * u + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kSegK; u++) v[u] = e + u < a.nnz ? __ldcs(a.val + e + u) : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kSegThreads, kSegMinBlocks) k_spmv_seg(SegArgs a) {
+    if (aborted(a.abort)) return;
+    const double c = a.c_dev ? *a.c_dev : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kSegThreads + threadIdx.x; i < a.nempty; i += (int64_t)gridDim.x * kSegThreads) {
+        const int r = a.empty[i];
+        double s = 0.0;
+        if (a.yprev) s -= c * a.yprev[r];
+        a.y[r] = s;
+    }
+    const int lane = threadIdx.x & 31;
+    const int w = blockIdx.x * (kSegThreads / 32) + (threadIdx.x >> 5);
+    if (w < a.nranges) {
+        const int c0 = w * a.cpw, c1 = min(a.nchunks, c0 + a.cpw);
+        int open = seg_mid(a, w) ? 1 : 0;  // 0 none, 1 began before this range, 2 began in it
+        int open_k = __ldg(a.cstart + c0) - 1;
+        double carry = 0.0;
+        // the piece of the row that began before this range, if it ended here
+        // (shared memory, lane 0: keeps the chunk loop's registers free)
+        __shared__ double s_pend_own[kSegThreads / 32];
+        __shared__ int s_pend_k[kSegThreads / 32];
+        const int wl = threadIdx.x >> 5;
+        if (lane == 0) s_pend_k[wl] = -1;
+        int ci[kSegK];
+        double v[kSegK];
+        uint32_t bits_n;
+        int kb_n;
+        seg_load_ci(a, c0, lane, ci, bits_n, kb_n);
+        seg_load_v(a, c0, lane, v);
+        for (int ch = c0; ch < c1; ch++) {
+            double p[kSegK];
+#pragma unroll
+            for (int u = 0; u < kSegK; u++) p[u] = __ldg(a.x + ci[u]);
+            const uint32_t bits = bits_n;
+            const int kb = kb_n;
+            // the next chunk's index stream is in flight while the gathers return,
+            // its value stream while this chunk is reduced and the next gathers issue
+            const bool more = ch + 1 < c1;
+            if (more) seg_load_ci(a, ch + 1, lane, ci, bits_n, kb_n);
+            if constexpr (kSegFullPf) {  // both next streams in flight under the gathers
+                double vn[kSegK];
+                if (more) seg_load_v(a, ch + 1, lane, vn);
+#pragma unroll
+                for (int u = 0; u < kSegK; u++) {
+                    p[u] *= v[u];
+                    v[u] = vn[u];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kSegK; u++) p[u] *= v[u];
+                if (more) seg_load_v(a, ch + 1, lane, v);
+            }
+            // starts before this lane in the chunk (exclusive warp scan of popcounts)
+            const int cnt = __popc(bits);
+            int incl = cnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off) incl += t;
+            }
+            const int k0 = kb + incl - cnt;  // row-start index of the lane's first start
+            // in-lane pieces: head (before the first start), finished rows, tail
+            double head = 0.0, tl = 0.0;
+            int kk = k0;
+#pragma unroll
+            for (int u = 0; u < kSegK; u++) {
+                if ((bits >> u) & 1u) {
+                    if (kk > k0) seg_store(a, kk - 1, tl, c);
+                    tl = p[u];
+                    kk++;
+                } else if (kk > k0) {
+                    tl += p[u];
+                } else {
+                    head += p[u];
+                }
+            }
+            const unsigned fmask = __ballot_sync(kFull, bits != 0u);
+            // R_l = head_l + (lane l has a start ? 0 : R_{l+1}): segmented suffix sum
+            double R = head;
+            int closed = bits != 0u;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                double Rn = __shfl_down_sync(kFull, R, off);
+                int cn = __shfl_down_sync(kFull, closed, off);
+                if (lane + off >= 32) {
+                    Rn = 0.0;
+                    cn = 1;
+                }
+                if (!closed) {
+                    R += Rn;
+                    closed = cn;
+                }
+            }
+            double Rn1 = __shfl_down_sync(kFull, R, 1);
+            if (lane == 31) Rn1 = 0.0;
+            const double R0 = __shfl_sync(kFull, R, 0);
+            const double piece = tl + Rn1;  // the row begun at this lane's last start, within the chunk
+            // that row ends in a later lane of this chunk: finished
+            if (bits != 0u && lane < 31 && (fmask >> (lane + 1)) != 0u) seg_store(a, kk - 1, piece, c);
+            if (fmask) {
+                // the open row ends in this chunk, with the items before its first start
+                if (lane == 0) {
+                    if (open == 1) {  // joined at the range end (its earlier pieces are published then)
+                        s_pend_own[wl] = carry + R0;
+                        s_pend_k[wl] = open_k;
+                    } else if (open == 2) {
+                        seg_store(a, open_k, carry + R0, c);
+                    }
+                }
+                const int last = 31 - __clz(fmask);
+                carry = __shfl_sync(kFull, piece, last);
+                open_k = __shfl_sync(kFull, kk - 1, last);
+                open = 2;
+            } else {
+                carry += R0;  // the whole chunk continues the open row
+            }
+        }
+        if (lane == 0) {
+            // publish this range's piece first, then join (no waiting chain
+            // across ranges: every range publishes before it waits)
+            if (open) {
+                const int64_t bend = (int64_t)c1 * kSegChunk;
+                const bool ends = bend >= a.nnz || ((__ldg(a.bits + (bend >> 5)) >> (bend & 31)) & 1u);
+                if (ends) {
+                    if (open == 1) {
+                        s_pend_own[wl] = carry;
+                        s_pend_k[wl] = open_k;
+                    } else {
+                        seg_store(a, open_k, carry, c);
+                    }
+                } else {
+                    if (open == 1) a.head[w] = carry;
+                    else a.tail[w] = carry;
+                    seg_publish(a, w);
+                }
+            }
+            if (s_pend_k[wl] >= 0) seg_join(a, w, s_pend_k[wl], s_pend_own[wl], c);
+        }
+    }
+}
+
+// analysis: row-start bits, non-empty / empty row lists, chunk start counts
+__global__ void k_seg_bits(int64_t nrows, const int64_t *__restrict__ rp, uint32_t *bits, int32_t *nzflag) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p0 = rp[r];
+        const bool ne = rp[r + 1] > p0;
+        if (ne) atomicOr(bits + (p0 >> 5), 1u << (p0 & 31));
+        nzflag[r] = ne ? 1 : 0;
+    }
+}
+
+__global__ void k_seg_rows(int64_t nrows, const int32_t *__restrict__ nzflag, const int32_t *__restrict__ pos,
+                           int32_t *rows, int32_t *empty) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        if (nzflag[r]) rows[pos[r]] = (int32_t)r;
+        else empty[r - pos[r]] = (int32_t)r;
+    }
+}
+
+__global__ void k_seg_chunkpop(int64_t nchunks, int64_t nwords, const uint32_t *__restrict__ bits, int32_t *cnt) {
+    for (int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ch < nchunks; ch += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        for (int q = 0; q < kSegChunk / 32; q++) {
+            const int64_t wd = ch * (kSegChunk / 32) + q;
+            if (wd < nwords) s += __popc(bits[wd]);
+        }
+        cnt[ch] = s;
     }
 }
 
@@ -547,13 +721,71 @@ void csr_free(CsrOp &op) {
     op.owned.clear();
 }
 
+namespace {
+void seg_analyze(CsrOp &op, cudaStream_t s) {
+    const int64_t nrows = op.nrows, nnz = op.nnz;
+    const int64_t nwords = std::max<int64_t>(1, (nnz + 31) / 32);
+    op.seg_bits = dev_alloc<uint32_t>(op, (size_t)nwords);
+    check(cudaMemsetAsync(op.seg_bits, 0, nwords * sizeof(uint32_t), s), "memset");
+    int32_t *nzflag = nullptr, *pos = nullptr, *cnt = nullptr;
+    check(cudaMalloc(&nzflag, std::max<int64_t>(nrows, 1) * sizeof(int32_t)), "cudaMalloc");
+    check(cudaMalloc(&pos, std::max<int64_t>(nrows, 1) * sizeof(int32_t)), "cudaMalloc");
+    if (nrows > 0) k_seg_bits<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, op.row_ptr, op.seg_bits, nzflag);
+    void *tmp = nullptr;
+    size_t tb = 0, tb2 = 0;
+    const int64_t nchunks = std::max<int64_t>(1, (nnz + kSegChunk - 1) / kSegChunk);
+    check(cub::DeviceScan::ExclusiveSum(nullptr, tb, nzflag, pos, (int)std::max<int64_t>(nrows, 1), s), "scan size");
+    check(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nzflag, pos, (int)nchunks, s), "scan size");
+    check(cudaMalloc(&tmp, std::max<size_t>({tb, tb2, (size_t)1})), "cudaMalloc");
+    int64_t n_nz = 0;
+    if (nrows > 0) {
+        check(cub::DeviceScan::ExclusiveSum(tmp, tb, nzflag, pos, (int)nrows, s), "scan");
+        int32_t last[2] = {0, 0};
+        check(cudaMemcpyAsync(&last[0], pos + nrows - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
+        check(cudaMemcpyAsync(&last[1], nzflag + nrows - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
+        check(cudaStreamSynchronize(s), "sync");
+        n_nz = (int64_t)last[0] + last[1];
+    }
+    op.seg_rows = dev_alloc<int32_t>(op, (size_t)std::max<int64_t>(n_nz, 1));
+    op.seg_nempty = nrows - n_nz;
+    op.seg_empty = dev_alloc<int32_t>(op, (size_t)std::max<int64_t>(op.seg_nempty, 1));
+    if (nrows > 0) k_seg_rows<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, nzflag, pos, op.seg_rows, op.seg_empty);
+    op.seg_nchunks = nchunks;
+    op.seg_cstart = dev_alloc<int32_t>(op, (size_t)nchunks);
+    check(cudaMalloc(&cnt, nchunks * sizeof(int32_t)), "cudaMalloc");
+    k_seg_chunkpop<<<grid_for(nchunks, 256), 256, 0, s>>>(nchunks, nwords, op.seg_bits, cnt);
+    check(cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, op.seg_cstart, (int)nchunks, s), "scan");
+    // persistent grid: 3 CTAs of 8 warps per SM, a contiguous run of chunks per warp
+    int dev = 0, nsm = 148, bps = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_seg, kSegThreads, 0);
+    const int64_t warps = (int64_t)nsm * std::max(1, bps) * (kSegThreads / 32);
+    op.seg_cpw = (int)std::max<int64_t>(1, (nchunks + warps - 1) / warps);
+    op.seg_nranges = (int)((nchunks + op.seg_cpw - 1) / op.seg_cpw);
+    op.seg_grid = (op.seg_nranges + kSegThreads / 32 - 1) / (kSegThreads / 32);
+    op.seg_head = dev_alloc<double>(op, (size_t)op.seg_nranges);
+    op.seg_tail = dev_alloc<double>(op, (size_t)op.seg_nranges);
+    op.seg_flag = dev_alloc<unsigned int>(op, (size_t)op.seg_nranges);
+    check(cudaMemsetAsync(op.seg_flag, 0, op.seg_nranges * sizeof(unsigned int), s), "memset");
+
+    check(cudaStreamSynchronize(s), "sync");
+    cudaFree(tmp);
+    cudaFree(cnt);
+    cudaFree(pos);
+    cudaFree(nzflag);
+    op.seg = true;
+}
+}  // namespace
+
 void csr_analyze(CsrOp &op, cudaStream_t s) {
     unsigned long long *cnt = dev_alloc<unsigned long long>(op, 16);
     check(cudaMemsetAsync(cnt, 0, 16 * sizeof(unsigned long long), s), "memset");
     k_bin_count<<<grid_for(op.nrows, 256), 256, 0, s>>>(op.nrows, op.row_ptr, cnt);
-    unsigned long long hc[8];
+    unsigned long long hc[9];
     check(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s), "D2H");
     check(cudaStreamSynchronize(s), "sync");
+    const unsigned long long max_len = hc[8];
     int64_t off[9];
     off[0] = 0;
     for (int b = 0; b < 8; b++) off[b + 1] = off[b] + (int64_t)hc[b];
@@ -611,68 +843,20 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
         check(cudaMemcpyAsync(op.chunk_first, first.data(), (op.n_long + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s), "H2D");
         check(cudaMemcpyAsync(op.chunk_row, crow.data(), nch * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
     }
-    // nnz-balanced merge schedule for operands with long rows (CTA-per-row and
-    // chunked bins non-empty: power-law rows), where the binned launches
-    // serialize and imbalance; measured 21% faster there (config 4), 35% slower
-    // on uniform rows (config 3).  Policy SVDSC_POLICY_SPMV (1 bins, 2 merge)
-    // forces either.
-    {
-        const bool aligned = ((reinterpret_cast<uintptr_t>(op.col) & 31) == 0) &&
-                             ((reinterpret_cast<uintptr_t>(op.val) & 63) == 0);
-        const bool long_rows = off[7] > off[5];
-        const int pol = g_policy.spmv;
-        const bool want = pol == 2 ? true : (pol == 1 ? false : long_rows);
-        if (op.nnz > 0 && op.nrows < (int64_t)INT32_MAX && aligned && want) {
-            const int64_t nt = (op.nnz + kMergeTile - 1) / kMergeTile;
-            op.n_tiles = nt;
-            op.tile_r0 = dev_alloc<int32_t>(op, nt);
-            op.tile_r1 = dev_alloc<int32_t>(op, nt);
-            op.tile_head = dev_alloc<double>(op, nt);
-            op.tile_tail = dev_alloc<double>(op, nt);
-            k_merge_tiles<<<grid_for(nt, 256), 256, 0, s>>>(op.nrows, op.nnz, nt, op.row_ptr, op.tile_r0);
-            std::vector<int32_t> r0(nt);
-            std::vector<int64_t> rp0(nt);
-            check(cudaMemcpyAsync(r0.data(), op.tile_r0, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
-            check(cudaStreamSynchronize(s), "sync");
-            // rp[r0(t)] for every tile (gathered one by one is too slow for 1e5 tiles: copy row_ptr once)
-            std::vector<int64_t> hrp(op.nrows + 1);
-            check(cudaMemcpyAsync(hrp.data(), op.row_ptr, (op.nrows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
-                  "D2H");
-            check(cudaStreamSynchronize(s), "sync");
-            std::vector<int32_t> r1(nt), srow, st0, st1;
-            for (int64_t t = 0; t < nt; t++) {
-                if (t + 1 < nt) {
-                    const int64_t e = (t + 1) * kMergeTile;
-                    r1[t] = hrp[r0[t + 1]] == e ? r0[t + 1] - 1 : r0[t + 1];
-                } else {
-                    r1[t] = (int32_t)(op.nrows - 1);
-                }
-            }
-            for (int64_t t = 1; t < nt; t++) {
-                const int64_t e = t * kMergeTile;
-                if (hrp[r0[t]] < e) {  // row r0[t] continues from tile t-1
-                    if (!srow.empty() && srow.back() == r0[t]) {
-                        st1.back() = (int32_t)t;
-                    } else {
-                        srow.push_back(r0[t]);
-                        st0.push_back((int32_t)(t - 1));
-                        st1.push_back((int32_t)t);
-                    }
-                }
-            }
-            op.n_span = (int64_t)srow.size();
-            if (op.n_span) {
-                op.span_row = dev_alloc<int32_t>(op, op.n_span);
-                op.span_t0 = dev_alloc<int32_t>(op, op.n_span);
-                op.span_t1 = dev_alloc<int32_t>(op, op.n_span);
-                check(cudaMemcpyAsync(op.span_row, srow.data(), op.n_span * 4, cudaMemcpyHostToDevice, s), "H2D");
-                check(cudaMemcpyAsync(op.span_t0, st0.data(), op.n_span * 4, cudaMemcpyHostToDevice, s), "H2D");
-                check(cudaMemcpyAsync(op.span_t1, st1.data(), op.n_span * 4, cudaMemcpyHostToDevice, s), "H2D");
-            }
-            check(cudaMemcpyAsync(op.tile_r1, r1.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
-            op.merge = true;
-        }
+    // schedule choice (SVDSC_POLICY_SPMV 0 = automatic): the row-length bins for
+    // small operands and for near-uniform rows of >= 48 nonzeros (measured faster
+    // there: config 3 A and A^T 53 vs 60 us, banded config-5 A^T), else the
+    // register-segmented chunks (power-law rows, short rows: config 4 A v 696 vs
+    // 856 us (round 1's nnz tiles), A^T u 631 vs 758 us (bins))
+    bool want_seg = g_policy.spmv == 2;
+    if (g_policy.spmv == 0) {
+        const double mean = op.nrows > 0 ? (double)op.nnz / (double)op.nrows : 0.0;
+        const bool uniform = mean >= 48.0 && (double)max_len <= 1.55 * mean;
+        want_seg = op.nnz >= (1 << 20) && !uniform;
     }
+    if (want_seg && op.nnz < (int64_t)INT32_MAX &&
+        ((reinterpret_cast<uintptr_t>(op.col) & 15) == 0) && ((reinterpret_cast<uintptr_t>(op.val) & 15) == 0))
+        seg_analyze(op, s);
     check(cudaStreamSynchronize(s), "sync");
     check(cudaGetLastError(), "analyze");
 }
@@ -744,15 +928,12 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
 
 void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, const double *yprev,
               const int *abort, cudaStream_t s) {
-    if (A.merge) {
-        k_spmv_merge<<<(unsigned)A.n_tiles, 256, 0, s>>>(A.nnz, A.tile_r0, A.tile_r1, A.row_ptr, A.col, A.val, x, y,
-                                                         c_dev, yprev, A.tile_head, A.tile_tail, abort);
+    if (A.seg) {
+        SegArgs sa{A.nnz, (int)A.seg_nchunks, A.seg_cpw, A.seg_nranges, A.col, A.val, x, A.seg_bits,
+                   A.seg_rows, A.seg_cstart, A.seg_empty, A.seg_nempty, y, c_dev, yprev, A.seg_head,
+                   A.seg_tail, A.seg_flag, abort};
+        k_spmv_seg<<<A.seg_grid, kSegThreads, 0, s>>>(sa);
         count_launch();
-        if (A.n_span) {
-            k_spmv_merge_fix<<<grid_for(A.n_span, 256), 256, 0, s>>>(A.n_span, A.span_row, A.span_t0, A.span_t1,
-                                                                      A.tile_head, A.tile_tail, y, c_dev, yprev, abort);
-            count_launch();
-        }
         return;
     }
     const int64_t *o = A.bin_off;

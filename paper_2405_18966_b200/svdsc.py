@@ -72,7 +72,7 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
            "svdsc_group_create", "svdsc_group_destroy", "svdsc_comm_init_group"]
 # svdsc_set_policy keys / values (include/svdsc.h)
 POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD = 0, 1, 2
-SPMV = {"auto": 0, "bins": 1, "merge": 2}
+SPMV = {"auto": 0, "bins": 1, "seg": 2}
 CGS2 = {"auto": 0, "split": 1, "qs": 2, "stream": 3, "tma": 4, "cluster": 5}
 SMALL_SVD = {"auto": 0, "one_cta": 1}
 PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",

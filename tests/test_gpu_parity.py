@@ -85,17 +85,17 @@ def check_products(S, H, A, seed=0):
 
 
 # ---------------------------------------------------------------- a1 / a5
-@pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
+@pytest.mark.parametrize("sched", ["auto", "bins", "seg"])
 @pytest.mark.parametrize("cid,scale", [(1, 1), (3, 10), (4, 100), (5, 1000), (4, 10), (3, 2)])
 def test_products_configs(S, Hp, cid, scale, sched):
-    """Every SpMV schedule on every config: "auto" = the merge schedule on
-    power-law operands, else the row bins (svdsc_set_policy SVDSC_POLICY_SPMV)."""
+    """Every SpMV schedule on every config (svdsc_set_policy SVDSC_POLICY_SPMV):
+    "auto" picks the row bins or the segmented chunks by row statistics."""
     Hp.set_policy(spmv=sched)
     wl = W.config(cid, scale=scale)
     check_products(S, Hp, wl.A)
 
 
-@pytest.mark.parametrize("sched", ["auto", "merge", "bins"])
+@pytest.mark.parametrize("sched", ["auto", "bins", "seg"])
 def test_products_edge_cases(S, Hp, sched):
     H = Hp
     H.set_policy(spmv=sched)

@@ -41,12 +41,16 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cgs-cols", type=int, default=200)
     ap.add_argument("--skip-cgs", action="store_true")
+    ap.add_argument("--spmv", default=None, help="SpMV schedule (svdsc_set_policy): auto, bins, merge, seg")
+    ap.add_argument("--tag", default="")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     t0 = time.time()
     wl = W.config(a.workload, scale=a.scale)
     tgen = time.time() - t0
     H = S.Handle(torch.cuda.current_stream())
+    if a.spmv:
+        H.set_policy(spmv=a.spmv)
     t0 = time.time()
     M = S.Matrix.from_host(H, wl.A)
     torch.cuda.synchronize()
@@ -55,7 +59,7 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(1)
     x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
     u = torch.randn(m, device="cuda", dtype=torch.float64, generator=g)
-    out = {"workload": wl.name, "m": m, "n": n, "nnz": wl.A.nnz, "gen_s": round(tgen, 1),
+    out = {"tag": a.tag, "spmv": a.spmv, "workload": wl.name, "m": m, "n": n, "nnz": wl.A.nnz, "gen_s": round(tgen, 1),
            "analysis_s": round(tana, 2)}
     bA = wl.A.bytes_one_pass() if wl.A.kind == "dense" else 12 * wl.A.nnz + 4 * (m + 1)
     bAt = wl.A.bytes_one_pass() if wl.A.kind == "dense" else 12 * wl.A.nnz + 4 * (n + 1)
