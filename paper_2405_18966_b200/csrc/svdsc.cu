@@ -88,6 +88,8 @@ struct Prof {
             if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
                 ms[p.fam] += t;
                 calls[p.fam]++;
+            } else {
+                cudaGetLastError();
             }
             pool.push_back({p.a, nullptr, 0});
             pool.push_back({p.b, nullptr, 0});
@@ -112,6 +114,7 @@ struct svdsc_handle {
     int nranks = 1, rank = 0;
     Policy policy;               // kernel-schedule policy (svdsc_set_policy)
     cudaMemPool_t pool = nullptr;  // private pool of the library's stream-ordered allocations
+    cudaStream_t cap = nullptr;    // graph-capture stream (the caller's may be the uncapturable legacy stream)
     Ctrl *hctrl = nullptr;       // pinned host mirror of the control block
     void *scratch = nullptr;     // op-level scratch
     size_t scratch_bytes = 0;
@@ -519,29 +522,114 @@ struct Solver {
     }
 
     // runs the plan from pos; handles breakdowns; returns with the pass complete
-    void run_plan(const std::vector<Half> &plan, int c0, bool with_svd) {
+    // enqueue the plan's half-steps [pos, end) and, for a full pass, the small
+    // SVD and the convergence test.  Check indices are relative to the plan
+    // (plans have an even number of half-steps, so the amax ring parity of
+    // reading Q7 is unchanged), which makes a restart pass's kernel sequence
+    // identical from pass to pass: it is captured once into a CUDA graph and
+    // replayed (one launch per pass instead of one per kernel).
+    void enqueue_plan(const std::vector<Half> &plan, size_t pos, bool with_svd) {
+        for (size_t idx = pos; idx < plan.size(); idx++) run_half(plan[idx], (int)idx);
+        if (with_svd) {
+            H->prof.begin(6, s);
+            small_svd(t, w.T, w.ldt, w.W, w.Vw, w.Uh, w.Sh, w.Vh, k, w.ctrl, abort, w.tlog, s);
+            H->prof.end(s);
+            H->prof.begin(7, s);
+            residuals(t, k, w.T, w.ldt, w.Uh, w.Sh, o->tol, w.resid, w.ctrl, abort, s);
+            H->prof.end(s);
+        }
+    }
+
+    cudaGraphExec_t gexec = nullptr;  // the restart pass (captured at its first use)
+    bool graph_ok = true;
+    unsigned int graph_launch_base = 0;  // fused-launch counter at the capture's start
+    int64_t graph_kernels = 0, graph_bytes_model = 0, graph_bytes_reorth = 0, graph_matvecs = 0, graph_steps = 0,
+            graph_reorth_halves = 0;
+
+    bool replay_restart_plan(const std::vector<Half> &plan) {
+        // (not while profiling: event records inside a stream capture failed on
+        // this driver -- cudaErrorIllegalState -- so profiled solves run eagerly)
+        if (!graph_ok || P != 1 || H->prof.on) return false;
+        if (!gexec) {
+            // capture: the barrier-slot ring is zeroed at the graph's start, so a
+            // replay does not depend on the slots the previous launches left
+            const unsigned int fl0 = fused_launches;
+            const int64_t l0 = g_launches, b0 = bytes_model, r0 = bytes_reorth, mv0 = matvecs, st0 = steps,
+                          rh0 = reorth_halves;
+            if (!H->cap && cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                graph_ok = false;
+                return false;
+            }
+            const cudaStream_t s_user = s;
+            s = H->cap;  // enqueue into the capture
+            if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                cudaGetLastError();
+                s = s_user;
+                graph_ok = false;
+                return false;
+            }
+            bool ok = true;
+            try {
+                fused_launches = 0;
+                ck(cudaMemsetAsync(w.ctrl->gflags, 0, sizeof(w.ctrl->gflags), s), "memset slots");
+                enqueue_plan(plan, 0, true);
+            } catch (...) {
+                ok = false;
+            }
+            cudaGraph_t g = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(s, &g);
+            s = s_user;
+            if (ok && ec == cudaSuccess && g && cudaGraphInstantiate(&gexec, g, 0) == cudaSuccess) {
+                cudaGraphDestroy(g);
+            } else {
+                if (g) cudaGraphDestroy(g);
+                gexec = nullptr;
+                cudaGetLastError();
+                graph_ok = false;
+                fused_launches = fl0;
+                g_launches = l0, bytes_model = b0, bytes_reorth = r0, matvecs = mv0, steps = st0;
+                reorth_halves = rh0;
+                return false;
+            }
+            graph_launch_base = fused_launches;  // launches inside the graph (from 0)
+            fused_launches = fl0;  // nothing ran yet: the host bookkeeping is redone per replay below
+            graph_kernels = g_launches - l0;
+            graph_bytes_model = bytes_model - b0, graph_bytes_reorth = bytes_reorth - r0;
+            graph_matvecs = matvecs - mv0, graph_steps = steps - st0, graph_reorth_halves = reorth_halves - rh0;
+            g_launches = l0, bytes_model = b0, bytes_reorth = r0, matvecs = mv0, steps = st0, reorth_halves = rh0;
+        }
+        ck(cudaGraphLaunch(gexec, s), "cudaGraphLaunch");
+        // the graph's launches used barrier slots 1..graph_launch_base and zeroed
+        // the next one: eager launches after it continue from there
+        fused_launches = graph_launch_base;
+        g_launches += graph_kernels;
+        bytes_model += graph_bytes_model, bytes_reorth += graph_bytes_reorth;
+        matvecs += graph_matvecs, steps += graph_steps, reorth_halves += graph_reorth_halves;
+        return true;
+    }
+
+    // runs the plan; handles breakdowns; returns with the pass complete
+    void run_plan(const std::vector<Half> &plan, bool with_svd, bool restart_plan) {
         size_t pos = 0;
         for (;;) {
-            for (size_t idx = pos; idx < plan.size(); idx++) run_half(plan[idx], c0 + (int)idx);
-            if (with_svd) {
-                H->prof.begin(6, s);
-                small_svd(t, w.T, w.ldt, w.W, w.Vw, w.Uh, w.Sh, w.Vh, k, w.ctrl, abort, w.tlog, s);
-                H->prof.end(s);
-                H->prof.begin(7, s);
-                residuals(t, k, w.T, w.ldt, w.Uh, w.Sh, o->tol, w.resid, w.ctrl, abort, s);
-                H->prof.end(s);
-            }
+            if (!(pos == 0 && restart_plan && with_svd && replay_restart_plan(plan)))
+                enqueue_plan(plan, pos, with_svd);
             Ctrl c = read_ctrl();
             if (!c.abort) return;
-            const int idx = c.abort_check - c0;
+            const int idx = c.abort_check;
             if (idx < 0 || idx >= (int)plan.size()) throw SvdscError(SVDSC_ECUDA, "breakdown bookkeeping");
             const int zero[2] = {0, 0};
             ck(cudaMemcpyAsync(&w.ctrl->abort, &zero[0], sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
             ck(cudaMemcpyAsync(&w.ctrl->abort_kind, &zero[1], sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-            if (c.abort_kind == 1) fix_norm(plan[idx], c0 + idx);
+            if (c.abort_kind == 1) fix_norm(plan[idx], idx);
             else fix(plan[idx]);
             pos = idx + 1;
         }
+    }
+
+    ~Solver() {
+        if (gexec) cudaGraphExecDestroy(gexec);
     }
 
     svdsc_status solve(void *ws_base, double *S, double *Uout, int64_t ldu_out, double *Vout, int64_t ldv_out,
@@ -586,10 +674,10 @@ struct Solver {
             plan.push_back({1, i});
             if (i < t) plan.push_back({2, i});  // u_{t+1} is not needed (reading Q2)
         }
-        int c0 = 0, passes = 0;
+        int passes = 0;
         Ctrl c{};
         if (lbp_only) {
-            run_plan(plan, c0, false);
+            run_plan(plan, false, false);
             for (int j = 0; j <= t; j++) {
                 ck(cudaMemcpyAsync(Uout + (int64_t)j * ldu_out, Ucol(j), m * sizeof(double), cudaMemcpyDeviceToDevice, s),
                    "copy U");
@@ -601,7 +689,7 @@ struct Solver {
             passes = 1;
         } else {
             for (;;) {
-                run_plan(plan, c0, true);
+                run_plan(plan, true, passes > 0);
                 c = *H->hctrl;
                 if (c.svd_status != 0) throw SvdscError(SVDSC_ESVD_NOCONV, "small Jacobi SVD did not converge in 50 sweeps");
                 if (c.rankdef) throw SvdscError(SVDSC_ERANKDEF, "zero Ritz value with non-negligible residual");
@@ -622,7 +710,6 @@ struct Solver {
                 }
                 H->prof.end(s);
                 matvecs += 0;
-                c0 += (int)plan.size();
                 plan.clear();
                 plan.push_back({3, 0});
                 for (int i = k + 1; i <= t; i++) {
@@ -811,6 +898,7 @@ void svdsc_destroy(svdsc_handle *h) {
     if (!h) return;
     cudaStreamSynchronize(h->stream);
     delete h->comm;
+    if (h->cap) cudaStreamDestroy(h->cap);
     if (h->hctrl) cudaFreeHost(h->hctrl);
     if (h->scratch) cudaFree(h->scratch);
     if (h->pool) cudaMemPoolDestroy(h->pool);

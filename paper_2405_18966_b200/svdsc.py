@@ -353,10 +353,18 @@ def workspace_size(M: Matrix, k, t=None, tol=1e-10, maxit=100) -> int:
 
 
 def svds_c_host(h: Handle, A, k, tol=1e-10, maxit=100, t=None, seed=0, v0=None, fixed_passes=0,
-                reorth=2):
-    """End-to-end with HOST buffers (svdsc_solve_host_*): numpy in, numpy out."""
+                reorth=2, out=None):
+    """End-to-end with HOST buffers (svdsc_solve_host_*): numpy in, numpy out.
+    out: optional (S[k], U[k, m], V[k, n], R[k]) host arrays to fill (e.g. views
+    of pinned memory: device-to-host copies into pageable memory are several
+    times slower); U / V are returned transposed views (column-major m x k)."""
     m, n = A.m, A.n
-    S, U, V, R = (np.zeros(k), np.zeros((k, m)), np.zeros((k, n)), np.zeros(k))
+    if out is None:
+        S, U, V, R = (np.zeros(k), np.zeros((k, m)), np.zeros((k, n)), np.zeros(k))
+    else:
+        S, U, V, R = out
+        assert S.shape == (k,) and U.shape == (k, m) and V.shape == (k, n) and R.shape == (k,)
+        assert all(x.dtype == np.float64 and x.flags.c_contiguous for x in (S, U, V, R))
     v0h = None if v0 is None else np.ascontiguousarray(v0, np.float64)
     o = Opts(k=k, tol=tol, t=t or 0, maxit=maxit, seed=seed,
              v0=None if v0h is None else v0h.ctypes.data, fixed_passes=fixed_passes, reorth=reorth)
