@@ -182,6 +182,108 @@ def relaunch_distributed(args_list, n):
     return subprocess.call(cmd)
 
 
+def run_loopback(args):
+    """--comm loopback: N ranks as threads of this process (svdsc_group_*), each
+    with its own handle, stream, rank-local rows and device (rank % visible).
+    Same workload recipe, partition and max-over-ranks timing as the NCCL path;
+    the collectives synchronize on the host, so the number is not a scaling
+    measurement (the line says so)."""
+    import numpy as np
+    import torch
+
+    import workloads as W
+    from paper_2405_18966_b200 import build as B
+    from paper_2405_18966_b200 import svdsc as S
+    B.build()
+    P, cid = args.gpus, args.workload
+    ndev = max(1, torch.cuda.device_count())
+    deg = W.degrees(cid)
+    if deg is not None:
+        rp = np.zeros(deg.size + 1, dtype=np.int64)
+        rp[1:] = np.cumsum(deg)
+        kt = {3: (100, 300), 4: (100, 300), 5: (200, 600)}[cid]
+        bounds = S.partition_rows(rp, (kt[0] + kt[1]) // 2, P)
+        m_global, nnz_global, full = int(deg.size), int(rp[-1]), None
+    else:
+        full = W.config(cid)
+        m_global, nnz_global = full.A.m, full.A.nnz
+        bounds = (S.partition_rows(full.A.row_ptr, (full.k + full.t) // 2, P) if full.A.kind == "csr"
+                  else np.linspace(0, full.A.m, P + 1).astype(np.int64))
+    g = S.Group(P)
+    res = [None] * P
+    barrier = threading.Barrier(P)
+
+    def rank_main(r):
+        try:
+            dev = r % ndev
+            torch.cuda.set_device(dev)
+            st = torch.cuda.Stream(device=dev)
+            r0, r1 = int(bounds[r]), int(bounds[r + 1])
+            if full is None:
+                wl = W.config(cid, r0=r0, r1=r1)
+                Al = wl.A
+            else:
+                wl = full
+                A = full.A
+                if A.kind == "csr":
+                    Al = W.Matrix("csr", r1 - r0, A.n, row_ptr=A.row_ptr[r0:r1 + 1] - A.row_ptr[r0],
+                                  col_idx=A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]],
+                                  values=A.values[A.row_ptr[r0]:A.row_ptr[r1]])
+                else:
+                    Al = W.dense_matrix(np.ascontiguousarray(A.dense[r0:r1]))
+            with torch.cuda.stream(st):
+                h = S.Handle(st)
+                h.comm_init_group(g, r)
+                M = S.Matrix.from_host(h, Al, row_offset=r0, m_global=m_global)
+                v0 = torch.from_numpy(wl.v0).cuda()
+                ws = torch.empty(S.workspace_size(M, wl.k, t=wl.t), dtype=torch.uint8, device="cuda")
+
+                def solve():
+                    return S.svds_c(M, wl.k, tol=wl.tol, maxit=wl.maxit, t=wl.t, v0=v0, workspace=ws)
+
+                for _ in range(args.warmup):
+                    solve()
+                st.synchronize()
+                barrier.wait()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                steps, passes = 0, []
+                for _ in range(args.steps):
+                    out = solve()
+                    steps += out.info["steps"]
+                    passes.append(out.info["passes"])
+                e1.record(st)
+                st.synchronize()
+                res[r] = (e0.elapsed_time(e1), steps, passes, out.S.cpu().numpy(), wl.name, wl.k, wl.t, Al.n)
+        except Exception as e:  # noqa: BLE001
+            res[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t_ in th:
+        t_.start()
+    for t_ in th:
+        t_.join()
+    g.close()
+    for x in res:
+        if isinstance(x, Exception):
+            raise x
+    ms = max(x[0] for x in res)
+    _, steps, passes, s0, name, k, t, n = res[0]
+    same = all(np.array_equal(x[3], s0) for x in res)
+    print(json.dumps({
+        "metric": METRIC, "value": steps / (ms / 1e3), "unit": "steps/s", "n_gpus": P, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "comm": f"loopback: {P} ranks as threads on {min(P, ndev)} GPU(s), host-synchronized collectives "
+                "(a test of the multi-rank path, not a scaling measurement)",
+        "config": {"workload": name, "m": m_global, "n": n, "nnz": nnz_global, "k": k, "t": t,
+                   "passes_per_solve": passes, "parallelism": f"rows{P}",
+                   "rows_per_rank": [int(bounds[r + 1] - bounds[r]) for r in range(P)]},
+        "sigma_identical_on_all_ranks": same, "sigma_1": float(s0[0]),
+    }), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -192,6 +294,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "loopback"],
+                    help="nccl: one process per GPU (the product path); loopback: --gpus N ranks as threads "
+                         "of this process on the visible GPUs (round robin), host-synchronized collectives "
+                         "-- exercises the multi-rank path on one GPU, not a scaling measurement")
     ap.add_argument("--reorth", type=int, default=2, choices=[1, 2],
                     help="2: full CGS2 every half-step (the paper's method, the headline); "
                          "1: partial re-orthogonalization (DESIGN.md Q20, SURVEY 8(f4)), an extra line")
@@ -200,6 +306,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and args.comm == "loopback":
+        return run_loopback(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch_distributed(sys.argv[1:], args.gpus)
 

@@ -2,7 +2,9 @@
 (SURVEY.md 8(e)).  The NCCL kernels cannot run here, so this pins the pieces
 that are host logic or pure math:
 
-  * the C++ partitioner + rank-local slicing used by bench.py cover A exactly;
+  * the C++ partitioner + rank-local slicing used by bench.py cover A exactly,
+    and bench.py's rank-local generation (workloads.degrees + config(r0, r1):
+    every rank generates only its rows) equals the rows of the global matrix;
   * the NCCL unique-id bootstrap broadcast (svdsc_comm_unique_id -> gloo);
   * the collective schedule the C++ driver issues per Lanczos step -- reduce-
     scatter of the partial A^T u, all-gather of v, all-reduces of the CGS2
@@ -70,6 +72,19 @@ def _worker(rank, world, port, q):
         np.add.at(Dl, (rows, col.astype(np.int64)), val)
         out["local_ok"] = bool(np.array_equal(Dl, D[r0:r1]))
 
+        # --- bench.py --gpus N: rank-local generation of a power-law config
+        deg = W.degrees(4, scale=100)
+        rpg = np.zeros(deg.size + 1, dtype=np.int64)
+        rpg[1:] = np.cumsum(deg)
+        bb = S.partition_rows(rpg, 200, world)
+        g0, g1 = int(bb[rank]), int(bb[rank + 1])
+        loc = W.config(4, scale=100, r0=g0, r1=g1).A
+        glob = W.config(4, scale=100).A
+        out["gen_rows"] = (g0, g1, int(bb[-1]))
+        out["gen_ok"] = bool(np.array_equal(loc.row_ptr, glob.row_ptr[g0:g1 + 1] - glob.row_ptr[g0]) and
+                             np.array_equal(loc.col_idx, glob.col_idx[glob.row_ptr[g0]:glob.row_ptr[g1]]) and
+                             np.array_equal(loc.values, glob.values[glob.row_ptr[g0]:glob.row_ptr[g1]]))
+
         # --- the per-step collective schedule of the C++ driver (P > 1)
         n, m_loc = A.n, r1 - r0
         n_pad, ns = _slices(n, world)
@@ -101,7 +116,7 @@ def _worker(rank, world, port, q):
             h2, nrmp = red[:-1], red[-1]
             wpp = wp - Q @ h2
             beta2 = nrmp - h2 @ h2
-            if not beta2 > 0.5 * nrmp:  # explicit norm fallback
+            if not beta2 > 0.5 * nrmp:  # explicit norm (the pass-end repair, reading G3)
                 beta2 = allreduce(np.array([wpp @ wpp]))[0]
             return wpp, np.sqrt(beta2)
 
@@ -161,6 +176,12 @@ def test_partition_covers_rows(results):
     (a0, a1), (b0, b1) = results[0]["rows"], results[1]["rows"]
     assert a0 == 0 and a1 == b0 and b1 == wl.A.m
     assert results[0]["local_ok"] and results[1]["local_ok"]
+
+
+def test_rank_local_generation(results):
+    (a0, a1, m), (b0, b1, m2) = results[0]["gen_rows"], results[1]["gen_rows"]
+    assert a0 == 0 and a1 == b0 and b1 == m == m2
+    assert results[0]["gen_ok"] and results[1]["gen_ok"]
 
 
 def test_distributed_schedule_matches_oracle(results):
