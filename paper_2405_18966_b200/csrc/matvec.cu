@@ -356,12 +356,37 @@ __device__ __forceinline__ void seg_join(const SegArgs &a, int w, int k, double 
 
 // one lane's kSegK consecutive nonzeros of a chunk: column indices, row-start
 // bits and the chunk's row-start offset (seg_load_ci), values (seg_load_v)
+// The chunk's row-start bits are kSegK whole words (the bitmap is padded to
+// whole chunks): every lane reads them (one broadcast 128-bit load per 4
+// words) and takes its own kSegK bits and the count of starts before them --
+// no warp scan for the row-start offsets.
 __device__ __forceinline__ void seg_load_ci(const SegArgs &a, int ch, int lane, int (&ci)[kSegK], uint32_t &bits,
                                             int &kb) {
     constexpr uint32_t kMask = (1u << kSegK) - 1u;
+    constexpr int kLanesPerWord = 32 / kSegK;
     const int64_t e = (int64_t)ch * kSegChunk + kSegK * lane;
-    bits = 0;
-    kb = __ldg(a.cstart + ch);
+    {
+        uint32_t wd[kSegK];
+        const uint4 *bp = reinterpret_cast<const uint4 *>(a.bits + (int64_t)ch * kSegK);
+#pragma unroll
+        for (int q = 0; q < kSegK / 4; q++) {
+            const uint4 t = __ldg(bp + q);
+            wd[4 * q] = t.x;
+            wd[4 * q + 1] = t.y;
+            wd[4 * q + 2] = t.z;
+            wd[4 * q + 3] = t.w;
+        }
+        const int myw = lane / kLanesPerWord, sh = kSegK * (lane % kLanesPerWord);
+        int before = 0;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int q = 0; q < kSegK; q++) {
+            if (q < myw) before += __popc(wd[q]);
+            if (q == myw) mine = wd[q];
+        }
+        bits = (mine >> sh) & kMask;
+        kb = __ldg(a.cstart + ch) + before + __popc(mine & ((1u << sh) - 1u));  // starts before this lane
+    }
     if (e + kSegK <= a.nnz) {
         const int4 *cp = reinterpret_cast<const int4 *>(a.col + e);
 #pragma unroll
@@ -372,11 +397,9 @@ __device__ __forceinline__ void seg_load_ci(const SegArgs &a, int ch, int lane, 
             ci[4 * q + 2] = t.z;
             ci[4 * q + 3] = t.w;
         }
-        bits = (__ldg(a.bits + (e >> 5)) >> (e & 31)) & kMask;
     } else {
 #pragma unroll
         for (int u = 0; u < kSegK; u++) ci[u] = e + u < a.nnz ? __ldcs(a.col + e + u) : 0;
-        if (e < a.nnz) bits = (__ldg(a.bits + (e >> 5)) >> (e & 31)) & kMask;
     }
 }
 __device__ __forceinline__ void seg_load_v(const SegArgs &a, int ch, int lane, double (&v)[kSegK]) {
@@ -447,14 +470,7 @@ __global__ void __launch_bounds__(kSegThreads, kSegMinBlocks) k_spmv_seg(SegArgs
                 if (more) seg_load_v(a, ch + 1, lane, v);
             }
             // starts before this lane in the chunk (exclusive warp scan of popcounts)
-            const int cnt = __popc(bits);
-            int incl = cnt;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int t = __shfl_up_sync(kFull, incl, off);
-                if (lane >= off) incl += t;
-            }
-            const int k0 = kb + incl - cnt;  // row-start index of the lane's first start
+            const int k0 = kb;  // row-start index of the lane's first start
             // in-lane pieces: head (before the first start), finished rows, tail
             double head = 0.0, tl = 0.0;
             int kk = k0;
@@ -472,24 +488,18 @@ __global__ void __launch_bounds__(kSegThreads, kSegMinBlocks) k_spmv_seg(SegArgs
             }
             const unsigned fmask = __ballot_sync(kFull, bits != 0u);
             // R_l = head_l + (lane l has a start ? 0 : R_{l+1}): segmented suffix sum
+            // (Hillis-Steele; the segment flags of a window come from the ballot)
             double R = head;
-            int closed = bits != 0u;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 double Rn = __shfl_down_sync(kFull, R, off);
-                int cn = __shfl_down_sync(kFull, closed, off);
-                if (lane + off >= 32) {
-                    Rn = 0.0;
-                    cn = 1;
-                }
-                if (!closed) {
-                    R += Rn;
-                    closed = cn;
-                }
+                // closed: a start in lanes [lane, lane + off), or the window passes lane 31
+                const bool closed = lane + off >= 32 || ((fmask >> lane) & ((1u << off) - 1u)) != 0u;
+                if (!closed) R += Rn;
             }
             double Rn1 = __shfl_down_sync(kFull, R, 1);
             if (lane == 31) Rn1 = 0.0;
-            const double R0 = __shfl_sync(kFull, R, 0);
+            // (carry, open and open_k are lane 0's: R_0 is its own R, no broadcast)
             const double piece = tl + Rn1;  // the row begun at this lane's last start, within the chunk
             // that row ends in a later lane of this chunk: finished
             if (bits != 0u && lane < 31 && (fmask >> (lane + 1)) != 0u) seg_store(a, kk - 1, piece, c);
@@ -497,10 +507,10 @@ __global__ void __launch_bounds__(kSegThreads, kSegMinBlocks) k_spmv_seg(SegArgs
                 // the open row ends in this chunk, with the items before its first start
                 if (lane == 0) {
                     if (open == 1) {  // joined at the range end (its earlier pieces are published then)
-                        s_pend_own[wl] = carry + R0;
+                        s_pend_own[wl] = carry + R;
                         s_pend_k[wl] = open_k;
                     } else if (open == 2) {
-                        seg_store(a, open_k, carry + R0, c);
+                        seg_store(a, open_k, carry + R, c);
                     }
                 }
                 const int last = 31 - __clz(fmask);
@@ -508,7 +518,7 @@ __global__ void __launch_bounds__(kSegThreads, kSegMinBlocks) k_spmv_seg(SegArgs
                 open_k = __shfl_sync(kFull, kk - 1, last);
                 open = 2;
             } else {
-                carry += R0;  // the whole chunk continues the open row
+                carry += R;  // (lane 0: R_0, the whole chunk) continues the open row
             }
         }
         if (lane == 0) {
@@ -724,7 +734,8 @@ void csr_free(CsrOp &op) {
 namespace {
 void seg_analyze(CsrOp &op, cudaStream_t s) {
     const int64_t nrows = op.nrows, nnz = op.nnz;
-    const int64_t nwords = std::max<int64_t>(1, (nnz + 31) / 32);
+    const int64_t nchunks0 = std::max<int64_t>(1, (nnz + kSegChunk - 1) / kSegChunk);
+    const int64_t nwords = nchunks0 * kSegK;  // whole chunks (the kernel reads a chunk's words at once)
     op.seg_bits = dev_alloc<uint32_t>(op, (size_t)nwords);
     check(cudaMemsetAsync(op.seg_bits, 0, nwords * sizeof(uint32_t), s), "memset");
     int32_t *nzflag = nullptr, *pos = nullptr, *cnt = nullptr;
