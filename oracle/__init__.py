@@ -81,6 +81,8 @@ def lib():
         L.or_pro_anorm.restype = D
         L.or_pro_nu_update.argtypes = [P, I64, I64, P, P, D, D]
         L.or_pro_mu_update.argtypes = [P, I64, I64, P, P, D, D]
+        L.or_pro_restart.argtypes = [I64, I64, P, P, P, P]
+        L.or_pro_restart.restype = None
         _lib = L
     return _lib
 
@@ -242,6 +244,18 @@ def pro_nu_update(T, i, mu, nu, beta, eps1):
     out[:len(nu)] = nu
     lib().or_pro_nu_update(T.ctypes.data, T.shape[0], i, _p(mu), _p(out), beta, eps1)
     return out[:i + 1]
+
+
+def pro_restart(t, k, Vh, nu, mu):
+    """or_pro_restart: the omega rows after an augmented restart (reading Q20)"""
+    Vh = np.asfortranarray(Vh, dtype=np.float64)
+    nu_o = np.zeros(t + 1)
+    nu_o[:len(nu)] = nu
+    mu_o = np.zeros(t + 1)
+    mu_o[:len(mu)] = mu
+    tmp = np.zeros(max(k, 1))
+    lib().or_pro_restart(t, k, Vh.ctypes.data, _p(nu_o), _p(mu_o), _p(tmp))
+    return nu_o[:k + 1], mu_o[:k + 1]
 
 
 def pro_mu_update(T, i, nu, mu, alpha, eps1):

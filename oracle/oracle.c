@@ -452,18 +452,22 @@ static int pro_u(or_state *S, int64_t i, const double *z) {
 
 /* After the restart (Alg. 2 steps 8-11): V(:,0:k-1) = V(:,0:t-1) Vh(:,0:k-1)
  * and v_k = old v_t, so v_k^T v~_j = sum_l (v_t^T v_l) Vh(l,j); u_k was
- * re-orthogonalized in full, so its row is eps. */
-static void pro_restart(or_state *S, int64_t k, const double *Vh) {
-    int64_t t = S->t;
+ * re-orthogonalized in full, so its row is eps.  nu / mu:
+ * length >= t+1 (in place), Vh: t x t column-major, tmp: k doubles. */
+void or_pro_restart(int64_t t, int64_t k, const double *Vh, double *nu, double *mu, double *tmp) {
     for (int64_t j = 0; j < k; j++) {
         double s = 0.0;
-        for (int64_t l = 0; l < t; l++) s += S->nu[l] * Vh[l + j * t];
-        S->tmp[j] = s;
+        for (int64_t l = 0; l < t; l++) s += nu[l] * Vh[l + j * t];
+        tmp[j] = s;
     }
-    for (int64_t j = 0; j < k; j++) S->nu[j] = S->tmp[j];
-    S->nu[k] = 1.0;
-    for (int64_t j = 0; j < k; j++) S->mu[j] = OR_EPS;
-    S->mu[k] = 1.0;
+    for (int64_t j = 0; j < k; j++) nu[j] = tmp[j];
+    nu[k] = 1.0;
+    for (int64_t j = 0; j < k; j++) mu[j] = OR_EPS;
+    mu[k] = 1.0;
+}
+
+static void pro_restart(or_state *S, int64_t k, const double *Vh) {
+    or_pro_restart(S->t, k, Vh, S->nu, S->mu, S->tmp);
     S->force_u = S->force_v = 0;
 }
 

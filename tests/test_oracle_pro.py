@@ -161,3 +161,26 @@ def test_pro_svds_closed_form_decay2_and_config1():
     assert a.converged and b.converged
     assert np.abs(a.S - b.S).max() <= 1e-12 * b.S[0]
     assert a.reorths < 0.2 * b.reorths
+
+
+@pytest.mark.parametrize("t,k", [(60, 20), (31, 10), (12, 1)])
+def test_pro_restart_against_inner_products(t, k):
+    """or_pro_restart (the omega rows after an augmented restart, reading Q20):
+    with V holding real Lanczos vectors that lost orthogonality and Vh a
+    non-symmetric orthogonal t x t matrix, the new row of v_{k+1} = old v_{t+1}
+    must equal the brute-force inner products v_{t+1}^T (V(:, 1:t) Vh(:, j))
+    with the Ritz vectors Ṽ_k (Alg. 2 step 8); the row of u_{k+1}, which is
+    re-orthogonalized in full, is eps, both diagonals are 1.
+    A transposed Vh, a wrong column range or a dropped term fails."""
+    A = decay2()
+    U, V, T, _ = O.lbp(A, t, np.random.default_rng(t).standard_normal(A.n), reorth=0)
+    nu = V[:, :t].T @ V[:, t]                       # row of the newest vector, brute force
+    assert np.abs(nu).max() > 1e-6                 # orthogonality really lost (not all ~eps)
+    Vh = np.linalg.qr(np.random.default_rng(k).standard_normal((t, t)))[0]
+    assert np.abs(Vh - Vh.T).max() > 0.1
+    nu_new, mu_new = O.pro_restart(t, k, Vh, nu, np.full(t, 0.5))
+    ritz = V[:, :t] @ Vh[:, :k]                    # Ṽ_k
+    true = ritz.T @ V[:, t]
+    assert np.abs(nu_new[:k] - true).max() <= 1e-12 * max(1.0, np.abs(true).max())
+    assert nu_new[k] == 1.0 and mu_new[k] == 1.0
+    assert np.all(mu_new[:k] == EPS)
