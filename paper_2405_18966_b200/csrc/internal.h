@@ -71,6 +71,8 @@ struct CsrOp {
     unsigned int *seg_flag = nullptr;  // per warp range: 1 once its partial is published (reset by the joiner)
     bool seg = false;                  // use the seg schedule for this operand
     std::vector<void *> owned;         // allocations owned by this operand
+    cudaStream_t free_stream = nullptr;  // stream of its pool allocations (g_pool at analysis)
+    bool pooled = false;
 };
 #ifndef SVDSC_SEG_K
 #define SVDSC_SEG_K 4
@@ -237,6 +239,17 @@ struct Policy {
     int small_svd = 0;  // SVDSC_POLICY_SMALL_SVD
 };
 extern thread_local Policy g_policy;
+
+// ---- matrix analysis allocations -------------------------------------------------
+// Set by the C ABI around matrix analysis: the handle's private memory pool and
+// stream, so derived structures (CSC copy, bins, seg tables) and the analysis
+// temporaries come from pooled memory (a host-buffer solve creates and
+// destroys its matrix every call: cudaMalloc / cudaFree of the 1.8 GB CSC copy
+// of BASELINE config 4 cost tens of ms each time).  NULL: cudaMalloc.
+extern thread_local cudaMemPool_t g_pool;
+extern thread_local cudaStream_t g_pool_stream;
+void *analysis_alloc(size_t bytes);
+void analysis_free(void *p);
 
 // ---- launch bookkeeping ----------------------------------------------------------
 extern thread_local int64_t g_launches;

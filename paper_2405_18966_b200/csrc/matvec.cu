@@ -30,6 +30,21 @@ namespace svdsc {
 
 thread_local int64_t g_launches = 0;
 thread_local Policy g_policy;
+thread_local cudaMemPool_t g_pool = nullptr;
+thread_local cudaStream_t g_pool_stream = nullptr;
+
+void *analysis_alloc(size_t bytes) {
+    void *p = nullptr;
+    bytes = std::max<size_t>(bytes, 8);
+    const cudaError_t e = g_pool ? cudaMallocFromPoolAsync(&p, bytes, g_pool, g_pool_stream) : cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("analysis allocation: ") + cudaGetErrorString(e));
+    return p;
+}
+void analysis_free(void *p) {
+    if (!p) return;
+    if (g_pool) cudaFreeAsync(p, g_pool_stream);
+    else cudaFree(p);
+}
 
 namespace {
 
@@ -711,9 +726,10 @@ inline void check(cudaError_t e, const char *what) {
 
 template <typename T>
 T *dev_alloc(CsrOp &op, size_t n) {
-    void *p = nullptr;
-    check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    void *p = analysis_alloc(std::max<size_t>(n, 1) * sizeof(T));
     op.owned.push_back(p);
+    op.pooled = g_pool != nullptr;
+    op.free_stream = g_pool_stream;
     return (T *)p;
 }
 
@@ -727,7 +743,10 @@ int grid_for(int64_t work, int threads, int cap = 148 * 16) {
 }  // namespace
 
 void csr_free(CsrOp &op) {
-    for (void *p : op.owned) cudaFree(p);
+    for (void *p : op.owned) {
+        if (op.pooled) cudaFreeAsync(p, op.free_stream);
+        else cudaFree(p);
+    }
     op.owned.clear();
 }
 
@@ -739,15 +758,15 @@ void seg_analyze(CsrOp &op, cudaStream_t s) {
     op.seg_bits = dev_alloc<uint32_t>(op, (size_t)nwords);
     check(cudaMemsetAsync(op.seg_bits, 0, nwords * sizeof(uint32_t), s), "memset");
     int32_t *nzflag = nullptr, *pos = nullptr, *cnt = nullptr;
-    check(cudaMalloc(&nzflag, std::max<int64_t>(nrows, 1) * sizeof(int32_t)), "cudaMalloc");
-    check(cudaMalloc(&pos, std::max<int64_t>(nrows, 1) * sizeof(int32_t)), "cudaMalloc");
+    nzflag = reinterpret_cast<decltype(nzflag)>(analysis_alloc(std::max<int64_t>(nrows, 1) * sizeof(int32_t)));
+    pos = reinterpret_cast<decltype(pos)>(analysis_alloc(std::max<int64_t>(nrows, 1) * sizeof(int32_t)));
     if (nrows > 0) k_seg_bits<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, op.row_ptr, op.seg_bits, nzflag);
     void *tmp = nullptr;
     size_t tb = 0, tb2 = 0;
     const int64_t nchunks = std::max<int64_t>(1, (nnz + kSegChunk - 1) / kSegChunk);
     check(cub::DeviceScan::ExclusiveSum(nullptr, tb, nzflag, pos, (int)std::max<int64_t>(nrows, 1), s), "scan size");
     check(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nzflag, pos, (int)nchunks, s), "scan size");
-    check(cudaMalloc(&tmp, std::max<size_t>({tb, tb2, (size_t)1})), "cudaMalloc");
+    tmp = reinterpret_cast<decltype(tmp)>(analysis_alloc(std::max<size_t>({tb, tb2, (size_t)1})));
     int64_t n_nz = 0;
     if (nrows > 0) {
         check(cub::DeviceScan::ExclusiveSum(tmp, tb, nzflag, pos, (int)nrows, s), "scan");
@@ -763,7 +782,7 @@ void seg_analyze(CsrOp &op, cudaStream_t s) {
     if (nrows > 0) k_seg_rows<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, nzflag, pos, op.seg_rows, op.seg_empty);
     op.seg_nchunks = nchunks;
     op.seg_cstart = dev_alloc<int32_t>(op, (size_t)nchunks);
-    check(cudaMalloc(&cnt, nchunks * sizeof(int32_t)), "cudaMalloc");
+    cnt = reinterpret_cast<decltype(cnt)>(analysis_alloc(nchunks * sizeof(int32_t)));
     k_seg_chunkpop<<<grid_for(nchunks, 256), 256, 0, s>>>(nchunks, nwords, op.seg_bits, cnt);
     check(cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, op.seg_cstart, (int)nchunks, s), "scan");
     // persistent grid: 3 CTAs of 8 warps per SM, a contiguous run of chunks per warp
@@ -781,10 +800,10 @@ void seg_analyze(CsrOp &op, cudaStream_t s) {
     check(cudaMemsetAsync(op.seg_flag, 0, op.seg_nranges * sizeof(unsigned int), s), "memset");
 
     check(cudaStreamSynchronize(s), "sync");
-    cudaFree(tmp);
-    cudaFree(cnt);
-    cudaFree(pos);
-    cudaFree(nzflag);
+    analysis_free(tmp);
+    analysis_free(cnt);
+    analysis_free(pos);
+    analysis_free(nzflag);
     op.seg = true;
 }
 }  // namespace
@@ -810,17 +829,17 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
         const int n32 = (int)op.nrows;
         check(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, ids, op.bin_rows, n32, 0, 3, s),
               "radix sort size");
-        check(cudaMalloc(&k_in, std::max<int64_t>(op.nrows, 1) * 2), "cudaMalloc");
+        k_in = reinterpret_cast<decltype(k_in)>(analysis_alloc(std::max<int64_t>(op.nrows, 1) * 2));
         k_out = k_in + std::max<int64_t>(op.nrows, 1);
-        check(cudaMalloc(&ids, std::max<int64_t>(op.nrows, 1) * sizeof(int32_t)), "cudaMalloc");
-        check(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)), "cudaMalloc");
+        ids = reinterpret_cast<decltype(ids)>(analysis_alloc(std::max<int64_t>(op.nrows, 1) * sizeof(int32_t)));
+        tmp = reinterpret_cast<decltype(tmp)>(analysis_alloc(std::max<size_t>(tmp_bytes, 1)));
         k_bin_keys<<<grid_for(op.nrows, 256), 256, 0, s>>>(op.nrows, op.row_ptr, k_in, ids);
         check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, ids, op.bin_rows, n32, 0, 3, s),
               "radix sort");
         check(cudaStreamSynchronize(s), "sync");
-        cudaFree(tmp);
-        cudaFree(ids);
-        cudaFree(k_in);
+        analysis_free(tmp);
+        analysis_free(ids);
+        analysis_free(k_in);
     }
     // a bin that holds every row lists them in order: the kernels index rows directly
     for (int b = 0; b < 8; b++) op.bin_identity[b] = (off[b + 1] - off[b] == op.nrows);
@@ -886,8 +905,8 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
     // exclusive scan -> tp[0..n-1], tp[n] = nnz
     const int64_t nb = (n + 1023) / 1024;
     int64_t *bsum = nullptr, *boff = nullptr;
-    check(cudaMalloc(&bsum, std::max<int64_t>(nb, 1) * sizeof(int64_t)), "cudaMalloc");
-    check(cudaMalloc(&boff, std::max<int64_t>(nb, 1) * sizeof(int64_t)), "cudaMalloc");
+    bsum = reinterpret_cast<decltype(bsum)>(analysis_alloc(std::max<int64_t>(nb, 1) * sizeof(int64_t)));
+    boff = reinterpret_cast<decltype(boff)>(analysis_alloc(std::max<int64_t>(nb, 1) * sizeof(int64_t)));
     k_scan_block<<<(unsigned)nb, 1024, 0, s>>>(n, cnt, tp, bsum);
     std::vector<int64_t> hb(nb), ho(nb);
     check(cudaMemcpyAsync(hb.data(), bsum, nb * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
@@ -900,8 +919,8 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
     // fill keys
     unsigned long long *cursor = nullptr;
     uint64_t *key = nullptr, *tmp = nullptr;
-    check(cudaMalloc(&cursor, std::max<int64_t>(n, 1) * sizeof(unsigned long long)), "cudaMalloc");
-    check(cudaMalloc(&key, std::max<int64_t>(nnz, 1) * sizeof(uint64_t)), "cudaMalloc");
+    cursor = reinterpret_cast<decltype(cursor)>(analysis_alloc(std::max<int64_t>(n, 1) * sizeof(unsigned long long)));
+    key = reinterpret_cast<decltype(key)>(analysis_alloc(std::max<int64_t>(nnz, 1) * sizeof(uint64_t)));
     static_assert(sizeof(unsigned long long) == sizeof(int64_t), "");
     check(cudaMemcpyAsync(cursor, tp, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s), "D2D");
     k_csc_fill<<<grid_for(a.nrows * 32, 256), 256, 0, s>>>(a.nrows, a.row_ptr, a.col, cursor, key);
@@ -913,7 +932,7 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
     for (int64_t c = 0; c < n; c++) {
         int64_t len = htp[c + 1] - htp[c];
         if (len <= kSegSmem) continue;
-        if (!tmp) check(cudaMalloc(&tmp, nnz * sizeof(uint64_t)), "cudaMalloc");
+        if (!tmp) tmp = reinterpret_cast<decltype(tmp)>(analysis_alloc(nnz * sizeof(uint64_t)));
         uint64_t *seg = key + htp[c], *alt = tmp + htp[c];
         k_chunk_sort<<<(unsigned)((len + kSegSmem - 1) / kSegSmem), 256, 0, s>>>(seg, len);
         for (int64_t w = kSegSmem; w < len; w <<= 1) {
@@ -926,11 +945,11 @@ void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s) {
     k_csc_gather<<<grid_for(nnz, 256), 256, 0, s>>>(nnz, key, a.row_ptr, a.val, tcol, tval);
     check(cudaStreamSynchronize(s), "sync");
     check(cudaGetLastError(), "transpose");
-    cudaFree(bsum);
-    cudaFree(boff);
-    cudaFree(cursor);
-    cudaFree(key);
-    if (tmp) cudaFree(tmp);
+    analysis_free(bsum);
+    analysis_free(boff);
+    analysis_free(cursor);
+    analysis_free(key);
+    if (tmp) analysis_free(tmp);
     at.row_ptr = tp;
     at.col = tcol;
     at.val = tval;

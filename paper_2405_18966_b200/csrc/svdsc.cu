@@ -946,6 +946,16 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
         M->A.row_ptr = row_ptr;
         M->A.col = col_idx;
         M->A.val = values;
+        struct PoolScope {  // analysis allocations from the handle's pool
+            PoolScope(cudaMemPool_t p, cudaStream_t st) {
+                g_pool = p;
+                g_pool_stream = st;
+            }
+            ~PoolScope() {
+                g_pool = nullptr;
+                g_pool_stream = nullptr;
+            }
+        } scope(h->pool, s);
         csr_analyze(M->A, s);
         csr_transpose(M->A, M->At, s);
         M->seconds_analysis = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
