@@ -1367,6 +1367,7 @@ struct CArgs {
     unsigned int epoch;
     const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
     int gate_want;
+    int qstage;           // 1: the CTA's rows of Q are staged in shared memory once (read from L2 once, not 3x)
 };
 
 __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
@@ -1382,10 +1383,24 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
     double *ws = csm;                       // rpb: this CTA's rows of w
     double *hs = ws + a.rpb;                // PS: reduced coefficients
     double *part = hs + PS;                 // 3 x PS: partial vectors (one buffer per reduction)
+    double *qs = part + 3 * PS;             // qstage: ncols x rpb, column-major (this CTA's rows of Q)
     __shared__ double sh[32];
     const int64_t r0 = (int64_t)me * a.rpb;
     const int nr = (int)max((int64_t)0, min((int64_t)a.rpb, a.N - r0));
     const double *Qb = a.Q + r0;
+    const bool staged = a.qstage != 0;
+    if (staged) {  // 16-byte copies (rpb and ldq are even: every column segment is aligned)
+        const int half = (nr + 1) / 2;
+        for (int idx = tid; idx < ncols * half; idx += kClThreads) {
+            const int j = idx / half, c2 = idx - j * half;
+            const int rem = nr - 2 * c2;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(qs + (int64_t)j * a.rpb + 2 * c2);
+            const double *src = Qb + (int64_t)j * a.ldq + 2 * c2;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(rem >= 2 ? 16 : 8)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (int i = tid; i < nr; i += kClThreads) {
         double x;
         if (a.pre.partial) {  // finish a dense split-K product (k_split_reduce order)
@@ -1397,18 +1412,22 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
         }
         ws[i] = x;
     }
+    if (staged) asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    // Q(i, j) of the CTA's rows: shared memory when staged, else L2
+    auto qv = [&](int i, int j) -> double {
+        return staged ? qs[(int64_t)j * a.rpb + i] : __ldg(Qb + i + (int64_t)j * a.ldq);
+    };
     // column dots of Q_b^T v (v in shared memory) -> part buffer pb[0..ncols)
     auto coldots = [&](const double *v, double *pb) {
         for (int j = wid; j < ncols; j += NWc) {
-            const double *qj = Qb + (int64_t)j * a.ldq;
             double s0 = 0.0, s1 = 0.0;
             int i = lane;
             for (; i + 32 < nr; i += 64) {
-                s0 = fma(__ldg(qj + i), v[i], s0);
-                s1 = fma(__ldg(qj + i + 32), v[i + 32], s1);
+                s0 = fma(qv(i, j), v[i], s0);
+                s1 = fma(qv(i + 32, j), v[i + 32], s1);
             }
-            if (i < nr) s0 = fma(__ldg(qj + i), v[i], s0);
+            if (i < nr) s0 = fma(qv(i, j), v[i], s0);
             double t = s0 + s1;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
@@ -1421,10 +1440,10 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
             double s0 = 0.0, s1 = 0.0;
             int j = 0;
             for (; j + 1 < ncols; j += 2) {
-                s0 = fma(__ldg(Qb + i + (int64_t)j * a.ldq), h[j], s0);
-                s1 = fma(__ldg(Qb + i + (int64_t)(j + 1) * a.ldq), h[j + 1], s1);
+                s0 = fma(qv(i, j), h[j], s0);
+                s1 = fma(qv(i, j + 1), h[j + 1], s1);
             }
-            if (j < ncols) s0 = fma(__ldg(Qb + i + (int64_t)j * a.ldq), h[j], s0);
+            if (j < ncols) s0 = fma(qv(i, j), h[j], s0);
             const double x = v[i] - (s0 + s1);
             v[i] = x;
             if (nrm) *nrm = fma(x, x, *nrm);
@@ -1544,8 +1563,13 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     if (pol == 0 || pol == 5) {
         const size_t cl_max = (size_t)2 << 20;
         const int C = 16;
-        const int64_t rpb = (N + C - 1) / C;
-        const size_t smem = ((size_t)rpb + 4 * ((size_t)ncols + 2)) * sizeof(double);
+        const int64_t rpb = ((N + C - 1) / C + 1) / 2 * 2;  // even: 16-byte aligned Q segments
+        const size_t smem0 = ((size_t)rpb + 4 * ((size_t)ncols + 2)) * sizeof(double);
+        // the CTA's rows of Q staged in shared memory when they fit (bases <= 2 MB:
+        // <= 128 KB per CTA) and ldq keeps them 16-byte aligned
+        const bool qstage = ncols > 0 && (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
+                            smem0 + (size_t)ncols * rpb * sizeof(double) <= 200 * 1024;
+        const size_t smem = smem0 + (qstage ? (size_t)ncols * rpb * sizeof(double) : 0);
         if ((pol == 5 || (size_t)N * (size_t)std::max(ncols, 1) * 8 <= cl_max) && smem <= 200 * 1024 &&
             ncols <= 1022) {
             static bool attr = false;
@@ -1570,6 +1594,7 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             ca.epoch = fs.epoch;
             ca.gate = fs.gate;
             ca.gate_want = fs.gate_want;
+            ca.qstage = qstage ? 1 : 0;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(C);
             cfg.blockDim = dim3(kClThreads);
