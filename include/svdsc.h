@@ -216,8 +216,10 @@ SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int
  *                           when the rows fit in shared memory, else streaming),
  *                           1 split sweeps, 2 Q-resident, 3 cp.async streaming,
  *                           4 TMA streaming, 5 thread-block cluster
- *   SVDSC_POLICY_SMALL_SVD: 0 auto (cluster block Jacobi + rotation replay),
- *                           1 one-CTA Jacobi
+ *   SVDSC_POLICY_SMALL_SVD: 0 auto (register Jacobi for p <= 64, else cluster
+ *                           block Jacobi + rotation replay), 1 one-CTA Jacobi,
+ *                           2 register Jacobi (p <= 64, else auto), 3 cluster
+ *                           block Jacobi + rotation replay
  * EINVAL for an unknown key or value. */
 #define SVDSC_POLICY_SPMV 0
 #define SVDSC_POLICY_CGS2 1

@@ -554,6 +554,167 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi_block(int p, int h, const 
     if (CL) cl.sync();
 }
 
+// ---------------------------------------------------------------------------
+// Register Jacobi for p <= 64 (pe / 2 <= 32 pair slots, one CTA).  Pair slot q
+// is a group of kJG = 8 lanes holding the slot's two columns of W AND of V in
+// registers (lane g: rows g + 8 u, u < RL), so V is accumulated as the
+// rotations are applied (no rotation log, no replay launch) and T is read in
+// place.  8-lane groups keep the per-round reductions to 3 butterfly levels
+// and 4 pairs per warp (one warp per pair spent most of a round in shuffles).
+// Circle method with position 0 fixed: in round r position i >= 1 holds
+// column ((i - 1 - r) mod (pe - 1)) + 1 and slot q pairs positions q and
+// pe - 1 - q; between rounds every column moves one position through a
+// double-buffered shared-memory exchange (one barrier per round; position
+// stride = 8 mod 16 doubles so the 4 groups of a warp hit both bank halves).
+// After pe - 1 rounds (one sweep) every pair has met once and the columns are
+// back in place.  Rotation rule, threshold and orientation (lower global
+// column first) as in k_jacobi_block; ctrl->svd_tiny = p eps ||T||_F as in
+// k_copy_T.
+constexpr int kJG = 8;
+
+template <int RL>
+__device__ __forceinline__ void group_pair_sums(const double (&a)[RL], const double (&b)[RL], double &al, double &be,
+                                                double &gam) {
+    al = be = gam = 0.0;
+#pragma unroll
+    for (int u = 0; u < RL; u++) {
+        al = fma(a[u], a[u], al);
+        be = fma(b[u], b[u], be);
+        gam = fma(a[u], b[u], gam);
+    }
+#pragma unroll
+    for (int off = kJG / 2; off > 0; off >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, off);
+        be += __shfl_xor_sync(0xffffffffu, be, off);
+        gam += __shfl_xor_sync(0xffffffffu, gam, off);
+    }
+}
+
+template <int RL>
+__global__ void __launch_bounds__(256) k_jacobi_reg(int p, const double *__restrict__ T, int ldt, double *Wout,
+                                                    double *Vout, Ctrl *ctrl, const int *abort, double ctol,
+                                                    int max_sweeps) {
+    if (aborted(abort)) return;
+    constexpr int R = kJG * RL;     // rows per column (p <= R)
+    constexpr int PS = 2 * R + 8;   // position stride: W column, V column, pad
+    extern __shared__ __align__(16) double xs[];  // [2 buffers][pe positions][PS]
+    __shared__ double red[32];
+    const int pe = p + (p & 1), np2 = pe / 2, m = pe - 1;
+    const int g = threadIdx.x % kJG, q = threadIdx.x / kJG;
+    const bool slot = q < np2;  // lanes past the last slot hold zero columns
+    const int ct0 = slot ? q : pe, cb0 = slot ? pe - 1 - q : pe;  // columns at round 0
+    double wt[RL], wb[RL], vt[RL], vb[RL];
+    double ss = 0.0;
+#pragma unroll
+    for (int u = 0; u < RL; u++) {
+        const int r = g + kJG * u;
+        wt[u] = (r < p && ct0 < p) ? T[r + (int64_t)ct0 * ldt] : 0.0;
+        wb[u] = (r < p && cb0 < p) ? T[r + (int64_t)cb0 * ldt] : 0.0;
+        vt[u] = (r < p && r == ct0) ? 1.0 : 0.0;
+        vb[u] = (r < p && r == cb0) ? 1.0 : 0.0;
+        ss = fma(wt[u], wt[u], ss);
+        ss = fma(wb[u], wb[u], ss);
+    }
+#pragma unroll
+    for (int off = kJG / 2; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (g == 0 && slot) red[q] = ss;
+    __syncthreads();
+    double tot = 0.0;
+    for (int i = 0; i < np2; i++) tot += red[i];  // fixed order
+    const double tiny = (double)p * 2.220446049250313e-16 * sqrt(tot);
+    const double tiny2 = tiny * tiny, ctol2 = ctol * ctol;
+    // positions moving into the slot's two positions (read side of the exchange)
+    const int srct = q == 0 ? 0 : (q == 1 ? pe - 1 : q - 1), srcb = pe - 2 - q;
+    int buf = 0, sweep;
+    bool conv = false;
+    for (sweep = 1; sweep <= max_sweeps; sweep++) {
+        int rot = 0, any = 0;
+        int gt = ct0, gb = cb0;  // columns at the slot's positions in round r
+        for (int r = 0; r < m; r++) {
+            const bool live = gt < p && gb < p;
+            const bool tlow = gt < gb;
+            // sums branch-free (the 4 groups of a warp differ in orientation;
+            // shuffles under divergence are serialized), then oriented
+            double st2, sb2, gam;
+            group_pair_sums<RL>(wt, wb, st2, sb2, gam);
+            const double al = tlow ? st2 : sb2, be = tlow ? sb2 : st2;
+            if (live && al > tiny2 && be > tiny2 && gam * gam > ctol2 * (al * be)) {
+                double c, s;
+                rot_cs(jacobi_tan(al, be, gam), c, s);
+                // (A, B) = (lower, higher): A' = c A - s B, B' = s A + c B; with the
+                // top column the higher one, the same form with s -> -s
+                const double sx = tlow ? s : -s;
+#pragma unroll
+                for (int u = 0; u < RL; u++) {
+                    const double x = wt[u], y = wb[u];
+                    wt[u] = c * x - sx * y;
+                    wb[u] = sx * x + c * y;
+                    const double vx = vt[u], vy = vb[u];
+                    vt[u] = c * vx - sx * vy;
+                    vb[u] = sx * vx + c * vy;
+                }
+                rot = 1;
+            }
+            if (m > 1) {
+                double *B = xs + (size_t)buf * pe * PS;
+                if (slot) {
+                    double *st = B + (size_t)q * PS + g, *sb = B + (size_t)(pe - 1 - q) * PS + g;
+#pragma unroll
+                    for (int u = 0; u < RL; u++) {
+                        st[kJG * u] = wt[u];
+                        st[R + kJG * u] = vt[u];
+                        sb[kJG * u] = wb[u];
+                        sb[R + kJG * u] = vb[u];
+                    }
+                }
+                if (r == m - 1) any = __syncthreads_or(rot);
+                else __syncthreads();
+                if (slot) {
+                    const double *lt = B + (size_t)srct * PS + g, *lb = B + (size_t)srcb * PS + g;
+#pragma unroll
+                    for (int u = 0; u < RL; u++) {
+                        if (q != 0) {
+                            wt[u] = lt[kJG * u];
+                            vt[u] = lt[R + kJG * u];
+                        }
+                        wb[u] = lb[kJG * u];
+                        vb[u] = lb[R + kJG * u];
+                    }
+                }
+                buf ^= 1;
+            } else {
+                any = __syncthreads_or(rot);
+            }
+            // next round: every column one position on (position 0 fixed)
+            if (q != 0) gt = (gt == 1) ? m : gt - 1;
+            gb = (gb == 1) ? m : gb - 1;
+        }
+        if (!any) {
+            conv = true;
+            break;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < RL; u++) {
+        const int r = g + kJG * u;
+        if (r < p) {
+            if (ct0 < p) {
+                Wout[r + (int64_t)ct0 * p] = wt[u];
+                Vout[r + (int64_t)ct0 * p] = vt[u];
+            }
+            if (cb0 < p) {
+                Wout[r + (int64_t)cb0 * p] = wb[u];
+                Vout[r + (int64_t)cb0 * p] = vb[u];
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        ctrl->svd_tiny = tiny;
+        ctrl->svd_sweeps = conv ? sweep : max_sweeps;
+        ctrl->svd_status = conv ? 0 : (int)SVDSC_ESVD_NOCONV;
+    }
+}
+
 // V = J_1 J_2 ... (the logged rotations) for R rows of V per CTA: row r of V is
 // e_r^T J_1 J_2 ..., independent of the other rows.  Thread (q, i) applies
 // rotation q of every round to row i of the CTA's R rows (rotations of one
@@ -967,8 +1128,10 @@ cudaError_t launch_jacobi(int C, int p, int h, size_t smem, double *W, RotLog *r
         k_jacobi_block<false, R><<<1, kJThreads, smem, s>>>(p, h, W, W, rlog, 50, ctrl, abort, ctol, 0);
         return cudaGetLastError();
     }
-    // bulk-copy exchange when the second buffer set fits, else a register pull
-    const int use_bulk = (2 * smem <= 210 * 1024) ? 1 : 0;
+    // bulk-copy exchange when the second buffer set fits and the half-blocks
+    // (h p doubles) are whole 16-byte units (cp.async.bulk alignment), else a
+    // register pull
+    const int use_bulk = (2 * smem <= 210 * 1024 && (h * p) % 2 == 0) ? 1 : 0;
     if (use_bulk) smem *= 2;
     cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (C > 8) cudaFuncSetAttribute(k_jacobi_block<true, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1002,10 +1165,27 @@ size_t small_svd_log_doubles(int p) {
 
 void small_svd(int p, const double *Tsrc, int ldt, double *W, double *Vw, double *Uh, double *Sh, double *Vh,
                int kneed, Ctrl *ctrl, const int *abort, double *tlog, cudaStream_t s) {
+    const double ctol = 2.0 * (double)p * 2.220446049250313e-16;  // reading Q10a
+    const int pol = g_policy.small_svd;  // SVDSC_POLICY_SMALL_SVD
+    if (p <= 64 && (pol == 0 || pol == 2)) {
+        // register Jacobi: one launch for W and V, then the finish
+        const int pe = p + (p & 1);
+        const int threads = ((pe / 2) * kJG + 31) / 32 * 32;
+        const size_t smem = (size_t)2 * pe * (2 * kJG * (p <= 32 ? 4 : 8) + 8) * sizeof(double);
+        if (p <= 32) {
+            k_jacobi_reg<4><<<1, threads, smem, s>>>(p, Tsrc, ldt, W, Vw, ctrl, abort, ctol, 50);
+        } else {
+            cudaFuncSetAttribute(k_jacobi_reg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_jacobi_reg<8><<<1, threads, smem, s>>>(p, Tsrc, ldt, W, Vw, ctrl, abort, ctol, 50);
+        }
+        count_launch();
+        k_svd_finish<<<1, 1024, 0, s>>>(p, W, Vw, Uh, Sh, Vh, kneed, ctrl, abort);
+        count_launch();
+        return;
+    }
     k_copy_T<<<1, 1024, 0, s>>>(p, Tsrc, ldt, W, Vw, ctrl, abort);
     count_launch();
-    if (g_policy.small_svd == 1) tlog = nullptr;  // one-CTA Jacobi (SVDSC_POLICY_SMALL_SVD = 1)
-    const double ctol = 2.0 * (double)p * 2.220446049250313e-16;  // reading Q10a
+    if (pol == 1) tlog = nullptr;  // one-CTA Jacobi
     bool done = false;
     int C, h;
     jacobi_geometry(p, C, h);

@@ -1319,7 +1319,7 @@ svdsc_status svdsc_comm_init_group(svdsc_handle *h, svdsc_group *g, int rank) {
 
 svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t value) {
     if (!h) return SVDSC_EINVAL;
-    const int maxv[3] = {2, 5, 1};
+    const int maxv[3] = {2, 5, 3};
     if (key < 0 || key > 2 || value < 0 || value > maxv[key]) {
         h->err = "svdsc_set_policy: unknown key or value";
         return SVDSC_EINVAL;

@@ -74,7 +74,7 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
 POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD = 0, 1, 2
 SPMV = {"auto": 0, "bins": 1, "seg": 2}
 CGS2 = {"auto": 0, "split": 1, "qs": 2, "stream": 3, "tma": 4, "cluster": 5}
-SMALL_SVD = {"auto": 0, "one_cta": 1}
+SMALL_SVD = {"auto": 0, "one_cta": 1, "register": 2, "block": 3}
 PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",
                  "recombine", "restart_misc", "collectives", "cgs2_fused", "pro_decide"]
 

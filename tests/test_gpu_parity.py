@@ -184,15 +184,16 @@ def _arrow(rng, p, k):
     return T
 
 
-@pytest.mark.parametrize("cluster", [True, False])
+@pytest.mark.parametrize("kernel", ["auto", "register", "block", "one_cta"])
 @pytest.mark.parametrize("p,kind", [(30, "bidiag"), (150, "arrow"), (300, "arrow"), (31, "bidiag"), (1, "bidiag"),
-                                    (601, "arrow")])
-def test_small_svd(S, Hp, p, kind, cluster):
+                                    (2, "bidiag"), (33, "arrow"), (63, "arrow"), (64, "bidiag"), (601, "arrow")])
+def test_small_svd(S, Hp, p, kind, kernel):
     H = Hp
-    if not cluster:
-        if p > 300:
-            pytest.skip("one-CTA fallback is slow at this size")
-        H.set_policy(small_svd="one_cta")
+    if kernel == "one_cta" and p > 300:
+        pytest.skip("one-CTA fallback is slow at this size")
+    if kernel == "register" and p > 64:
+        pytest.skip("register Jacobi is for p <= 64 (auto beyond)")
+    H.set_policy(small_svd=kernel)
     rng = np.random.default_rng(p)
     T = _bidiag(rng, p) if kind == "bidiag" or p < 3 else _arrow(rng, p, p // 3)
     Td = S.colmajor(p, p)
