@@ -1376,9 +1376,6 @@ struct CArgs {
 __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
     namespace cgx = cooperative_groups;
     cgx::cluster_group cl = cgx::this_cluster();
-    grid_prepare(a.flags, a.epoch);  // keep the barrier-slot chain of the fused launches intact
-    if (*(volatile int *)&a.ctrl->abort) return;  // uniform over the cluster
-    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NWc = kClThreads / 32;
     const int ncols = a.ncols, PS = ncols + 2;
@@ -1392,17 +1389,27 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
     const int nr = (int)max((int64_t)0, min((int64_t)a.rpb, a.N - r0));
     const double *Qb = a.Q + r0;
     const bool staged = a.qstage != 0;
+    // Q was written before the stream predecessor (the product) started: it is
+    // staged before the PDL wait, under the predecessor's tail
     if (staged) {  // 16-byte copies (rpb and ldq are even: every column segment is aligned)
         const int half = (nr + 1) / 2;
-        for (int idx = tid; idx < ncols * half; idx += kClThreads) {
-            const int j = idx / half, c2 = idx - j * half;
-            const int rem = nr - 2 * c2;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(qs + (int64_t)j * a.rpb + 2 * c2);
-            const double *src = Qb + (int64_t)j * a.ldq + 2 * c2;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(rem >= 2 ? 16 : 8)
-                         : "memory");
-        }
+        for (int j = wid; j < ncols; j += NWc)
+            for (int c2 = lane; c2 < half; c2 += 32) {
+                const int rem = nr - 2 * c2;
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(qs + (int64_t)j * a.rpb + 2 * c2);
+                const double *src = Qb + (int64_t)j * a.ldq + 2 * c2;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src),
+                             "r"(rem >= 2 ? 16 : 8)
+                             : "memory");
+            }
         asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    pdl_wait();  // launched with launch_pdl: w (and ctrl) are the predecessor's output
+    pdl_trigger();
+    grid_prepare(a.flags, a.epoch);  // keep the barrier-slot chain of the fused launches intact
+    if (*(volatile int *)&a.ctrl->abort || (a.gate && *(volatile const int *)a.gate != a.gate_want)) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;  // uniform over the cluster (abort / PRO gate)
     }
     for (int i = tid; i < nr; i += kClThreads) {
         double x;
@@ -1598,19 +1605,7 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
             ca.gate = fs.gate;
             ca.gate_want = fs.gate_want;
             ca.qstage = qstage ? 1 : 0;
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(C);
-            cfg.blockDim = dim3(kClThreads);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = s;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = C;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            if (cudaLaunchKernelEx(&cfg, k_cgs2_cluster, ca) == cudaSuccess) {
+            if (launch_pdl(k_cgs2_cluster, dim3(C), dim3(kClThreads), smem, s, C, ca) == cudaSuccess) {
                 count_launch();
                 return true;
             }

@@ -255,6 +255,42 @@ void analysis_free(void *p);
 extern thread_local int64_t g_launches;
 inline void count_launch() { ++g_launches; }
 
+// Programmatic dependent launch (PDL): a kernel launched by launch_pdl may be
+// scheduled while its stream predecessor is still draining (onto the SMs that
+// predecessor leaves idle); it runs only work that reads nothing the
+// predecessor writes (e.g. staging the basis Q), then pdl_wait() -- which
+// returns once the predecessor grid has completed and its writes are visible
+// -- before anything else.  pdl_trigger(), issued after the wait, lets the
+// successor launch early in turn.  A kernel that never calls pdl_wait must not
+// be launched with launch_pdl.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    int na = 1;
+    if (cluster > 1) {
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = cluster;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        na = 2;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 }  // namespace svdsc
 
 #define SVDSC_CUDA_CHECK_LAUNCH() ::svdsc::count_launch()

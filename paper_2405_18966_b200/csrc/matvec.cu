@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(256) k_spmv_bins(BinArgs ba, const int64_t *__
                                                    const double *__restrict__ x, double *__restrict__ y,
                                                    const double *c_dev, const double *__restrict__ yprev,
                                                    const int *abort) {
+    pdl_wait();  // launched with launch_pdl: x is the predecessor's output
+    pdl_trigger();
     if (aborted(abort)) return;
     const int bx = blockIdx.x;
     int b = 0, lo = ba.bstart[0], hi = ba.bstart[1];
@@ -434,6 +436,8 @@ __device__ __forceinline__ void seg_load_v(const SegArgs &a, int ch, int lane, d
 }
 
 __global__ void __launch_bounds__(kSegThreads, kSegMinBlocks) k_spmv_seg(SegArgs a) {
+    pdl_wait();  // launched with launch_pdl: x is the predecessor's output
+    pdl_trigger();
     if (aborted(a.abort)) return;
     const double c = a.c_dev ? *a.c_dev : 0.0;
     for (int64_t i = blockIdx.x * (int64_t)kSegThreads + threadIdx.x; i < a.nempty; i += (int64_t)gridDim.x * kSegThreads) {
@@ -962,7 +966,7 @@ void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, c
         SegArgs sa{A.nnz, (int)A.seg_nchunks, A.seg_cpw, A.seg_nranges, A.col, A.val, x, A.seg_bits,
                    A.seg_rows, A.seg_cstart, A.seg_empty, A.seg_nempty, y, c_dev, yprev, A.seg_head,
                    A.seg_tail, A.seg_flag, abort};
-        k_spmv_seg<<<A.seg_grid, kSegThreads, 0, s>>>(sa);
+        (void)launch_pdl(k_spmv_seg, dim3(A.seg_grid), dim3(kSegThreads), 0, s, 0, sa);  // errors: cudaGetLastError
         count_launch();
         return;
     }
@@ -1000,7 +1004,8 @@ void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev, c
         ba.bstart[5] = nb_tot;
         if (nb_tot > 0) {
             // one full wave: the grid-stride loops then have no partial second wave
-            k_spmv_bins<<<nb_tot, 256, 0, s>>>(ba, A.row_ptr, A.col, A.val, x, y, c_dev, yprev, abort);
+            (void)launch_pdl(k_spmv_bins, dim3(nb_tot), dim3(256), 0, s, 0, ba, (const int64_t *)A.row_ptr,
+                             (const int32_t *)A.col, (const double *)A.val, x, y, c_dev, yprev, abort);
             count_launch();
         }
     }
