@@ -1535,6 +1535,228 @@ __global__ void __launch_bounds__(kClThreads) k_cgs2_cluster(CArgs a) {
     cl.sync();  // no CTA exits while its shared memory may still be read remotely
 }
 
+// ---------------------------------------------------------------------------
+// Cluster CGS2 for narrow small bases (ncols <= 32 MC, basis <= 2 MB: BASELINE
+// config 1).  Same 16-CTA cluster and row blocks as k_cgs2_cluster, every
+// phase arranged for latency (the call is ~20 dependent phases of a few hundred
+// cycles each, not a bandwidth problem):
+//  * Q staged with 8-byte cp.async into an odd-stride column-major block
+//    BEFORE the PDL wait, i.e. under the product's tail;
+//  * column dots: warp w owns a slab of rows, lane l columns l + 32 m (odd
+//    stride: conflict-free), cross-warp sums through shared memory;
+//  * cluster all-reduce by push: the thread that forms entry j of the CTA's
+//    partial vector stores it into slot [me] of every CTA's receive buffer
+//    (DSMEM stores), one cluster barrier (release / acquire), then every CTA
+//    sums the C slots locally in rank order (bitwise identical everywhere, no
+//    remote loads after the barrier);
+//  * ||w'||^2 rides in the h2 vector; ||h2||^2 is summed by every thread itself.
+template <int MC>
+__global__ void __launch_bounds__(kClThreads) k_cgs2_cl(CArgs a) {
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = kClThreads / 32;
+    const int ncols = a.ncols, PS = ncols + 2, qld = a.rpb | 1;
+    extern __shared__ __align__(16) double csm[];
+    double *ws = csm;                   // rpb: this CTA's rows of w
+    double *hs = ws + a.rpb;            // PS: reduced vector
+    double *red = hs + PS;              // NW x PS: per-warp column sums
+    double *recv = red + NW * PS;       // 3 x C x PS: pushed CTA partials, one set per reduction
+    double *qs = recv + 3 * C * PS;     // ncols x qld: this CTA's rows of Q
+    __shared__ double sh[NW];
+    __shared__ __align__(8) uint64_t rbar[3];  // one per reduction: completes when all C pushes landed
+    const int64_t r0 = (int64_t)me * a.rpb;
+    const int nr = (int)max((int64_t)0, min((int64_t)a.rpb, a.N - r0));
+    const double *Qb = a.Q + r0;
+    // Q was final before the stream predecessor (the product) started
+    for (int j = wid; j < ncols; j += NW)
+        for (int i = lane; i < nr; i += 32) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(qs + (int64_t)j * qld + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Qb + (int64_t)j * a.ldq + i)
+                         : "memory");
+        }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // receive barriers armed for the byte counts of the three reductions; the
+    // cluster barrier that publishes their initialization is awaited just
+    // before the first push
+    if (tid == 0) {
+        for (int r = 0; r < 3; r++) mbar_init(&rbar[r], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&rbar[0], (unsigned)(C * ncols * 8));
+        mbar_expect_tx(&rbar[1], (unsigned)(C * (ncols + 1) * 8));
+        mbar_expect_tx(&rbar[2], (unsigned)(C * 8));
+    }
+    cl.barrier_arrive();
+    bool joined = false;
+    pdl_wait();  // launched with launch_pdl: w (and ctrl) are the predecessor's output
+    pdl_trigger();
+    grid_prepare(a.flags, a.epoch);  // keep the barrier-slot chain of the fused launches intact
+    if (*(volatile int *)&a.ctrl->abort || (a.gate && *(volatile const int *)a.gate != a.gate_want)) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        cl.barrier_wait();  // (nothing is pushed: uniform over the cluster)
+        return;  // abort / PRO gate
+    }
+    for (int i = tid; i < nr; i += kClThreads) {
+        double x;
+        if (a.pre.partial) {  // finish a dense split-K product (k_split_reduce order)
+            x = 0.0;
+            for (int q = 0; q < a.pre.splits; q++) x += a.pre.partial[q * a.N + r0 + i];
+            if (a.pre.yprev) x -= *a.pre.c_dev * a.pre.yprev[r0 + i];
+        } else {
+            x = a.w[r0 + i];
+        }
+        ws[i] = x;
+    }
+    if (a.pre_h)
+        for (int j = tid; j < ncols; j += kClThreads) hs[j] = a.pre_h[j];
+    const double amax = a.ctrl->amax[a.check & 1];  // (loaded early: off the tail's critical path)
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // ws[i] -= sum_j Q(i, j) hs[j] (thread per row: unit stride in qs)
+    auto rowupdate = [&](double *nrm) {
+        for (int i = tid; i < nr; i += kClThreads) {
+            double s0 = 0.0, s1 = 0.0;
+            int j = 0;
+            for (; j + 1 < ncols; j += 2) {
+                s0 = fma(qs[(int64_t)j * qld + i], hs[j], s0);
+                s1 = fma(qs[(int64_t)(j + 1) * qld + i], hs[j + 1], s1);
+            }
+            if (j < ncols) s0 = fma(qs[(int64_t)j * qld + i], hs[j], s0);
+            const double x = ws[i] - (s0 + s1);
+            ws[i] = x;
+            if (nrm) *nrm = fma(x, x, *nrm);
+        }
+    };
+    // push value t into slot [me] entry j of reduction set r of every CTA
+    // (st.async: the store completes on the receiver's mbarrier rbar[r])
+    // (every thread has joined the initialization barrier before its first push)
+    auto push = [&](int r, int j, double t) {
+        const unsigned la = smem_u32(recv + (int64_t)(r * C + me) * PS + j), lb = smem_u32(&rbar[r]);
+        for (int c = 0; c < C; c++) {
+            unsigned ra, rb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(c));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(c));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra),
+                         "d"(t), "r"(rb)
+                         : "memory");
+        }
+    };
+    // CTA partial of Q_b^T ws (+ ||ws_b||^2 in entry ncols when with_norm),
+    // pushed into reduction set r of every CTA; once all C pushes landed hs =
+    // the cluster sum in rank order
+    const int rs = (nr + NW - 1) / NW, i0 = min(nr, wid * rs), i1 = min(nr, i0 + rs);
+    auto coldots_allreduce = [&](int r, bool with_norm) {
+        double acc[MC];
+#pragma unroll
+        for (int m = 0; m < MC; m++) acc[m] = 0.0;
+        double nrm = 0.0;
+#pragma unroll 4
+        for (int i = i0; i < i1; i++) {
+            const double x = ws[i];
+#pragma unroll
+            for (int m = 0; m < MC; m++) {
+                const int j = lane + 32 * m;
+                if (j < ncols) acc[m] = fma(qs[(int64_t)j * qld + i], x, acc[m]);
+            }
+            nrm = fma(x, x, nrm);
+        }
+#pragma unroll
+        for (int m = 0; m < MC; m++) {
+            const int j = lane + 32 * m;
+            if (j < ncols) red[wid * PS + j] = acc[m];
+        }
+        if (with_norm && lane == 0) red[wid * PS + ncols] = nrm;
+        __syncthreads();
+        const int cnt = ncols + (with_norm ? 1 : 0);
+        if (!joined) {
+            cl.barrier_wait();
+            joined = true;
+        }
+        for (int j = tid; j < cnt; j += kClThreads) {
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;  // fixed order: ((w0+w4+..) + (w1+..)) + ...
+#pragma unroll
+            for (int w = 0; w < NW; w += 4) {
+                t0 += red[w * PS + j];
+                t1 += red[(w + 1) * PS + j];
+                t2 += red[(w + 2) * PS + j];
+                t3 += red[(w + 3) * PS + j];
+            }
+            push(r, j, (t0 + t1) + (t2 + t3));
+        }
+        mbar_wait(&rbar[r], 0);  // all C pushes landed
+        for (int j = tid; j < cnt; j += kClThreads) {
+            double t = 0.0;
+            for (int c = 0; c < C; c++) t += recv[(int64_t)(r * C + c) * PS + j];
+            hs[j] = t;
+        }
+        __syncthreads();
+    };
+    if (a.pre_h) {  // w -= Q pre_h (restart, Eq. (7))
+        rowupdate(nullptr);
+        __syncthreads();
+    }
+    if (ncols > 0) {
+        coldots_allreduce(0, false);  // h1
+        rowupdate(nullptr);           // w' = w - Q h1
+        __syncthreads();
+    }
+    coldots_allreduce(1, true);  // [h2; ||w'||^2]
+    const double nrmp = hs[ncols];
+    double hh = 0.0;
+    {  // every thread, same order (four chains)
+        double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+        int j = 0;
+        for (; j + 3 < ncols; j += 4) {
+            h0 = fma(hs[j], hs[j], h0);
+            h1 = fma(hs[j + 1], hs[j + 1], h1);
+            h2 = fma(hs[j + 2], hs[j + 2], h2);
+            h3 = fma(hs[j + 3], hs[j + 3], h3);
+        }
+        for (; j < ncols; j++) h0 = fma(hs[j], hs[j], h0);
+        hh = (h0 + h1) + (h2 + h3);
+    }
+    double beta2 = nrmp - hh;
+    const bool pyth = beta2 > 0.5 * nrmp;
+    double nrm2 = 0.0;
+    if (ncols > 0) rowupdate(pyth ? nullptr : &nrm2);  // w'' = w' - Q h2
+    if (!pyth) {  // explicit norm (uniform branch): block sum, then a third push all-reduce
+        nrm2 = warp_sum(nrm2);
+        if (lane == 0) sh[wid] = nrm2;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int q = 0; q < NW; q++) t += sh[q];
+            push(2, 0, t);
+        }
+        mbar_wait(&rbar[2], 0);
+        double t = 0.0;
+        for (int c = 0; c < C; c++) t += recv[(int64_t)(2 * C + c) * PS];
+        beta2 = t;
+    } else {
+        __syncthreads();
+    }
+    const double beta = sqrt(fmax(beta2, 0.0));
+    const bool bd = !(beta > 1e-14 * fmax(amax, 1.0));
+    if (me == 0 && tid == 0) {
+        if (bd) {
+            *a.t_entry = 0.0;
+            a.ctrl->amax[(a.check + 1) & 1] = amax;
+            a.ctrl->abort_check = a.check;
+            __threadfence();
+            a.ctrl->abort = 1;
+        } else {
+            *a.t_entry = beta;
+            a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
+        }
+    }
+    if (!bd) {
+        const double rbeta = 1.0 / beta;
+        for (int i = tid; i < nr; i += kClThreads) a.w[r0 + i] = ws[i] * rbeta;
+    }
+    // every push into this CTA landed before its last mbarrier wait: CTAs may exit
+}
+
 // returns false if the fused path cannot be used (caller falls back)
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
@@ -1573,6 +1795,43 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     if (pol == 0 || pol == 5) {
         const size_t cl_max = (size_t)2 << 20;
         const int C = 16;
+        if (ncols <= 64 && (pol == 5 || (size_t)N * (size_t)std::max(ncols, 1) * 8 <= cl_max)) {
+            // narrow bases: the latency-arranged cluster kernel
+            const int64_t rpb = (N + C - 1) / C;
+            const int PS = ncols + 2;
+            const size_t smem = ((size_t)rpb + PS + 16 * (size_t)PS + 3 * (size_t)C * PS +
+                                 (size_t)ncols * (size_t)(rpb | 1)) * sizeof(double);
+            if (smem <= 200 * 1024) {
+                CArgs ca{};
+                ca.N = N;
+                ca.ncols = ncols;
+                ca.Q = Q;
+                ca.ldq = ldq;
+                ca.w = w;
+                ca.ctrl = ctrl;
+                ca.t_entry = t_entry;
+                ca.check = check;
+                ca.pre_h = pre_h;
+                if (fs.pre) ca.pre = *fs.pre;
+                ca.rpb = (int)rpb;
+                ca.flags = fs.flags;
+                ca.epoch = fs.epoch;
+                ca.gate = fs.gate;
+                ca.gate_want = fs.gate_want;
+                auto kern = ncols <= 32 ? k_cgs2_cl<1> : k_cgs2_cl<2>;
+                static bool attr[2] = {false, false};
+                if (!attr[ncols > 32]) {
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                    attr[ncols > 32] = true;
+                }
+                if (launch_pdl(kern, dim3(C), dim3(kClThreads), smem, s, C, ca) == cudaSuccess) {
+                    count_launch();
+                    return true;
+                }
+                cudaGetLastError();
+            }
+        }
         const int64_t rpb = ((N + C - 1) / C + 1) / 2 * 2;  // even: 16-byte aligned Q segments
         const size_t smem0 = ((size_t)rpb + 4 * ((size_t)ncols + 2)) * sizeof(double);
         // the CTA's rows of Q staged in shared memory when they fit (bases <= 2 MB:
