@@ -86,6 +86,12 @@ __global__ void k_bin_count(int64_t nrows, const int64_t *__restrict__ rp, unsig
     if (threadIdx.x == 0) atomicMax(&cnt[8], smax);
 }
 
+// lengths of the listed rows (the long-row table: one D2H instead of one per row)
+__global__ void k_row_len(int64_t n, const int32_t *__restrict__ rows, const int64_t *__restrict__ rp, int64_t *len) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) len[i] = rp[rows[i] + 1] - rp[rows[i]];
+}
+
 // bin key and row id per row; a stable radix sort by key then lists every bin's
 // rows in ascending order (streaming access to row_ptr / col / val / y)
 __global__ void k_bin_keys(int64_t nrows, const int64_t *__restrict__ rp, uint8_t *key, int32_t *ids) {
@@ -851,17 +857,28 @@ void csr_analyze(CsrOp &op, cudaStream_t s) {
     op.n_long = off[7] - off[6];
     if (op.n_long > 0) {
         std::vector<int32_t> lr(op.n_long);
+        std::vector<int64_t> len(op.n_long);
+        int64_t *dlen = reinterpret_cast<int64_t *>(analysis_alloc(op.n_long * sizeof(int64_t)));
+        k_row_len<<<grid_for(op.n_long, 256), 256, 0, s>>>(op.n_long, op.bin_rows + off[6], op.row_ptr, dlen);
         check(cudaMemcpyAsync(lr.data(), op.bin_rows + off[6], op.n_long * sizeof(int32_t),
                               cudaMemcpyDeviceToHost, s), "D2H");
+        check(cudaMemcpyAsync(len.data(), dlen, op.n_long * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
         check(cudaStreamSynchronize(s), "sync");
-        std::sort(lr.begin(), lr.end());
+        analysis_free(dlen);
+        {  // rows ascending (the bin lists them by key only), lengths alongside
+            std::vector<std::pair<int32_t, int64_t>> rl(op.n_long);
+            for (int64_t i = 0; i < op.n_long; i++) rl[i] = {lr[i], len[i]};
+            std::sort(rl.begin(), rl.end());
+            for (int64_t i = 0; i < op.n_long; i++) {
+                lr[i] = rl[i].first;
+                len[i] = rl[i].second;
+            }
+        }
         std::vector<int64_t> first(op.n_long + 1);
         std::vector<int32_t> crow;
         int64_t nch = 0;
         for (int64_t i = 0; i < op.n_long; i++) {
-            int64_t rr[2];
-            check(cudaMemcpy(rr, op.row_ptr + lr[i], 2 * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
-            int64_t L = rr[1] - rr[0];
+            const int64_t L = len[i];
             first[i] = nch;
             int64_t c = (L + kLongRow - 1) / kLongRow;
             for (int64_t q = 0; q < c; q++) crow.push_back((int32_t)i);
