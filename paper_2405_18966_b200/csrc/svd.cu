@@ -787,6 +787,7 @@ __global__ void __launch_bounds__(1024) k_svd_finish(int p, const double *__rest
     if (aborted(abort)) return;
     const double tiny = ctrl->svd_tiny;
     __shared__ double sig[kMaxP];
+    __shared__ double sorted[kMaxP];  // Sh in shared memory (the completion scan reads it)
     __shared__ int dest[kMaxP];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = wid; j < p; j += nw) {
@@ -809,7 +810,10 @@ __global__ void __launch_bounds__(1024) k_svd_finish(int p, const double *__rest
     for (int j = wid; j < p; j += nw) {
         const int d = dest[j];
         const double sj = sig[j];
-        if (lane == 0) Sh[d] = sj;
+        if (lane == 0) {
+            Sh[d] = sj;
+            sorted[d] = sj;
+        }
         for (int r = lane; r < p; r += 32) {
             Vh[r + (int64_t)d * p] = V[r + (int64_t)j * p];
             Uh[r + (int64_t)d * p] = sj > 0.0 ? W[r + (int64_t)j * p] / sj : 0.0;
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(1024) k_svd_finish(int p, const double *__rest
     // previous columns is largest (the oracle's rule).  Rare: exact rank loss.
     if (wid == 0) {
         for (int d = 0; d < kneed && d < p; d++) {
-            if (Sh[d] > 0.0) continue;
+            if (sorted[d] > 0.0) continue;
             double *ud = Uh + (int64_t)d * p;
             int best = 0;
             double bestn = -1.0;
