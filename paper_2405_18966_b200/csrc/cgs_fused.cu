@@ -639,17 +639,26 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             else p[1] = other;
         }
     };
-    // cross-warp column sums of acc -> partial[block][j]
-    auto flush_cols = [&](const double (&acc)[M]) {
+    // cross-warp column sums of acc -> partial[block][j]; with a norm, the
+    // thread partials nrm (summed per warp, then over the warps in order:
+    // block_sum_all's order) go to partial[block][ncols]
+    auto flush_cols = [&](const double (&acc)[M], const double *nrm) {
 #pragma unroll
         for (int m = 0; m < M; m++) {
             const int j = lane + 32 * m;
             if (j < ncols) red[wid * ncols + j] = acc[m];
         }
+        if (nrm) {
+            const double v = warp_sum(*nrm);
+            if (lane == 0) red[NW * ncols + wid] = v;
+        }
         __syncthreads();
-        for (int j = tid; j < ncols; j += kSThr) {
+        for (int j = tid; j < ncols + (nrm ? 1 : 0); j += kSThr) {
             double s = 0.0;
-            for (int w = 0; w < NW; w++) s += red[w * ncols + j];
+            if (j < ncols)
+                for (int w = 0; w < NW; w++) s += red[w * ncols + j];
+            else
+                for (int w = 0; w < NW; w++) s += red[NW * ncols + w];
             a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
         }
         __syncthreads();
@@ -696,7 +705,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
                     if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
             }
         });
-        flush_cols(acc);
+        flush_cols(acc, nullptr);
         if (ph == 0) {
             prefetch();  // phase B re-reads the same tiles: start them under the reduction
             prefetched = true;
@@ -760,7 +769,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
                 }
             });
         }
-        flush_cols(acc);
+        flush_cols(acc, &nrm_wp);  // [partial h2, ||w'_b||^2]
     } else if (ph == 0 || ph == 2) {
         run_tiles([&](int k, const double *, const double *W) {
 #pragma unroll
@@ -772,7 +781,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         });
     }
     if (ph == 0 || ph == 2) {
-        {
+        if (ncols == 0) {
             const double bn = block_sum_all(nrm_wp, sh);
             if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
         }
@@ -789,12 +798,13 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     }
     load_h(a.h2, hreg);
     const double nrmp = __ldcg(a.h2 + ncols);
+    // ||h2||^2 from the coefficients every warp already holds (lane: columns
+    // lane + 32 m, zeros past ncols); lane 0's butterfly result broadcast, so
+    // every thread of every CTA uses the same value
     double hh = 0.0;
-    for (int j = tid; j < ncols; j += kSThr) {
-        const double x = __ldcg(a.h2 + j);
-        hh = fma(x, x, hh);
-    }
-    hh = block_sum_all(hh, sh);
+#pragma unroll
+    for (int m = 0; m < M; m++) hh = fma(hreg[m], hreg[m], hh);
+    hh = __shfl_sync(0xffffffffu, warp_sum(hh), 0);
     double beta2 = nrmp - hh;
     const bool pyth = beta2 > 0.5 * nrmp;
     const double amax = a.ctrl->amax[a.check & 1];
