@@ -411,6 +411,7 @@ def main():
         uid = [S.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         H.comm_init(world, rank, uid[0])
+        H.comm_check()  # fail fast on a broken NCCL / NVLink setup (one small collective of each kind)
     M = S.Matrix.from_host(H, Al, device=dev, row_offset=r0, m_global=m_global)
     v0 = torch.from_numpy(wl_full.v0).to(dev)
     k, t = wl_full.k, wl_full.t

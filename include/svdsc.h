@@ -233,6 +233,13 @@ SVDSC_API svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t va
  * SVDSC_ENCCL if unavailable. */
 SVDSC_API svdsc_status svdsc_comm_unique_id(unsigned char id[128]);
 SVDSC_API svdsc_status svdsc_comm_init(svdsc_handle *h, int nranks, int rank, const unsigned char id[128]);
+/* Collective self-check of the handle's communicator (NCCL or loopback group;
+ * call on every rank): one all-gather, reduce-scatter, all-reduce (fp64,
+ * rank-dependent integers, exact) and the status all-reduce(min), results
+ * compared on the host.  SVDSC_EINVAL without a communicator, SVDSC_ENCCL on a
+ * failed call or a wrong sum.  Not needed before a solve; a cheap way to fail
+ * fast on a broken NVLink / NCCL setup (bench.py calls it after init). */
+SVDSC_API svdsc_status svdsc_comm_check(svdsc_handle *h);
 /* In-process ("loopback") group: nranks (<= 16) ranks that are threads of this
  * process, each with its own handle and stream (on one device, or on devices
  * with peer access enabled by the caller).  Each rank's thread calls

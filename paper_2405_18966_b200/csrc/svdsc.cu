@@ -1283,10 +1283,49 @@ svdsc_status svdsc_comm_init(svdsc_handle *h, int nranks, int rank, const unsign
         h->comm = nullptr;
         h->nranks = 1;
         h->rank = 0;
-        if (nranks == 1) return;
+        // (a one-rank communicator is created too: the solver runs its single-GPU
+        // path, svdsc_comm_check exercises the collectives)
         h->comm = comm_nccl_create(id, nranks, rank);
         h->nranks = nranks;
         h->rank = rank;
+    });
+}
+
+svdsc_status svdsc_comm_check(svdsc_handle *h) {
+    if (!h) return SVDSC_EINVAL;
+    return guarded(h, [&] {
+        einval(!h->comm, "no communicator (svdsc_comm_init / svdsc_comm_init_group first)");
+        Comm *c = h->comm;
+        const int P = c->nranks, r = c->rank;
+        constexpr int E = 5, A = 7;
+        cudaStream_t s = h->stream;
+        std::vector<double> hb((size_t)2 * E + 2 * (size_t)E * P + A);
+        double *ag_in = hb.data(), *ag_out = ag_in + E, *rs_in = ag_out + (size_t)E * P, *rs_out = rs_in + (size_t)E * P,
+               *ar = rs_out + E;
+        for (int i = 0; i < E; i++) ag_in[i] = r * 10 + i;
+        for (int i = 0; i < E * P; i++) rs_in[i] = (double)(r + 1) * (i + 1);
+        for (int i = 0; i < A; i++) ar[i] = r + 1 + i;
+        double *d = nullptr;
+        ck(cudaMalloc(&d, hb.size() * sizeof(double)), "cudaMalloc");
+        struct Free {
+            double *p;
+            ~Free() { cudaFree(p); }
+        } fr{d};
+        ck(cudaMemcpyAsync(d, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+        const size_t o_ago = E, o_rsi = o_ago + (size_t)E * P, o_rso = o_rsi + (size_t)E * P, o_ar = o_rso + E;
+        c->allgather(d, d + o_ago, E, s);
+        c->reduce_scatter_sum(d + o_rsi, d + o_rso, E, s);
+        c->allreduce_sum(d + o_ar, A, s);
+        ck(cudaMemcpyAsync(hb.data(), d, hb.size() * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+        const int mn = c->allreduce_min_int(r + 3, s);
+        const double tri = 0.5 * P * (P + 1);
+        bool ok = mn == 3;
+        for (int q = 0; q < P; q++)
+            for (int i = 0; i < E; i++) ok = ok && ag_out[q * E + i] == q * 10 + i;
+        for (int i = 0; i < E; i++) ok = ok && rs_out[i] == tri * (r * E + i + 1);
+        for (int i = 0; i < A; i++) ok = ok && ar[i] == tri + (double)P * i;
+        if (!ok) throw CommError(SVDSC_ENCCL, "communicator check: collective results differ from the expected sums");
     });
 }
 
@@ -1310,7 +1349,6 @@ svdsc_status svdsc_comm_init_group(svdsc_handle *h, svdsc_group *g, int rank) {
         h->comm = nullptr;
         h->nranks = 1;
         h->rank = 0;
-        if (g->nranks() == 1) return;
         h->comm = comm_loopback_create(g->g, rank);
         h->nranks = g->nranks();
         h->rank = rank;

@@ -69,7 +69,7 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
            "svdsc_op_cgs2", "svdsc_op_small_svd", "svdsc_op_recombine", "svdsc_op_lbp",
            "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows",
            "svdsc_profile_enable", "svdsc_profile_read", "svdsc_set_policy",
-           "svdsc_group_create", "svdsc_group_destroy", "svdsc_comm_init_group"]
+           "svdsc_group_create", "svdsc_group_destroy", "svdsc_comm_init_group", "svdsc_comm_check"]
 # svdsc_set_policy keys / values (include/svdsc.h)
 POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD = 0, 1, 2
 SPMV = {"auto": 0, "bins": 1, "seg": 2}
@@ -121,6 +121,7 @@ def lib():
         L.svdsc_group_destroy.argtypes = [P]
         L.svdsc_group_destroy.restype = None
         L.svdsc_comm_init_group.argtypes = [P, P, ctypes.c_int]
+        L.svdsc_comm_check.argtypes = [P]
         # the paper's interface (include/svdsc_paper.h)
         PM, PC = ctypes.POINTER(PaperMat), ctypes.POINTER(PaperCsr)
         for f in ("svds_C", "svds_C_opt"):
@@ -181,6 +182,10 @@ class Handle:
     def comm_init(self, nranks, rank, uid: bytes):
         self._check(lib().svdsc_comm_init(self.ptr, nranks, rank, uid))
         self.nranks, self.rank = nranks, rank
+
+    def comm_check(self):
+        """Collective self-check of the communicator (svdsc_comm_check; every rank)."""
+        self._check(lib().svdsc_comm_check(self.ptr))
 
     def comm_init_group(self, group: "Group", rank):
         """Join an in-process loopback group (svdsc_comm_init_group)."""

@@ -150,3 +150,61 @@ def test_loopback_breakdown_and_restarts(S):
         assert not isinstance(o, Exception), o
     assert out[0][4]["restarts"] >= 1
     assert np.abs(out[0][1] - r2.S).max() <= 1e-10 * r2.S[0]
+
+
+def test_comm_check_nccl_one_rank(S):
+    """The NCCL communicator code (runtime-loaded libnccl, ncclCommInitRank and
+    every collective wrapper of comm.cu) on the one GPU of the box: a one-rank
+    communicator passes svdsc_comm_check, and a solve on that handle (single-GPU
+    path) is bitwise equal to one without a communicator."""
+    uid = S.comm_unique_id()
+    assert len(uid) == 128
+    wl = W.config(1, scale=2)
+    res = []
+    for with_comm in (False, True):
+        h = S.Handle()
+        if with_comm:
+            h.comm_init(1, 0, uid)
+            h.comm_check()
+        M = S.Matrix.from_host(h, wl.A)
+        r = S.svds_c(M, wl.k, tol=wl.tol, t=wl.t, maxit=wl.maxit, v0=torch.from_numpy(wl.v0).cuda(), fixed_passes=3)
+        res.append((r.S.cpu().numpy(), r.U.cpu().numpy(), r.V.cpu().numpy()))
+        M.close()
+        h.close()
+    for a, b in zip(res[0], res[1]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_comm_check_loopback(S, P):
+    g = S.Group(P)
+    errs = [None] * P
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                h = S.Handle(st)
+                h.comm_init_group(g, r)
+                h.comm_check()
+                h.close()
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+        assert not t.is_alive(), "a rank hung"
+    g.close()
+    assert errs == [None] * P, errs
+
+
+def test_comm_check_without_communicator(S):
+    h = S.Handle()
+    with pytest.raises(S.SvdscError) as e:
+        h.comm_check()
+    assert e.value.status == -1
+    h.close()
