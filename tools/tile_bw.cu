@@ -101,14 +101,14 @@ int main(int argc, char **argv) {
     {                                                                                                  \
         int64_t rpb = ((N + nsm - 1) / nsm + RT - 1) / RT * RT;                                        \
         size_t smem = (size_t)NS * C * RT * 8;                                                         \
-        if (smem <= 220 * 1024) {                                                                      \
-            cudaFuncSetAttribute(k_tiles<RT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
+        if (smem <= 227 * 1024) {                                                                      \
+            cudaFuncSetAttribute(k_tiles<RT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
             char nm[64];                                                                               \
             snprintf(nm, 64, "tiles RT=%d NS=%d", RT, NS);                                             \
             timeit(nm, [&] { k_tiles<RT, NS><<<nsm, 512, smem>>>(Q, N, C, rpb, sink); });              \
         }                                                                                              \
     }
-    TILES(32, 2) TILES(32, 3) TILES(16, 4) TILES(16, 6) TILES(8, 8) TILES(64, 1)
+    TILES(32, 2) TILES(32, 3) TILES(32, 4) TILES(16, 4) TILES(16, 6) TILES(64, 2) TILES(64, 3) TILES(128, 2)
 #define DIRECT(U, G)                                                                          \
     {                                                                                         \
         int64_t rpb = ((N + nsm * G - 1) / (nsm * G) + 1) / 2 * 2;                            \
