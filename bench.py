@@ -280,6 +280,7 @@ def run_loopback(args):
                    "passes_per_solve": passes, "parallelism": f"rows{P}",
                    "rows_per_rank": [int(bounds[r + 1] - bounds[r]) for r in range(P)]},
         "sigma_identical_on_all_ranks": same, "sigma_1": float(s0[0]),
+        "e2e": None,  # (a host-logic harness: no end-to-end measurement)
     }), flush=True)
     return 0
 
@@ -294,6 +295,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-rows", action="store_true",
+                    help="measure e2e the multi-GPU way (each rank copies its rows in and U/S/V out around "
+                         "svdsc_matrix_csr + svdsc_solve) even on one GPU (the default for --gpus > 1)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "loopback"],
                     help="nccl: one process per GPU (the product path); loopback: --gpus N ranks as threads "
                          "of this process on the visible GPUs (round robin), host-synchronized collectives "
@@ -506,9 +510,69 @@ def main():
     step_bytes = res.info["bytes_model"] / max(res.info["steps"], 1)
     total_prof = sum(v[0] for v in prof_all.values())
 
-    # ---- end to end through the host-buffer C-ABI entry point ----
+    # ---- end to end, multi-GPU: every rank copies its rows of A (pinned host)
+    # in, analyses and solves through the device-buffer C ABI (svdsc_matrix_*
+    # + svdsc_solve, the calls a multi-GPU user makes) and copies S, its rows of
+    # U and V out; timed per rank on its stream between barriers, max over ranks
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and (world > 1 or args.e2e_rows):
+        if Al.kind == "dense":
+            hA = torch.from_numpy(np.asfortranarray(Al.dense).T.copy()).pin_memory()  # (n, m): column-major A
+            h2d_r = 8 * Al.m * Al.n
+        else:
+            hrp = torch.from_numpy(np.ascontiguousarray(Al.row_ptr, np.int64)).pin_memory()
+            hci = torch.from_numpy(np.ascontiguousarray(Al.col_idx, np.int32)).pin_memory()
+            hva = torch.from_numpy(np.ascontiguousarray(Al.values, np.float64)).pin_memory()
+            h2d_r = 8 * (Al.m + 1) + 12 * Al.nnz
+        hv0 = torch.from_numpy(wl_full.v0).pin_memory()
+        h2d_r += 8 * wl_full.v0.size
+        hS = torch.empty(k, dtype=torch.float64).pin_memory()
+        hU = torch.empty((k, Al.m), dtype=torch.float64).pin_memory()
+        hV = torch.empty((k, n_cols), dtype=torch.float64).pin_memory()
+        d2h_r = 8 * (k + Al.m * k + n_cols * k)
+
+        def e2e_solve():
+            if Al.kind == "dense":
+                Md = S.Matrix.dense(H, hA.to(dev, non_blocking=True).t(), row_offset=r0, m_global=m_global)
+            else:
+                Md = S.Matrix.csr(H, hrp.to(dev, non_blocking=True), hci.to(dev, non_blocking=True),
+                                  hva.to(dev, non_blocking=True), n_cols, row_offset=r0, m_global=m_global)
+            r = S.svds_c(Md, k, tol=wl_full.tol, maxit=wl_full.maxit, t=t, v0=hv0.to(dev, non_blocking=True),
+                         reorth=args.reorth)
+            hS.copy_(r.S, non_blocking=True)
+            hU.copy_(r.U.t(), non_blocking=True)
+            hV.copy_(r.V.t(), non_blocking=True)
+            torch.cuda.current_stream().synchronize()  # the host buffers are the result
+            Md.close()
+            return r.info["steps"]
+
+        e2e_solve()  # warm
+        e2e_steps, e2e_ms = 0, 0.0
+        for _ in range(args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_steps += e2e_solve()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([e2e_ms, float(h2d_r), float(d2h_r)], device=dev, dtype=torch.float64)
+            mx = tt[:1].clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            e2e_ms, h2d, d2h = float(mx.item()), int(tt[1].item()), int(tt[2].item())
+        else:
+            h2d, d2h = h2d_r, d2h_r
+        e2e = {"value": e2e_steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.e2e_steps,
+               "note": "every rank: pinned host rows of A and v0 in, S and its rows of U / V out, matrix analysis "
+                       "and solve through svdsc_matrix_* + svdsc_solve; bytes summed over the ranks, time = max "
+                       "over the ranks"}
+    # ---- end to end through the host-buffer C-ABI entry point ----
+    if not args.no_e2e and world == 1 and not args.e2e_rows:
         e2e_steps, e2e_ms, h2d, d2h = 0, 0.0, 0, 0
         if Al.kind == "dense":
             hostA = torch.empty((Al.n, Al.m), dtype=torch.float64).pin_memory()
