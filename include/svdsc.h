@@ -169,6 +169,30 @@ SVDSC_API svdsc_status svdsc_op_matvec(svdsc_matrix *M, int trans, const double 
  * SVDSC_POLICY_CGS2 overrides).  Synchronous. */
 SVDSC_API svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const double *Q,
                            int64_t ldq, double *w, double *norm_dev);
+/* a2-a4 / a6 across P row-partitioned ranks, the multi-GPU re-orthogonalization
+ * of SURVEY.md 8(f2) (BASELINE.json north_star (e): all-reduce of the
+ * Gram-Schmidt coefficient vectors): ONE kernel per half-step whose two global
+ * reductions (h1 = Q^T w and [h2 = Q^T w'; ||w'||^2]) and the rare
+ * explicit norm are completed across the ranks inside the kernel -- each rank
+ * pushes its column sums into every rank's mailbox and sums the P slots in rank
+ * order.  The solver runs this kernel for P > 1 over NCCL (one process per GPU,
+ * mailboxes mapped through CUDA IPC / NVLink).  This entry point EMULATES P
+ * ranks on the handle's one GPU as P groups of CTAs of one cooperative launch
+ * (kernels that wait on one another are never separate launches on one GPU),
+ * each group with its own operands, scratch and mailbox: the same kernel code
+ * and protocol, for tests.
+ *   P: 1..8 ranks; row0: host array of P+1 row offsets (row0[0] = 0,
+ *   row0[P] = N, every row0[q] even, every rank >= 1 row); rank q owns rows
+ *   [row0[q], row0[q+1]) of the device basis Q (N x ncols, column-major,
+ *   ldq >= N, even, 16-byte aligned; ncols <= 384) and of the device vector w
+ *   (16-byte aligned), re-orthogonalized and normalized in place.
+ *   beta_out: host array of P: the norm each rank computed (bitwise equal on
+ *   every rank; 0 on breakdown, reading Q7).
+ * Errors: SVDSC_EINVAL (arguments), SVDSC_ECUDA (launch; e.g. fewer than P
+ * SMs), SVDSC_ENCCL (a group never arrived: protocol failure).  Synchronous. */
+SVDSC_API svdsc_status svdsc_op_cgs2_peer_emulate(svdsc_handle *h, int32_t P, const int64_t *row0,
+                                                  int64_t ncols, const double *Q, int64_t ldq, double *w,
+                                                  double *beta_out);
 /* a7: SVD of the p x p column-major device matrix Tm (Alg. 2 step 4) by the
  * device one-sided Jacobi: U, V (p x p, ld p) and S (p, descending), sign rule
  * of SPEC.md:158.  Returns SVDSC_ESVD_NOCONV after 50 sweeps.  Synchronous. */
@@ -215,7 +239,11 @@ SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int
  *   SVDSC_POLICY_CGS2:      0 auto (cluster for bases <= 2 MB, else Q-resident
  *                           when the rows fit in shared memory, else streaming),
  *                           1 split sweeps, 2 Q-resident, 3 cp.async streaming,
- *                           4 TMA streaming, 5 thread-block cluster
+ *                           4 TMA streaming, 5 thread-block cluster, 6 peer
+ *                           (the multi-GPU kernel with in-kernel all-reduces,
+ *                           also at P = 1 with a communicator), 7 phased (P > 1:
+ *                           three launches with NCCL all-reduces between them);
+ *                           set it identically on every rank
  *   SVDSC_POLICY_SMALL_SVD: 0 auto (register Jacobi for p <= 64, else cluster
  *                           block Jacobi + rotation replay), 1 one-CTA Jacobi,
  *                           2 register Jacobi (p <= 64, else auto), 3 cluster

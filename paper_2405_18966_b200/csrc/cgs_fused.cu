@@ -86,6 +86,36 @@ __device__ __forceinline__ void grid_sync(unsigned int *flags, unsigned int v) {
 __device__ __forceinline__ void grid_prepare(unsigned int *flags, unsigned int epoch) {
     if (blockIdx.x == 0 && threadIdx.x == 0) flags[2 + (((epoch >> 4) + 1) & (kBarSlots - 1))] = 0u;
 }
+// the same over a group of nb CTAs (bid = index in the group): the grid of one
+// rank in an emulated multi-rank launch, else the whole grid
+__device__ __forceinline__ void grid_sync_n(unsigned int *flags, unsigned int v, int nb) {
+    unsigned int *ctr = flags + 2 + ((v >> 4) & (kBarSlots - 1));
+    const unsigned int target = (v & 15u) * (unsigned)nb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_add(ctr, 1u);
+        while (ld_acquire(ctr) < target) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void grid_prepare_n(unsigned int *flags, unsigned int epoch, int bid) {
+    if (bid == 0 && threadIdx.x == 0) flags[2 + (((epoch >> 4) + 1) & (kBarSlots - 1))] = 0u;
+}
+// system scope (another GPU's memory over NVLink): peer mailbox protocol
+__device__ __forceinline__ void red_release_sys_add(unsigned int *p, unsigned int v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// a peer that never arrives (a dead rank) ends the wait after ~2^34 cycles
+// (~9 s) with ctrl->abort_kind = 2 instead of hanging the job
+constexpr long long kPeerTimeoutCycles = 1LL << 34;
 
 constexpr int kTile = 16;
 
@@ -454,6 +484,9 @@ struct SArgs {
     int phase;
     const int *gate;      // partial re-orthogonalization gate (FusedScratch::gate)
     int gate_want;
+    // peer instantiation (k_cgs2_stream2p, cgs2_peer): the rank's mailbox, whose
+    // one-shot all-reduces replace the host all-reduces of the phased launches
+    const PeerArgs *peer;
 };
 
 template <int RT>
@@ -498,10 +531,10 @@ __device__ __forceinline__ void issue_tile(const SArgs &a, double *buf, double *
 
 // one warp per column (fixed lane-strided order + xor tree: deterministic);
 // a block-wide reduction per column cost ~2 us per column (3 __syncthreads)
-__device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double *) {
-    const int nb = gridDim.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int tw = gridDim.x * nw;
-    for (int j = blockIdx.x * nw + (threadIdx.x >> 5); j < ncols_tot; j += tw) {
+__device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, int bid, int nb) {
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int tw = nb * nw;
+    for (int j = bid * nw + (threadIdx.x >> 5); j < ncols_tot; j += tw) {
         double s = 0.0;
         for (int t = lane; t < nb; t += 32) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
         s = warp_sum(s);
@@ -515,12 +548,15 @@ __device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, double 
 // (h1, h2) accumulate in registers across all tiles and are combined across
 // warps once per phase; row dots (w', w'') are one warp reduction per row.
 // The tile body has no __syncthreads (only the cp.async ring's two per tile).
-template <int RT, int NS, int M>
-__global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
+// bid / nb: this CTA's index among the rank's CTAs and their number (the grid,
+// except in an emulated multi-rank launch).  PEER: the global reductions are
+// completed across the ranks inside the kernel (PeerArgs, internal.h).
+template <int RT, int NS, int M, bool PEER>
+__device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid, const int nb) {
     constexpr int kSThr = 512, NW = 16, RPW = RT / NW, kCh = RT / 2;
-    grid_prepare(a.flags, a.epoch);
+    grid_prepare_n(a.flags, a.epoch, bid);
     if (*(volatile int *)&a.ctrl->abort) return;
-    if (a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
+    if (!PEER && a.gate && *(volatile const int *)a.gate != a.gate_want) return;  // PRO gate, uniform
     unsigned int nbar = 0;
     extern __shared__ __align__(16) double smem_s[];
     __shared__ double sh[32];
@@ -532,7 +568,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
     // NW x ncols cross-warp column sums: aliases the ring, which is idle when
     // a phase flushes (its last tile consumed, the next prefetch not issued)
     double *red = buf;
-    const int64_t rb = (int64_t)blockIdx.x * a.rpb;
+    const int64_t rb = (int64_t)bid * a.rpb;
     const int64_t re = min(a.N, rb + a.rpb);
     const int ntiles = rb < re ? (int)((re - rb + RT - 1) / RT) : 0;
     const int sw = lane & (kCh - 1);  // swizzle term of every column this lane owns
@@ -659,7 +695,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
                 for (int w = 0; w < NW; w++) s += red[w * ncols + j];
             else
                 for (int w = 0; w < NW; w++) s += red[NW * ncols + w];
-            a.partial[(int64_t)blockIdx.x * a.PS + j] = s;
+            a.partial[(int64_t)bid * a.PS + j] = s;
         }
         __syncthreads();
     };
@@ -668,6 +704,60 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
         for (int m = 0; m < M; m++) {
             const int j = lane + 32 * m;
             hreg[m] = j < ncols ? __ldcg(h + j) : 0.0;
+        }
+    };
+    // PEER: one-shot all-reduce of this rank's CTA partials [.][0, nc) across
+    // the ranks (PeerArgs, internal.h).  The warp that owns column j forms the
+    // rank's sum in sreduce_cols' order, lane q stores it into slot [par][rank]
+    // of rank q's mailbox; every CTA then releases one arrival to every rank
+    // and waits for the P x nb arrivals of this reduction on its own counter.
+    // Returns this rank's [P][PS] slots of the reduction (summed by the caller).
+    unsigned int seq0 = 0, npeer = 0;
+    if constexpr (PEER) seq0 = *(volatile const unsigned int *)a.peer->seq;
+    auto peer_exchange = [&](int nc) -> const double * {
+        const PeerArgs *pa = a.peer;
+        const int P = pa->P, PS = pa->PS;
+        const unsigned int rs = seq0 + (++npeer);
+        const int par = (int)(rs & 1u);
+        const int64_t slot = ((int64_t)par * P + pa->rank) * PS;
+        for (int j = bid * NW + wid; j < nc; j += nb * NW) {
+            double s = 0.0;
+            for (int t = lane; t < nb; t += 32) s += __ldcg(a.partial + (int64_t)t * a.PS + j);
+            s = warp_sum(s);
+            if (lane < P) __stcg(pa->mbox_peer[lane] + slot + j, s);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            for (int q = 0; q < P; q++) red_release_sys_add(pa->ctr_peer[q] + par, 1u);
+            const unsigned int target = ((rs + 1u) >> 1) * pa->expect;
+            const long long t0 = clock64();
+            while (ld_acquire_sys(pa->ctr + par) < target) {
+                if (clock64() - t0 > kPeerTimeoutCycles) {
+                    a.ctrl->abort_check = a.check;
+                    a.ctrl->abort_kind = 2;
+                    __threadfence();
+                    a.ctrl->abort = 1;
+                    break;
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        return pa->mbox + (int64_t)par * P * PS;
+    };
+    // sum over the ranks in rank order of entry j of the slots
+    auto peer_entry = [&](const double *sl, int j) -> double {
+        const PeerArgs *pa = a.peer;
+        double s = __ldcg(sl + j);
+        for (int q = 1; q < pa->P; q++) s += __ldcg(sl + (int64_t)q * pa->PS + j);
+        return s;
+    };
+    auto peer_h = [&](const double *sl, double (&hreg)[M]) {
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int j = lane + 32 * m;
+            hreg[m] = j < ncols ? peer_entry(sl, j) : 0.0;
         }
     };
 
@@ -685,7 +775,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
                 if (lane == q * kHalf && r < re) a.w[r] = W[rr] - s[q];
             }
         });
-        grid_sync(a.flags, a.epoch + (++nbar));
+        grid_sync_n(a.flags, a.epoch + (++nbar), nb);
     }
 
     double nrm_wp = 0.0;
@@ -710,12 +800,18 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             prefetch();  // phase B re-reads the same tiles: start them under the reduction
             prefetched = true;
         }
-        grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, ncols, a.h1, sh);
-        if (ph == 1) return;  // the host all-reduces h1 across the ranks
-        grid_sync(a.flags, a.epoch + (++nbar));
+        grid_sync_n(a.flags, a.epoch + (++nbar), nb);
+        if constexpr (PEER) {
+            peer_h(peer_exchange(ncols), hreg);
+        } else {
+            sreduce_cols(a, ncols, a.h1, bid, nb);
+            if (ph == 1) return;  // the host all-reduces h1 across the ranks
+            grid_sync_n(a.flags, a.epoch + (++nbar), nb);
+            load_h(a.h1, hreg);
         }
-        load_h(a.h1, hreg);
+        } else {
+            load_h(a.h1, hreg);
+        }
         // phase B: w' = w - Q h1 (written back), partial h2, ||w'||^2
 #pragma unroll
         for (int m = 0; m < M; m++) acc[m] = 0.0;
@@ -780,10 +876,11 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             }
         });
     }
+    const double *sl2 = nullptr;  // PEER: the slots of the [h2; ||w'||^2] exchange
     if (ph == 0 || ph == 2) {
         if (ncols == 0) {
             const double bn = block_sum_all(nrm_wp, sh);
-            if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS + ncols] = bn;
+            if (tid == 0) a.partial[(int64_t)bid * a.PS + ncols] = bn;
         }
         if (ncols > 0 && ph == 0) {  // phase C reads w' written above by this CTA
             __threadfence();
@@ -791,13 +888,23 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             prefetch();
             prefetched = true;
         }
-        grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, ncols + 1, a.h2, sh);
-        if (ph == 2) return;  // the host all-reduces [h2; ||w'||^2] across the ranks
-        grid_sync(a.flags, a.epoch + (++nbar));
+        grid_sync_n(a.flags, a.epoch + (++nbar), nb);
+        if constexpr (PEER) {
+            sl2 = peer_exchange(ncols + 1);
+        } else {
+            sreduce_cols(a, ncols + 1, a.h2, bid, nb);
+            if (ph == 2) return;  // the host all-reduces [h2; ||w'||^2] across the ranks
+            grid_sync_n(a.flags, a.epoch + (++nbar), nb);
+        }
     }
-    load_h(a.h2, hreg);
-    const double nrmp = __ldcg(a.h2 + ncols);
+    double nrmp;
+    if constexpr (PEER) {
+        peer_h(sl2, hreg);
+        nrmp = peer_entry(sl2, ncols);
+    } else {
+        load_h(a.h2, hreg);
+        nrmp = __ldcg(a.h2 + ncols);
+    }
     // ||h2||^2 from the coefficients every warp already holds (lane: columns
     // lane + 32 m, zeros past ncols); lane 0's butterfly result broadcast, so
     // every thread of every CTA uses the same value
@@ -845,7 +952,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
                     if (lane == q * kHalf && r < re) a.w[r] = W[rr] - s[q];
                 }
             });
-        if (blockIdx.x == 0 && tid == 0) {
+        if (bid == 0 && tid == 0) {
             a.ctrl->abort_check = a.check;
             a.ctrl->abort_kind = 1;
             __threadfence();
@@ -874,17 +981,24 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             for (int64_t r = rb + tid; r < re; r += kSThr) nrm2 = fma(a.w[r], a.w[r], nrm2);
         }
         const double bn = block_sum_all(nrm2, sh);
-        if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
-        grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, 1, a.h3, sh);
-        grid_sync(a.flags, a.epoch + (++nbar));
-        beta = sqrt(fmax(__ldcg(a.h3), 0.0));
+        if (tid == 0) a.partial[(int64_t)bid * a.PS] = bn;
+        grid_sync_n(a.flags, a.epoch + (++nbar), nb);
+        if constexpr (PEER) {
+            beta = sqrt(fmax(peer_entry(peer_exchange(1), 0), 0.0));
+        } else {
+            sreduce_cols(a, 1, a.h3, bid, nb);
+            grid_sync_n(a.flags, a.epoch + (++nbar), nb);
+            beta = sqrt(fmax(__ldcg(a.h3), 0.0));
+        }
         bd = !(beta > thr);
         if (!bd)
             for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
     }
     cp_wait<0>();  // a prefetch may be pending if phase C was skipped
-    if (blockIdx.x == 0 && tid == 0) {
+    if (bid == 0 && tid == 0) {
+        // every CTA read seq0 before the first grid barrier, so the next launch
+        // is the first to see the advanced count
+        if constexpr (PEER) *a.peer->seq = seq0 + npeer;
         if (bd) {
             *a.t_entry = 0.0;
             a.ctrl->amax[(a.check + 1) & 1] = amax;
@@ -896,6 +1010,24 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
             a.ctrl->amax[(a.check + 1) & 1] = fmax(amax, beta);
         }
     }
+}
+
+template <int RT, int NS, int M>
+__global__ void __launch_bounds__(512) k_cgs2_stream2(SArgs a) {
+    cgs2_stream2_body<RT, NS, M, false>(a, blockIdx.x, gridDim.x);
+}
+// multi-GPU (peer mailboxes).  grp == NULL: this rank's CTAs are the grid
+// (production, one launch per rank); else an emulated multi-rank launch on one
+// GPU: CTA group g = blockIdx.x / nb runs rank g with grp[g]
+template <int RT, int NS, int M>
+__global__ void __launch_bounds__(512) k_cgs2_stream2p(SArgs a) {
+    cgs2_stream2_body<RT, NS, M, true>(a, blockIdx.x, gridDim.x);
+}
+// test support: P ranks emulated as P CTA groups of one cooperative launch
+template <int RT, int NS, int M>
+__global__ void __launch_bounds__(512) k_cgs2_stream2e(const SArgs *__restrict__ grp, int nb) {
+    const int g = blockIdx.x / nb;
+    cgs2_stream2_body<RT, NS, M, true>(grp[g], blockIdx.x - g * nb, nb);
 }
 
 template <int RT, int NS, int M>
@@ -939,6 +1071,63 @@ bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
     if (nc <= 512) return launch_stream2<16, 2, 16>(a, nsm, s);
     if (nc <= 768) return launch_stream2<16, 2, 24>(a, nsm, s);
     return launch_stream2<16, 2, 32>(a, nsm, s);
+}
+
+// peer-mailbox streaming CGS2: ngroups = 1 (one rank per GPU, production) or P
+// (emulated ranks, grp_dev: device room for P SArgs).  nb CTAs per rank
+// whatever its row count (CTAs past the rows contribute zero partials), so
+// every rank releases the same number of arrivals (PeerArgs::expect).
+template <int RT, int NS, int M>
+bool launch_stream2p(SArgs *ga, int ngroups, int nb, void *grp_dev, cudaStream_t s) {
+    const int ncols = ga[0].ncols;
+    const size_t smem = ((size_t)NS * ncols * RT + NS * RT) * sizeof(double);
+    if (smem > 220 * 1024 || ncols > 32 * M || nb < 1) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cgs2_stream2p<RT, NS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if constexpr (RT == 32)
+            cudaFuncSetAttribute(k_cgs2_stream2e<RT, NS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    for (int g = 0; g < ngroups; g++) {
+        int64_t rpb = (ga[g].N + nb - 1) / nb;
+        rpb = std::max<int64_t>(RT, (rpb + RT - 1) / RT * RT);
+        ga[g].rpb = rpb;
+    }
+    cudaError_t e;
+    if (!grp_dev) {
+        void *args[] = {&ga[0]};
+        e = cudaLaunchCooperativeKernel((void *)k_cgs2_stream2p<RT, NS, M>, nb, 512, args, smem, s);
+    } else if constexpr (RT == 32) {  // emulation: bases up to 384 columns
+        if (cudaMemcpyAsync(grp_dev, ga, ngroups * sizeof(SArgs), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        const SArgs *grp = static_cast<const SArgs *>(grp_dev);
+        int nbk = nb;
+        void *args[] = {&grp, &nbk};
+        e = cudaLaunchCooperativeKernel((void *)k_cgs2_stream2e<RT, NS, M>, nb * ngroups, 512, args, smem, s);
+    } else {
+        return false;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    count_launch();
+    return true;
+}
+bool launch_stream2p_any(SArgs *ga, int ngroups, int nb, void *grp_dev, cudaStream_t s) {
+    const int nc = ga[0].ncols;
+    if (nc <= 64) return launch_stream2p<32, 4, 2>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 128) return launch_stream2p<32, 5, 4>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 192) return launch_stream2p<32, 4, 6>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 256) return launch_stream2p<32, 3, 8>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 320) return launch_stream2p<32, 2, 10>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 384) return launch_stream2p<32, 2, 12>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 512) return launch_stream2p<16, 2, 16>(ga, ngroups, nb, grp_dev, s);
+    if (nc <= 768) return launch_stream2p<16, 2, 24>(ga, ngroups, nb, grp_dev, s);
+    return launch_stream2p<16, 2, 32>(ga, ngroups, nb, grp_dev, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1169,7 +1358,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         flush_cols(acc);
         prefetch();
         grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, ncols, a.h1, sh);
+        sreduce_cols(a, ncols, a.h1, blockIdx.x, gridDim.x);
         grid_sync(a.flags, a.epoch + (++nbar));
         load_h(a.h1);
 #pragma unroll
@@ -1206,7 +1395,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         prefetch();
     }
     grid_sync(a.flags, a.epoch + (++nbar));
-    sreduce_cols(a, ncols + 1, a.h2, sh);
+    sreduce_cols(a, ncols + 1, a.h2, blockIdx.x, gridDim.x);
     grid_sync(a.flags, a.epoch + (++nbar));
     load_h(a.h2);
     const double nrmp = __ldcg(a.h2 + ncols);
@@ -1253,7 +1442,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_cgs2_tma(const __grid_consta
         const double bn = block_sum_all(nrm2, sh);
         if (tid == 0) a.partial[(int64_t)blockIdx.x * a.PS] = bn;
         grid_sync(a.flags, a.epoch + (++nbar));
-        sreduce_cols(a, 1, a.h3, sh);
+        sreduce_cols(a, 1, a.h3, blockIdx.x, gridDim.x);
         grid_sync(a.flags, a.epoch + (++nbar));
         beta = sqrt(fmax(__ldcg(a.h3), 0.0));
         bd = !(beta > thr);
@@ -1994,6 +2183,110 @@ bool cgs2_phased(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, 
     comm->allreduce_sum(fs.h2, (size_t)ncols + 1, s);
     launch(3);
     return true;
+}
+
+size_t peer_mailbox_bytes(int P, int PS) { return kPeerHdrBytes + (size_t)2 * P * PS * sizeof(double); }
+
+namespace {
+SArgs peer_sargs(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
+                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, const PeerArgs *peer) {
+    SArgs sa{};
+    sa.N = N;
+    sa.ncols = ncols;
+    sa.Q = Q;
+    sa.ldq = ldq;
+    sa.w = w;
+    sa.partial = fs.partial;
+    sa.PS = ncols + 2;
+    sa.h1 = fs.h1;
+    sa.h2 = fs.h2;
+    sa.h3 = fs.h3;
+    sa.flags = fs.flags;
+    sa.epoch = fs.epoch;
+    sa.gate = nullptr;
+    sa.ctrl = ctrl;
+    sa.t_entry = t_entry;
+    sa.check = check;
+    sa.pre_h = pre_h;
+    sa.snake = 1;
+    sa.phase = 0;
+    sa.peer = peer;
+    return sa;
+}
+bool peer_applicable(int ncols, const double *Q, int64_t ldq, const double *w) {
+    if (g_policy.cgs2 == 1) return false;
+    const bool aligned = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    return aligned && ncols <= 840;  // wider than the streaming kernel's shared-memory ring
+}
+}  // namespace
+
+// Multi-GPU CGS2 over peer memory: one launch per
+// re-orthogonalization; the h1 and [h2; ||w'||^2] all-reduces (and the rare
+// explicit norm, reading G3) run inside the kernel as one-shot pushes into the
+// ranks' mailboxes -- no NCCL call, no kernel boundary, no host round trip.
+bool cgs2_peer(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
+               const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nb, cudaStream_t s,
+               const PeerArgs *peer) {
+    if (!peer || N < 1 || !peer_applicable(ncols, Q, ldq, w)) return false;
+    SArgs sa = peer_sargs(N, ncols, Q, ldq, w, pre_h, fs, ctrl, t_entry, check, peer);
+    return launch_stream2p_any(&sa, 1, nb, nullptr, s);
+}
+
+size_t cgs2_peer_emulate_grp_bytes(int P) { return (size_t)P * sizeof(SArgs); }
+
+bool cgs2_peer_emulate(int P, int ncols, const PeerEmuRank *ranks, int nb, void *grp_dev, cudaStream_t s) {
+    if (P < 1 || P > kMaxPeers) return false;
+    std::vector<SArgs> ga((size_t)P);
+    for (int g = 0; g < P; g++) {
+        const PeerEmuRank &r = ranks[g];
+        if (r.N < 1 || !peer_applicable(ncols, r.Q, r.ldq, r.w)) return false;
+        ga[g] = peer_sargs(r.N, ncols, r.Q, r.ldq, r.w, nullptr, r.fs, r.ctrl, r.t_entry, 0, r.peer);
+    }
+    return launch_stream2p_any(ga.data(), P, nb, grp_dev, s);
+}
+
+namespace {
+// one CTA, one exchange of the peer protocol (the CGS2 kernel's, with nb = 1)
+__global__ void k_peer_check(const PeerArgs *pa, int n, double *out, Ctrl *ctrl) {
+    const int P = pa->P, PS = pa->PS;
+    const unsigned int rs = *(volatile const unsigned int *)pa->seq + 1u;
+    const int par = (int)(rs & 1u);
+    const int64_t slot = ((int64_t)par * P + pa->rank) * PS;
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        for (int q = 0; q < P; q++) __stcg(pa->mbox_peer[q] + slot + j, (double)(pa->rank + 1) * (double)(j + 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int q = 0; q < P; q++) red_release_sys_add(pa->ctr_peer[q] + par, 1u);
+        const unsigned int target = ((rs + 1u) >> 1) * (unsigned)P;  // one CTA per rank
+        const long long t0 = clock64();
+        while (ld_acquire_sys(pa->ctr + par) < target) {
+            if (clock64() - t0 > kPeerTimeoutCycles) {
+                ctrl->abort_kind = 2;
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    const double *sl = pa->mbox + (int64_t)par * P * PS;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        double s = __ldcg(sl + j);
+        for (int q = 1; q < P; q++) s += __ldcg(sl + (int64_t)q * PS + j);
+        out[j] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *pa->seq = rs;
+}
+}  // namespace
+
+// one arrival per rank instead of PeerArgs::expect: the caller runs it on
+// freshly reset counters (peer_reset + a collective), and the next solve resets
+// them again before its CGS2 kernels count P x nb arrivals per exchange
+void peer_check(const PeerArgs *peer, int n, double *out, Ctrl *ctrl, cudaStream_t s) {
+    k_peer_check<<<1, 256, 0, s>>>(peer, n, out, ctrl);
+    count_launch();
 }
 
 }  // namespace svdsc

@@ -88,9 +88,102 @@ void ckc(cudaError_t e, const char *what) {
 struct NcclComm : Comm {
     ncclComm_t c = nullptr;
     int *dint = nullptr;
+    // peer mailboxes (cgs2_peer): this rank's block (IPC-exported), the peers'
+    // blocks opened through CUDA IPC (NVLink P2P mappings), the device PeerArgs
+    bool peer_tried = false;
+    void *mbox_block = nullptr;
+    std::vector<void *> peer_blocks;
+    PeerArgs *peer_dev = nullptr;
     ~NcclComm() override {
+        peer_release();
         if (dint) cudaFree(dint);
         if (c && g_nccl.CommDestroy) g_nccl.CommDestroy(c);
+    }
+    void peer_release() {
+        for (void *p : peer_blocks)
+            if (p) cudaIpcCloseMemHandle(p);
+        peer_blocks.clear();
+        if (mbox_block) cudaFree(mbox_block);
+        if (peer_dev) cudaFree(peer_dev);
+        mbox_block = nullptr;
+        peer_dev = nullptr;
+        cudaGetLastError();
+    }
+    void peer_reset(cudaStream_t s) override {
+        if (mbox_block) ckc(cudaMemsetAsync(mbox_block, 0, kPeerHdrBytes, s), "peer mailbox reset");
+    }
+    // first call: allocate and zero this rank's mailbox, all-gather
+    // [ok, nsm, IPC handle] over NCCL, open every peer's block, agree (min) on
+    // success; on any failure every rank returns NULL (the phased path runs)
+    const PeerArgs *peer_setup(int nsm, cudaStream_t s) override {
+        if (peer_tried) return peer_dev;
+        peer_tried = true;
+        const int P = nranks;
+        if (P > kMaxPeers) return nullptr;
+        const size_t bytes = peer_mailbox_bytes(P, kPeerPS);
+        constexpr int kRec = 2 + (int)(sizeof(cudaIpcMemHandle_t) + 7) / 8;  // doubles per rank
+        std::vector<double> mine(kRec, 0.0), all((size_t)kRec * P, 0.0);
+        int ok = 1;
+        cudaIpcMemHandle_t h{};
+        if (cudaMalloc(&mbox_block, bytes) != cudaSuccess || cudaMemsetAsync(mbox_block, 0, bytes, s) != cudaSuccess ||
+            (P > 1 && cudaIpcGetMemHandle(&h, mbox_block) != cudaSuccess))
+            ok = 0;
+        cudaGetLastError();
+        mine[0] = ok;
+        mine[1] = nsm;
+        std::memcpy(mine.data() + 2, &h, sizeof(h));
+        double *dbuf = nullptr;
+        ckc(cudaMalloc(&dbuf, sizeof(double) * kRec * (P + 1)), "cudaMalloc");
+        ckc(cudaMemcpyAsync(dbuf + (size_t)kRec * P, mine.data(), sizeof(double) * kRec, cudaMemcpyHostToDevice, s),
+            "H2D");
+        allgather(dbuf + (size_t)kRec * P, dbuf, kRec, s);
+        ckc(cudaMemcpyAsync(all.data(), dbuf, sizeof(double) * kRec * P, cudaMemcpyDeviceToHost, s), "D2H");
+        ckc(cudaStreamSynchronize(s), "sync");
+        cudaFree(dbuf);
+        PeerArgs pa{};
+        pa.P = P;
+        pa.rank = rank;
+        pa.PS = kPeerPS;
+        pa.expect = (unsigned)(P * nsm);
+        for (int q = 0; q < P && ok; q++) {
+            if (all[(size_t)q * kRec] != 1.0 || all[(size_t)q * kRec + 1] != (double)nsm) ok = 0;
+        }
+        peer_blocks.assign(P, nullptr);
+        for (int q = 0; q < P && ok; q++) {
+            char *base = nullptr;
+            if (q == rank) {
+                base = static_cast<char *>(mbox_block);
+            } else {
+                cudaIpcMemHandle_t hq;
+                std::memcpy(&hq, all.data() + (size_t)q * kRec + 2, sizeof(hq));
+                void *p = nullptr;
+                if (cudaIpcOpenMemHandle(&p, hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    ok = 0;
+                    break;
+                }
+                peer_blocks[q] = p;
+                base = static_cast<char *>(p);
+            }
+            pa.ctr_peer[q] = reinterpret_cast<unsigned int *>(base);
+            pa.mbox_peer[q] = reinterpret_cast<double *>(base + kPeerHdrBytes);
+        }
+        if (ok) {
+            char *mb = static_cast<char *>(mbox_block);
+            pa.ctr = reinterpret_cast<unsigned int *>(mb);
+            pa.seq = reinterpret_cast<unsigned int *>(mb) + 2;
+            pa.mbox = reinterpret_cast<double *>(mb + kPeerHdrBytes);
+            if (cudaMalloc(&peer_dev, sizeof(PeerArgs)) != cudaSuccess ||
+                cudaMemcpyAsync(peer_dev, &pa, sizeof(PeerArgs), cudaMemcpyHostToDevice, s) != cudaSuccess)
+                ok = 0;
+            cudaGetLastError();
+        }
+        if (allreduce_min_int(ok, s) != 1) {
+            ckc(cudaStreamSynchronize(s), "sync");
+            peer_release();
+            return nullptr;
+        }
+        return peer_dev;
     }
     void allreduce_sum(double *buf, size_t n, cudaStream_t s) override {
         ckn(g_nccl.AllReduce(buf, buf, n, kNcclFloat64, kNcclSum, c, s), "ncclAllReduce");

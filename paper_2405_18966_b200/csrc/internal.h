@@ -163,7 +163,61 @@ struct FusedScratch {
 bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
                 const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nsm, cudaStream_t s,
                 const void *tmap);
+// Peer mailbox of one rank for the in-kernel one-shot all-reduces of the
+// multi-GPU CGS2 (cgs2_peer).  Lives in device memory.  Rank r
+// owns `mbox` = [2 parities][P slots][PS doubles] and two arrival counters; the
+// CGS2 kernel of rank q writes its column sums of reduction rs into slot
+// [rs & 1][q] of EVERY rank's mailbox (NVLink P2P stores through mbox_peer),
+// then adds 1 per CTA to every rank's counter [rs & 1] (red.release.sys); a CTA
+// proceeds once its own counter [rs & 1] holds ((rs + 1) / 2) * expect arrivals
+// and sums the P slots in rank order (bitwise identical on every rank, and
+// equal to the loopback backend's rank-ordered sums).  `seq` = reductions
+// completed so far on this rank; the counters and seq are zeroed at solve start
+// before the status agreement, which all ranks pass only after every rank has
+// zeroed (no arrival of the new solve can be lost).
+constexpr int kMaxPeers = 8;
+struct PeerArgs {
+    int P, rank;
+    int PS;                // slot stride in doubles (>= ncols + 1 of any call)
+    unsigned int expect;   // arrivals per reduction: P x CTAs per rank
+    double *mbox;          // this rank's mailbox [2][P][PS]
+    unsigned int *ctr;     // this rank's counters [2] (followed by seq)
+    unsigned int *seq;     // reductions completed on this rank
+    double *mbox_peer[kMaxPeers];       // rank q's mailbox, mapped in this rank's address space
+    unsigned int *ctr_peer[kMaxPeers];  // rank q's counters
+};
+// device bytes of one rank's mailbox block (counters, seq, slots) for P ranks
+size_t peer_mailbox_bytes(int P, int PS);
+// offsets inside that block
+constexpr size_t kPeerHdrBytes = 256;  // ctr[2], seq, padding; slots follow
+
 struct Comm;
+// P > 1, peer-memory backend: the whole CGS2 in ONE launch of the streaming
+// kernel, its two reductions (and the explicit norm, reading G3) completed
+// across the ranks inside the kernel through the peer mailboxes (no NCCL call,
+// no host round trip).  peer: device PeerArgs of this rank; nb: CTAs per rank
+// (identical on every rank).  false: not applicable.
+bool cgs2_peer(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
+               const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nb, cudaStream_t s,
+               const PeerArgs *peer);
+// test support (svdsc_op_cgs2_peer_emulate): P ranks emulated as P groups of
+// CTAs of ONE cooperative launch on one GPU, each group with its own operands,
+// scratch, control block and peer mailbox (mailboxes of the other groups as
+// its peers): the protocol of cgs2_peer without kernels that wait on other
+// launches.  grp: device array of P argument blocks prepared by
+// cgs2_peer_emulate_prepare.
+struct PeerEmuRank {
+    int64_t N;
+    const double *Q;
+    int64_t ldq;
+    double *w;
+    FusedScratch fs;
+    Ctrl *ctrl;
+    double *t_entry;
+    const PeerArgs *peer;
+};
+bool cgs2_peer_emulate(int P, int ncols, const PeerEmuRank *ranks, int nb, void *grp_dev, cudaStream_t s);
+size_t cgs2_peer_emulate_grp_bytes(int P);
 // P > 1: the streaming CGS2 in three launches with the cross-rank all-reduces of
 // h1 and [h2; ||w'||^2] between them; *launches is the per-solve fused-launch
 // counter (grid-barrier slot chain).  false: not applicable.
@@ -220,7 +274,21 @@ struct Comm {
     // blocking: the minimum of v over the ranks (status agreement before compute)
     virtual int allreduce_min_int(int v, cudaStream_t s) = 0;
     virtual void abort() {}  // a rank failed mid-solve: release the others (loopback)
+    // peer mailboxes of the in-kernel all-reduces (cgs2_peer).  peer_setup is
+    // collective (every rank, same point, after the status agreement): the first
+    // call allocates and exchanges the mailboxes, later calls return the same
+    // device PeerArgs; NULL on every rank when any rank cannot map its peers (or
+    // the backend has none: loopback, whose ranks share one GPU and must not run
+    // kernels that wait on one another).  peer_reset zeroes this rank's counters
+    // and seq on s; called at solve start BEFORE the status agreement.
+    virtual const PeerArgs *peer_setup(int nsm, cudaStream_t s) { return nullptr; }
+    virtual void peer_reset(cudaStream_t s) {}
 };
+// one-shot peer exchange self-check (svdsc_comm_check): every rank pushes
+// (rank + 1) (j + 1) for j < n through the mailboxes; out[j] = the rank-ordered
+// sum (device, n <= PS).  Advances seq like one CGS2 reduction.
+void peer_check(const PeerArgs *peer, int n, double *out, Ctrl *ctrl, cudaStream_t s);
+constexpr int kPeerPS = 1032;  // slot stride: >= t + 2 for t <= 1023
 bool comm_nccl_available();
 void comm_nccl_unique_id(unsigned char id[128]);
 Comm *comm_nccl_create(const unsigned char id[128], int nranks, int rank);

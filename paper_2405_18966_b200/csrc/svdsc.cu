@@ -361,12 +361,27 @@ struct Solver {
 
     bool fused_ok = true;
     unsigned int fused_launches = 0;
+    // peer mailboxes of the in-kernel all-reduces (NCCL backend, P > 1, or
+    // SVDSC_POLICY_CGS2 = 6 with a one-rank communicator); NULL: not used
+    const PeerArgs *peer = nullptr;
     alignas(64) unsigned char tmapU[128], tmapV[128];
     bool have_tmap = false;
     // re-orthogonalize wv against Q(:, 0:ncols) (optionally after wv -= Q pre_h),
     // then beta = ||wv||, breakdown test, T entry, wv /= beta.
     void orth_norm(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, double *t_entry, int chk,
                    const double *pre_h) {
+        if (peer && o->reorth != 0 && fused_ok) {
+            // one launch: CGS2 + norm + normalization with the cross-rank
+            // reductions completed inside the kernel
+            FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches), nullptr};
+            if (pending.partial) finish_pending(N, wv);
+            H->prof.begin(11, s);
+            const bool ok = cgs2_peer(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s, peer);
+            H->prof.end(s);
+            if (ok) return;
+            // not applicable (identical shapes on every rank: every rank falls back)
+            --fused_launches;
+        }
         if (P == 1 && o->reorth != 0 && fused_ok) {
             FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches),
                             pending.partial ? &pending : nullptr};
@@ -618,6 +633,8 @@ struct Solver {
             Ctrl c = read_ctrl();
             if (!c.abort) return;
             const int idx = c.abort_check;
+            if (c.abort_kind == 2)
+                throw CommError(SVDSC_ENCCL, "multi-GPU CGS2: a peer rank did not arrive at an in-kernel all-reduce");
             if (idx < 0 || idx >= (int)plan.size()) throw SvdscError(SVDSC_ECUDA, "breakdown bookkeeping");
             const int zero[2] = {0, 0};
             ck(cudaMemcpyAsync(&w.ctrl->abort, &zero[0], sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
@@ -789,6 +806,12 @@ svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o_in, void *ws, size_
         need = carve(probe, nullptr, M->m_local, M->n, sv.t, sv.k, sv.P);
         einval(ws && ws_bytes < need, "workspace too small (see svdsc_workspace_size)");
     });
+    // the peer CGS2 (P > 1 with a backend that maps peer memory, or forced by
+    // SVDSC_POLICY_CGS2 = 6): counters zeroed before the status agreement, so
+    // no rank's first arrival of this solve can precede another rank's reset
+    const bool want_peer = H->comm && oo.reorth == 2 && g_policy.cgs2 != 7 &&
+                           (H->nranks > 1 || g_policy.cgs2 == 6);
+    if (st == SVDSC_OK && want_peer) st = guarded(H, [&] { H->comm->peer_reset(H->stream); });
     if (H->nranks > 1) {
         int agreed = (int)st;
         const std::string local_err = H->err;
@@ -806,6 +829,7 @@ svdsc_status run_solver(svdsc_matrix *M, const svdsc_opts *o_in, void *ws, size_
         return st;
     }
     st = guarded(H, [&] {
+        if (want_peer) sv.peer = H->comm->peer_setup(H->nsm, sv.s);
         void *base = ws;
         const bool own = !base;
         if (own) base = pool_alloc(H, need, sv.s);
@@ -1219,6 +1243,84 @@ svdsc_status svdsc_op_cgs2(svdsc_handle *h, int64_t N, int64_t ncols, const doub
     });
 }
 
+svdsc_status svdsc_op_cgs2_peer_emulate(svdsc_handle *h, int32_t P, const int64_t *row0, int64_t ncols,
+                                        const double *Q, int64_t ldq, double *w, double *beta_out) {
+    if (!h) return SVDSC_EINVAL;
+    return guarded(h, [&] {
+        einval(P < 1 || P > kMaxPeers || !row0 || !w || !beta_out || ncols < 0 || ncols > 384, "bad arguments");
+        einval(row0[0] != 0, "row0[0] must be 0");
+        for (int q = 0; q < P; q++)
+            einval(row0[q + 1] <= row0[q] || (row0[q] & 1), "row0: ranks need >= 1 row and even offsets");
+        const int64_t N = row0[P];
+        einval(ncols > 0 && (!Q || ldq < N || (ldq & 1)), "bad basis");
+        einval((reinterpret_cast<uintptr_t>(w) & 15) || (ncols > 0 && (reinterpret_cast<uintptr_t>(Q) & 15)),
+               "Q and w must be 16-byte aligned");
+        const int nb = h->nsm / P;
+        einval(nb < 1, "fewer SMs than ranks");
+        cudaStream_t s = h->stream;
+        // per rank: Ctrl, partials [nb][ncols + 2], h1, h2, h3, T entry; mailbox block; PeerArgs
+        const int PSp = (int)ncols + 2;
+        const size_t mb = (peer_mailbox_bytes(P, kPeerPS) + 255) / 256 * 256;
+        const size_t per = (sizeof(Ctrl) + 255) / 256 * 256 + ((size_t)nb * PSp + 3 * (size_t)PSp + 8) * sizeof(double);
+        const size_t per_al = (per + 255) / 256 * 256;
+        const size_t total = (size_t)P * (per_al + mb) + P * sizeof(PeerArgs) + cgs2_peer_emulate_grp_bytes(P) + 512;
+        char *base = nullptr;
+        ck(cudaMalloc(&base, total), "cudaMalloc");
+        struct FreeB {
+            char *p;
+            ~FreeB() { cudaFree(p); }
+        } fb{base};
+        ck(cudaMemsetAsync(base, 0, total, s), "memset");
+        std::vector<PeerEmuRank> ranks((size_t)P);
+        std::vector<PeerArgs> pa((size_t)P);
+        char *mbox0 = base + (size_t)P * per_al;
+        PeerArgs *pa_dev = reinterpret_cast<PeerArgs *>(mbox0 + (size_t)P * mb);
+        void *grp_dev = reinterpret_cast<char *>(pa_dev) + ((P * sizeof(PeerArgs) + 255) / 256 * 256);
+        for (int q = 0; q < P; q++) {
+            char *r = base + (size_t)q * per_al;
+            Ctrl *ctrl = reinterpret_cast<Ctrl *>(r);
+            double *d = reinterpret_cast<double *>(r + (sizeof(Ctrl) + 255) / 256 * 256);
+            PeerEmuRank &e = ranks[q];
+            e.N = row0[q + 1] - row0[q];
+            e.Q = ncols > 0 ? Q + row0[q] : nullptr;
+            e.ldq = ncols > 0 ? ldq : 2;
+            e.w = w + row0[q];
+            e.fs = FusedScratch{d, d + (size_t)nb * PSp, d + (size_t)nb * PSp + PSp, d + (size_t)nb * PSp + 2 * PSp,
+                                ctrl->gflags, 16u, nullptr};
+            e.ctrl = ctrl;
+            e.t_entry = d + (size_t)nb * PSp + 3 * PSp;
+            e.peer = pa_dev + q;
+            PeerArgs &a = pa[q];
+            a.P = P;
+            a.rank = q;
+            a.PS = kPeerPS;
+            a.expect = (unsigned)(P * nb);
+            char *mq = mbox0 + (size_t)q * mb;
+            a.ctr = reinterpret_cast<unsigned int *>(mq);
+            a.seq = reinterpret_cast<unsigned int *>(mq) + 2;
+            a.mbox = reinterpret_cast<double *>(mq + kPeerHdrBytes);
+            for (int z = 0; z < P; z++) {
+                char *mz = mbox0 + (size_t)z * mb;
+                a.ctr_peer[z] = reinterpret_cast<unsigned int *>(mz);
+                a.mbox_peer[z] = reinterpret_cast<double *>(mz + kPeerHdrBytes);
+            }
+        }
+        ck(cudaMemcpyAsync(pa_dev, pa.data(), P * sizeof(PeerArgs), cudaMemcpyHostToDevice, s), "H2D");
+        if (!cgs2_peer_emulate(P, (int)ncols, ranks.data(), nb, grp_dev, s))
+            throw SvdscError(SVDSC_ECUDA, "emulated multi-rank CGS2 launch failed");
+        bool lost = false;
+        for (int q = 0; q < P; q++) {
+            Ctrl c;
+            ck(cudaMemcpyAsync(&c, ranks[q].ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaMemcpyAsync(beta_out + q, ranks[q].t_entry, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaStreamSynchronize(s), "sync");
+            lost = lost || (c.abort && c.abort_kind == 2);
+        }
+        ck(cudaGetLastError(), "cgs2 peer emulate");
+        if (lost) throw CommError(SVDSC_ENCCL, "emulated peer exchange timed out");
+    });
+}
+
 svdsc_status svdsc_op_small_svd(svdsc_handle *h, int32_t p, const double *Tm, double *U, double *S, double *V,
                                 int32_t *sweeps) {
     if (!h) return SVDSC_EINVAL;
@@ -1326,6 +1428,29 @@ svdsc_status svdsc_comm_check(svdsc_handle *h) {
         for (int i = 0; i < E; i++) ok = ok && rs_out[i] == tri * (r * E + i + 1);
         for (int i = 0; i < A; i++) ok = ok && ar[i] == tri + (double)P * i;
         if (!ok) throw CommError(SVDSC_ENCCL, "communicator check: collective results differ from the expected sums");
+        // the peer mailboxes (NCCL backend): one in-kernel exchange
+        c->peer_reset(s);
+        (void)c->allreduce_min_int(0, s);  // every rank has reset before any arrival
+        const PeerArgs *pa = c->peer_setup(h->nsm, s);
+        if (pa) {
+            constexpr int X = 9;
+            OpScratch sc = op_scratch(h, 0, 1);
+            double *dx = nullptr;
+            ck(cudaMalloc(&dx, X * sizeof(double)), "cudaMalloc");
+            Free fx{dx};
+            ck(cudaMemsetAsync(sc.ctrl, 0, sizeof(Ctrl), s), "memset");
+            peer_check(pa, X, dx, sc.ctrl, s);
+            double hx[X];
+            Ctrl cc;
+            ck(cudaMemcpyAsync(hx, dx, sizeof(hx), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaMemcpyAsync(&cc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaStreamSynchronize(s), "sync");
+            ck(cudaGetLastError(), "peer_check");
+            bool pok = cc.abort_kind != 2;
+            for (int j = 0; j < X; j++) pok = pok && hx[j] == tri * (j + 1);
+            if (c->allreduce_min_int(pok ? 1 : 0, s) != 1)
+                throw CommError(SVDSC_ENCCL, "communicator check: peer-mailbox exchange failed");
+        }
     });
 }
 
@@ -1357,7 +1482,7 @@ svdsc_status svdsc_comm_init_group(svdsc_handle *h, svdsc_group *g, int rank) {
 
 svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t value) {
     if (!h) return SVDSC_EINVAL;
-    const int maxv[3] = {2, 5, 3};
+    const int maxv[3] = {2, 7, 3};
     if (key < 0 || key > 2 || value < 0 || value > maxv[key]) {
         h->err = "svdsc_set_policy: unknown key or value";
         return SVDSC_EINVAL;

@@ -66,14 +66,14 @@ class PaperMat(ctypes.Structure):
 EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_error", "svdsc_version",
            "svdsc_matrix_csr", "svdsc_matrix_dense", "svdsc_matrix_destroy", "svdsc_workspace_size",
            "svdsc_solve", "svdsc_solve_host_csr", "svdsc_solve_host_dense", "svdsc_op_matvec",
-           "svdsc_op_cgs2", "svdsc_op_small_svd", "svdsc_op_recombine", "svdsc_op_lbp",
+           "svdsc_op_cgs2", "svdsc_op_cgs2_peer_emulate", "svdsc_op_small_svd", "svdsc_op_recombine", "svdsc_op_lbp",
            "svdsc_comm_unique_id", "svdsc_comm_init", "svdsc_partition_rows",
            "svdsc_profile_enable", "svdsc_profile_read", "svdsc_set_policy",
            "svdsc_group_create", "svdsc_group_destroy", "svdsc_comm_init_group", "svdsc_comm_check"]
 # svdsc_set_policy keys / values (include/svdsc.h)
 POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD = 0, 1, 2
 SPMV = {"auto": 0, "bins": 1, "seg": 2}
-CGS2 = {"auto": 0, "split": 1, "qs": 2, "stream": 3, "tma": 4, "cluster": 5}
+CGS2 = {"auto": 0, "split": 1, "qs": 2, "stream": 3, "tma": 4, "cluster": 5, "peer": 6, "phased": 7}
 SMALL_SVD = {"auto": 0, "one_cta": 1, "register": 2, "block": 3}
 PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",
                  "recombine", "restart_misc", "collectives", "cgs2_fused", "pro_decide"]
@@ -107,6 +107,7 @@ def lib():
                                              ctypes.POINTER(Info)]
         L.svdsc_op_matvec.argtypes = [P, ctypes.c_int, P, P, P, P]
         L.svdsc_op_cgs2.argtypes = [P, I64, I64, P, I64, P, P]
+        L.svdsc_op_cgs2_peer_emulate.argtypes = [P, I32, P, I64, P, I64, P, P]
         L.svdsc_op_small_svd.argtypes = [P, I32, P, P, P, P, ctypes.POINTER(I32)]
         L.svdsc_op_recombine.argtypes = [P, I64, I32, I32, P, I64, P, I32, P, I64]
         L.svdsc_op_lbp.argtypes = [P, ctypes.POINTER(Opts), I32, P, P, I64, P, I64, P,
@@ -409,6 +410,23 @@ def cgs2(h: Handle, Q, w):
     ldq = _ld(Q) if ncols else N
     h._check(lib().svdsc_op_cgs2(h.ptr, N, ncols, _ptr(Q) if ncols else None, ldq, _ptr(w), _ptr(nrm)))
     return w, nrm
+
+
+def cgs2_peer_emulate(h: Handle, Q, w, row0):
+    """f2: the multi-GPU CGS2 (in-kernel peer all-reduces) with len(row0)-1 ranks
+    emulated on one GPU; rank q owns rows row0[q]:row0[q+1].  Returns (w, betas)
+    with w re-orthogonalized and normalized in place on a padded copy."""
+    N = w.numel()
+    wp = torch.zeros(-(-N // 32) * 32, device=w.device, dtype=torch.float64)
+    wp[:N] = w
+    w = wp[:N]
+    ncols = 0 if Q is None else Q.shape[1]
+    r0 = np.ascontiguousarray(row0, dtype=np.int64)
+    betas = np.zeros(len(r0) - 1)
+    ldq = _ld(Q) if ncols else N
+    h._check(lib().svdsc_op_cgs2_peer_emulate(h.ptr, len(r0) - 1, r0.ctypes.data, ncols,
+                                              _ptr(Q) if ncols else None, ldq, _ptr(w), betas.ctypes.data))
+    return w, betas
 
 
 def small_svd(h: Handle, T):
