@@ -18,6 +18,12 @@ workload's synthetic input, which is resident in HBM before timing starts.
   e2e          same metric through the C-ABI host-buffer entry point
                (svdsc_solve_host_*), H2D of A and v0 and D2H of S, U, V, resid
                inside the timed region
+  spmv_vs_gather_ceiling  (sparse, N = 1) each product (10 back-to-back
+               svdsc_op_matvec calls) against the live ceiling of a kernel
+               doing only its memory operations, timed the same way right
+               after (index + value streams and one random 8-byte gather per
+               nonzero, tools/gather_bw.cu): random gathers are bound by L1
+               wavefronts / L2 sectors, not HBM
   cpu_baseline the CPU oracle (oracle/oracle.c, 1 thread pinned to one core):
                per-step cost t(i) = a + b i fitted on two bounded samples of
                the first Lanczos steps, extrapolated to the GPU solve's step
@@ -98,6 +104,26 @@ class ClockSampler:
                           if r[2 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(sm)}
+
+
+def gather_ceiling(nnz, n):
+    """Memory-side ceiling of a random-column CSR SpMV of this size, measured
+    live by tools/gather_bw (the index + value streams and one 8-byte x gather
+    per nonzero, nothing else): the best rate over its gather
+    kernels, in nonzeros per second.  None if the tool is missing."""
+    exe = os.path.join(ROOT, "tools", "gather_bw")
+    src = exe + ".cu"
+    try:
+        if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+            subprocess.check_call(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", src, "-o", exe],
+                                  stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        out = subprocess.run([exe, str(int(nnz)), str(int(n))], capture_output=True, text=True, timeout=120).stdout
+        rows = [json.loads(ln) for ln in out.splitlines() if ln.startswith("{")]
+        best = min((r for r in rows if r["kernel"] in ("gather", "gnc")), key=lambda r: r["us"])
+        return {"gnnz_per_s": best["gnnz_per_s"], "us": best["us"], "kernel": best["kernel"],
+                "ctas_per_sm": best["ctas_per_sm"]}
+    except Exception:
+        return None
 
 
 def host_info():
@@ -294,6 +320,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ceiling", action="store_true", help="skip the live SpMV gather-ceiling measurement")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-rows", action="store_true",
                     help="measure e2e the multi-GPU way (each rank copies its rows in and U/S/V out around "
@@ -510,6 +537,36 @@ def main():
     step_bytes = res.info["bytes_model"] / max(res.info["steps"], 1)
     total_prof = sum(v[0] for v in prof_all.values())
 
+    # ---- sparse products against their own ceiling: random 8-byte gathers are
+    # bound by L1 wavefronts / L2 sectors, not HBM, so each SpMV
+    # family is also reported against the live gather ceiling of its shape ----
+    spmv_ceiling = None
+    if Al.kind == "csr" and world == 1 and not args.no_ceiling:
+        # both sides measured the same way, back to back: 10 products through
+        # svdsc_op_matvec (the solver's kernel for this operand) between CUDA
+        # events on the library stream, then the ceiling kernels (10 launches each)
+        spmv_ceiling = {}
+        for f, trans, ncol_x in (("Av", False, Al.n), ("ATu", True, Al.m)):
+            xin = torch.randn(ncol_x, dtype=torch.float64, device=dev)
+            S.matvec(M, xin, trans=trans)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(10):
+                S.matvec(M, xin, trans=trans)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            us = 1e3 * a0.elapsed_time(a1) / 10
+            ceil = gather_ceiling(Al.nnz, ncol_x)
+            f_ms_all, calls = prof_all[f]
+            ent = {"isolated_us": us, "gnnz_per_s": Al.nnz / (us * 1e3),
+                   "alg_GBps": (bA if f == "Av" else bAt) / (us * 1e3), "ceiling": ceil,
+                   "in_solve_us": 1e3 * f_ms_all / calls if calls else None}
+            if ceil:
+                ent["frac_of_ceiling"] = ceil["us"] / us
+            spmv_ceiling[f] = ent
+            del xin
+
     # ---- end to end, multi-GPU: every rank copies its rows of A (pinned host)
     # in, analyses and solves through the device-buffer C ABI (svdsc_matrix_*
     # + svdsc_solve, the calls a multi-GPU user makes) and copies S, its rows of
@@ -653,6 +710,7 @@ def main():
                          "share_of_step": f_ms / ms_roof if ms_roof else None, "peak_source": peak_src,
                          "timing": "CUDA events around every launch of the family in a second timed region "
                                    "of the same solves (eager launches), right after the headline one"},
+            "spmv_vs_gather_ceiling": spmv_ceiling,
             "breakdown_ms_one_solve": {f: round(v[0], 3) for f, v in prof_all.items() if v[1]},
             "breakdown_share": {f: round(v[0] / total_prof, 4) for f, v in prof_all.items() if v[1] and total_prof},
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
