@@ -90,6 +90,9 @@ struct DenseOp {
 void csr_analyze(CsrOp &op, cudaStream_t s);       // bins + long-row chunks
 void csr_transpose(const CsrOp &a, CsrOp &at, cudaStream_t s);  // device CSC -> CSR of A^T
 void csr_free(CsrOp &op);
+// multi-GPU: split a rank's rows by column into loc (columns [c0, c1), rebased)
+// and rem (the rest, global columns); both analysed (bins / seg tables)
+void csr_split_columns(const CsrOp &a, int64_t c0, int64_t c1, CsrOp &loc, CsrOp &rem, cudaStream_t s);
 
 // y = A x - c yprev (c = *c_dev if c_dev, else 0).  abort: skip if *abort.
 void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev,

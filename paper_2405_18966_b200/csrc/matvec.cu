@@ -1233,4 +1233,96 @@ void gemv_t_partial(const DenseOp &A, const double *x, PreReduce &pr, const doub
     pr.yprev = yprev;
 }
 
+// ---------------------------------------------------------------------------
+// Column split of a rank's rows (multi-GPU A v): loc holds the
+// entries whose column lies in [c0, c1) (the rank's own slice of v, columns
+// rebased to c - c0), rem the others (global columns), each row's entries in
+// their original order.  A v = loc v_slice + rem v_full: the first product
+// runs while the all-gather of v is in flight.
+namespace {
+__global__ void k_split_count(int64_t nrows, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                              int32_t c0, int32_t c1, int64_t *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < nrows; r += nw) {
+        int64_t c = 0;
+        for (int64_t p = rp[r] + lane; p < rp[r + 1]; p += 32) c += (col[p] >= c0 && col[p] < c1);
+        for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+        if (lane == 0) cnt[r] = c;
+    }
+}
+__global__ void k_split_fill(int64_t nrows, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                             const double *__restrict__ val, int32_t c0, int32_t c1, const int64_t *__restrict__ rpl,
+                             int32_t *__restrict__ coll, double *__restrict__ vall, int64_t *__restrict__ rpr,
+                             int32_t *__restrict__ colr, double *__restrict__ valr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r <= nrows; r += nw) {
+        if (r == nrows) {  // last row pointer of rem
+            if (lane == 0) rpr[nrows] = rp[nrows] - rpl[nrows];
+            continue;
+        }
+        int64_t ol = rpl[r], orm = rp[r] - rpl[r];
+        if (lane == 0) rpr[r] = orm;
+        for (int64_t p0 = rp[r]; p0 < rp[r + 1]; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const bool ok = p < rp[r + 1];
+            const int32_t c = ok ? col[p] : 0;
+            const bool isl = ok && c >= c0 && c < c1;
+            const unsigned ml = __ballot_sync(0xffffffffu, isl), mr = __ballot_sync(0xffffffffu, ok && !isl);
+            const unsigned below = (1u << lane) - 1u;
+            if (isl) {
+                coll[ol + __popc(ml & below)] = c - c0;
+                vall[ol + __popc(ml & below)] = val[p];
+            } else if (ok) {
+                colr[orm + __popc(mr & below)] = c;
+                valr[orm + __popc(mr & below)] = val[p];
+            }
+            ol += __popc(ml);
+            orm += __popc(mr);
+        }
+    }
+}
+}  // namespace
+
+void csr_split_columns(const CsrOp &a, int64_t c0, int64_t c1, CsrOp &loc, CsrOp &rem, cudaStream_t s) {
+    const int64_t nrows = a.nrows;
+    int64_t *cnt = reinterpret_cast<int64_t *>(analysis_alloc((nrows + 1) * sizeof(int64_t)));
+    check(cudaMemsetAsync(cnt, 0, (nrows + 1) * sizeof(int64_t), s), "memset");
+    if (nrows > 0)
+        k_split_count<<<grid_for(nrows * 32, 256), 256, 0, s>>>(nrows, a.row_ptr, a.col, (int32_t)c0, (int32_t)c1, cnt);
+    int64_t *rpl = dev_alloc<int64_t>(loc, (size_t)nrows + 1);
+    size_t tb = 0;
+    check(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, rpl, (int)(nrows + 1), s), "scan size");
+    void *tmp = analysis_alloc(std::max<size_t>(tb, 1));
+    check(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, rpl, (int)(nrows + 1), s), "scan");
+    int64_t nl = 0;
+    check(cudaMemcpyAsync(&nl, rpl + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    analysis_free(tmp);
+    analysis_free(cnt);
+    const int64_t nr = a.nnz - nl;
+    int32_t *coll = dev_alloc<int32_t>(loc, (size_t)std::max<int64_t>(nl, 1));
+    double *vall = dev_alloc<double>(loc, (size_t)std::max<int64_t>(nl, 1));
+    int64_t *rpr = dev_alloc<int64_t>(rem, (size_t)nrows + 1);
+    int32_t *colr = dev_alloc<int32_t>(rem, (size_t)std::max<int64_t>(nr, 1));
+    double *valr = dev_alloc<double>(rem, (size_t)std::max<int64_t>(nr, 1));
+    k_split_fill<<<grid_for((nrows + 1) * 32, 256), 256, 0, s>>>(nrows, a.row_ptr, a.col, a.val, (int32_t)c0,
+                                                                (int32_t)c1, rpl, coll, vall, rpr, colr, valr);
+    check(cudaGetLastError(), "k_split_fill");
+    loc.nrows = rem.nrows = nrows;
+    loc.ncols = c1 - c0;
+    rem.ncols = a.ncols;
+    loc.nnz = nl;
+    rem.nnz = nr;
+    loc.row_ptr = rpl;
+    loc.col = coll;
+    loc.val = vall;
+    rem.row_ptr = rpr;
+    rem.col = colr;
+    rem.val = valr;
+    csr_analyze(loc, s);
+    csr_analyze(rem, s);
+}
+
 }  // namespace svdsc

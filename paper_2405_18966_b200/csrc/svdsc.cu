@@ -118,6 +118,9 @@ struct svdsc_handle {
     Ctrl *hctrl = nullptr;       // pinned host mirror of the control block
     void *scratch = nullptr;     // op-level scratch
     size_t scratch_bytes = 0;
+    // P > 1: stream of the v all-gather that overlaps the local-column product
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_v = nullptr, ev_g = nullptr;
 };
 
 struct svdsc_group {
@@ -131,6 +134,11 @@ struct svdsc_matrix {
     int kind = 0;  // 0 CSR, 1 dense
     int64_t m_local = 0, n = 0, row_offset = 0, m_global = 0, nnz = 0;
     CsrOp A, At;
+    // P > 1 (CSR): A split by column into the rank's own slice of v (Aloc,
+    // rebased columns) and the rest (Arem), so A v overlaps the all-gather
+    bool split = false;
+    int split_P = 0;
+    CsrOp Aloc, Arem;
     DenseOp D;
     double *dense_partial = nullptr;
     double seconds_analysis = 0.0;  // host wall time of svdsc_matrix_* (validation, bins, CSC)
@@ -202,6 +210,7 @@ struct Ws {
     double *pro_mu = nullptr, *pro_nu = nullptr, *pro_part = nullptr;  // reorth = 1 (pro.cu)
     Ctrl *ctrl = nullptr;
     int64_t ldu = 0, ldv = 0, nv = 0, n_pad = 0;
+    double *cm1 = nullptr;  // P > 1: the constant -1 (z += Arem v_full as z = Arem v_full - (-1) z)
     int ldt = 0;
 };
 
@@ -247,6 +256,7 @@ size_t carve(Ws &w, void *base, int64_t m, int64_t n, int t, int k, int P) {
         w.yfull = c.take<double>(w.n_pad);
         w.vfull = c.take<double>(w.n_pad);
         w.vtmp = c.take<double>((size_t)w.n_pad * k);
+        w.cm1 = c.take<double>(1);
     }
     return c.off + 256;
 }
@@ -299,6 +309,22 @@ struct Solver {
     // z = A x - c zprev on the local rows (x = V column slice)
     void Av(const double *vcol, double *z, const double *c_dev, const double *zprev) {
         const double *x = vcol;
+        if (P > 1 && M->split && M->split_P == P) {
+            // the all-gather of v runs on the comm stream while
+            // the rank's own columns are multiplied (z = Aloc v_slice - c zprev),
+            // then z += Arem v_full (c = -1, in place)
+            ck(cudaEventRecord(H->ev_v, s), "event");
+            ck(cudaStreamWaitEvent(H->comm_stream, H->ev_v, 0), "wait");
+            H->comm->allgather(vcol, w.vfull, (size_t)nv, H->comm_stream);
+            ck(cudaEventRecord(H->ev_g, H->comm_stream), "event");
+            H->prof.begin(0, s);
+            spmv_csr(M->Aloc, vcol, z, c_dev, zprev, abort, s);
+            ck(cudaStreamWaitEvent(s, H->ev_g, 0), "wait");
+            spmv_csr(M->Arem, w.vfull, z, w.cm1, z, abort, s);
+            H->prof.end(s);
+            matvecs++;
+            return;
+        }
         if (P > 1) {
             H->comm->allgather(vcol, w.vfull, (size_t)nv, s);
             x = w.vfull;
@@ -666,6 +692,13 @@ struct Solver {
         ck(cudaMemsetAsync(w.T, 0, sizeof(double) * (t + 1) * (t + 1), s), "memset");
         if (o->reorth == 1) pro_init(t, w.pro_mu, w.pro_nu, s);
         if (P > 1) {
+            static const double minus_one = -1.0;
+            ck(cudaMemcpyAsync(w.cm1, &minus_one, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+            if (M->split && !H->comm_stream) {
+                ck(cudaStreamCreateWithFlags(&H->comm_stream, cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&H->ev_v, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&H->ev_g, cudaEventDisableTiming), "event");
+            }
             ck(cudaMemsetAsync(w.V, 0, sizeof(double) * w.ldv * (t + 1), s), "memset");
             ck(cudaMemsetAsync(w.yfull, 0, sizeof(double) * w.n_pad, s), "memset");
         }
@@ -923,6 +956,12 @@ void svdsc_destroy(svdsc_handle *h) {
     cudaStreamSynchronize(h->stream);
     delete h->comm;
     if (h->cap) cudaStreamDestroy(h->cap);
+    if (h->comm_stream) {
+        cudaStreamSynchronize(h->comm_stream);
+        cudaStreamDestroy(h->comm_stream);
+        cudaEventDestroy(h->ev_v);
+        cudaEventDestroy(h->ev_g);
+    }
     if (h->hctrl) cudaFreeHost(h->hctrl);
     if (h->scratch) cudaFree(h->scratch);
     if (h->pool) cudaMemPoolDestroy(h->pool);
@@ -982,11 +1021,23 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
         } scope(h->pool, s);
         csr_analyze(M->A, s);
         csr_transpose(M->A, M->At, s);
+        if (h->nranks > 1) {
+            // the solver's slices of v: nv = ceil(n / P) rows per rank (carve)
+            const int64_t P = h->nranks, nv = (ncols + P - 1) / P;
+            const int64_t c0 = std::min<int64_t>(ncols, (int64_t)h->rank * nv), c1 = std::min<int64_t>(ncols, c0 + nv);
+            if (c1 > c0) {
+                csr_split_columns(M->A, c0, c1, M->Aloc, M->Arem, s);
+                M->split = true;
+                M->split_P = (int)P;
+            }
+        }
         M->seconds_analysis = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
     if (st != SVDSC_OK) {
         csr_free(M->A);
         csr_free(M->At);
+        csr_free(M->Aloc);
+        csr_free(M->Arem);
         delete M;
         return st;
     }
@@ -1041,6 +1092,8 @@ void svdsc_matrix_destroy(svdsc_matrix *M) {
     if (!M) return;
     csr_free(M->A);
     csr_free(M->At);
+    csr_free(M->Aloc);
+    csr_free(M->Arem);
     if (M->dense_partial) cudaFree(M->dense_partial);
     delete M;
 }
