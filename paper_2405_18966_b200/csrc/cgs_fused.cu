@@ -487,6 +487,13 @@ struct SArgs {
     // peer instantiation (k_cgs2_stream2p, cgs2_peer): the rank's mailbox, whose
     // one-shot all-reduces replace the host all-reduces of the phased launches
     const PeerArgs *peer;
+    // deferred second update (single GPU; internal.h DeferState): dst = this
+    // side's state, qw = Q (writable: the pending column is formed in place),
+    // xs = the next product's input, defer = leave this call's column pending
+    DeferState *dst;
+    double *qw;
+    double *xs;
+    int defer;
 };
 
 template <int RT>
@@ -763,6 +770,25 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
 
     const int ph = a.phase;
     double hreg[M];
+    // the previous call on this side left its column (the last of this basis)
+    // pending: it is formed in this call's first sweep, (w' - Q h2) / beta
+    int pend = 0;
+    double prb = 0.0;
+    if constexpr (!PEER) {
+        if (a.dst && ncols > 0 && *(volatile const int *)&a.dst->flag) {
+            pend = 1;
+            prb = a.dst->rbeta;
+            if (a.dst->col != ncols - 1) {  // host bookkeeping broken: fail loudly
+                if (bid == 0 && tid == 0) {
+                    a.ctrl->abort_check = a.check;
+                    a.ctrl->abort_kind = 3;
+                    __threadfence();
+                    a.ctrl->abort = 1;
+                }
+                return;
+            }
+        }
+    }
     if (a.pre_h && ph <= 1) {  // w -= Q pre_h (restart, Eq. (7))
         load_h(a.pre_h, hreg);
         run_tiles([&](int k, const double *T, const double *W) {
@@ -785,6 +811,35 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
         // phase A: partial h1
 #pragma unroll
         for (int m = 0; m < M; m++) acc[m] = 0.0;
+        if (pend) {
+            // the pending column pc = ncols - 1: its rows of this tile are formed
+            // from the tile itself (row dots with the stored h2 over columns
+            // < pc), written back to the basis and used for h1 in place of w'
+            const int pc = ncols - 1;
+#pragma unroll
+            for (int m = 0; m < M; m++) {
+                const int j = lane + 32 * m;
+                hreg[m] = j < pc ? __ldcg(a.dst->h + j) : 0.0;
+            }
+            run_tiles([&](int k, const double *T, const double *W) {
+                double s[RPW];
+                rowdots(T, hreg, s);
+                allrows(s);
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = wid + NW * q;
+                    const int64_t r = rb + (int64_t)k * RT + rr;
+                    const double u = (T[pc * RT + (((rr >> 1) ^ (pc & (kCh - 1))) << 1) + (rr & 1)] - s[q]) * prb;
+                    if (lane == q * kHalf && r < re) a.qw[r + (int64_t)pc * a.ldq] = u;
+                    const double x = W[rr];
+#pragma unroll
+                    for (int m = 0; m < M; m++) {
+                        const int j = lane + 32 * m;
+                        if (j < ncols) acc[m] = fma(j == pc ? u : tval(T, rr, m), x, acc[m]);
+                    }
+                }
+            });
+        } else {
         run_tiles([&](int, const double *T, const double *W) {
 #pragma unroll
             for (int q = 0; q < RPW; q++) {
@@ -795,7 +850,12 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                     if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
             }
         });
+        }
         flush_cols(acc, nullptr);
+        if (pend) {  // the formed column rows precede phase B's re-reads of the tiles
+            __threadfence();
+            __syncthreads();
+        }
         if (ph == 0) {
             prefetch();  // phase B re-reads the same tiles: start them under the reduction
             prefetched = true;
@@ -882,7 +942,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             const double bn = block_sum_all(nrm_wp, sh);
             if (tid == 0) a.partial[(int64_t)bid * a.PS + ncols] = bn;
         }
-        if (ncols > 0 && ph == 0) {  // phase C reads w' written above by this CTA
+        if (ncols > 0 && ph == 0 && !(PEER ? 0 : a.defer)) {  // phase C reads w' written above by this CTA
             __threadfence();
             __syncthreads();
             prefetch();
@@ -918,10 +978,18 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     const double thr = 1e-14 * fmax(amax, 1.0);
     bool bd = false;
     double beta = 0.0;
+    bool deferred = false;
     if (pyth) {
         beta = sqrt(beta2);
         bd = !(beta > thr);
-        if (!bd && ncols > 0) {
+        if (!PEER && a.defer && !bd && ncols > 0) {
+            // deferred second update: the column keeps w'; the next product reads
+            // xs = w' / beta (differs from the final vector by -Q h2 / beta, in
+            // span(Q): DESIGN.md 7), the next call on this side forms the column
+            const double rbeta = 1.0 / beta;
+            for (int64_t r = rb + tid; r < re; r += kSThr) a.xs[r] = __ldcg(a.w + r) * rbeta;
+            deferred = true;
+        } else if (!bd && ncols > 0) {
             // one reciprocal per kernel instead of a division per row (the
             // division sequence would double this sweep's instruction count)
             const double rbeta = 1.0 / beta;
@@ -995,6 +1063,30 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
     }
     cp_wait<0>();  // a prefetch may be pending if phase C was skipped
+    if constexpr (!PEER) {
+        if (a.dst) {
+            if (a.defer && !deferred && !bd) {
+                // the final vector was formed here after all (explicit norm, reading
+                // G3, or no basis): the next product reads it from xs as planned
+                __syncthreads();
+                for (int64_t r = rb + tid; r < re; r += kSThr) a.xs[r] = __ldcg(a.w + r);
+            }
+            if (bid == 0) {
+                if (deferred) {
+#pragma unroll
+                    for (int m = 0; m < M; m++) {
+                        const int j = lane + 32 * m;
+                        if (wid == 0 && j < ncols) a.dst->h[j] = hreg[m];
+                    }
+                    if (tid == 0) {
+                        a.dst->rbeta = 1.0 / beta;
+                        a.dst->col = ncols;
+                    }
+                }
+                if (tid == 0) a.dst->flag = deferred ? 1 : 0;
+            }
+        }
+    }
     if (bid == 0 && tid == 0) {
         // every CTA read seq0 before the first grid barrier, so the next launch
         // is the first to see the advanced count
@@ -1988,10 +2080,18 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     a.t_entry = t_entry;
     a.check = check;
     a.pre_h = pre_h;
+    // a column of this basis left pending by the previous (streaming) call on
+    // this side is formed by the streaming kernel's first sweep: go there (the
+    // automatic choice is monotone in the basis size, so it would anyway)
+    const bool pending = fs.defer_st && fs.maybe_pending;
+    auto flush_pending = [&]() {
+        if (pending) flush_deferred(N, const_cast<double *>(Q), ldq, fs.defer_st, nsm, s);
+    };
+    if (fs.deferred) *fs.deferred = false;
     // small bases: one thread-block cluster, DSMEM reductions (measured: 12.7 vs
     // 17.2 us per call at config 1 (1.2 MB); slower than the Q-resident kernel
     // at 6 MB, the config 2 V side)
-    if (pol == 0 || pol == 5) {
+    if ((pol == 0 || pol == 5) && !pending) {
         const size_t cl_max = (size_t)2 << 20;
         const int C = 16;
         if (ncols <= 64 && (pol == 5 || (size_t)N * (size_t)std::max(ncols, 1) * 8 <= cl_max)) {
@@ -2073,7 +2173,7 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     }
     // Q-resident mode: the CTA's rows of Q staged once in shared memory (1 CTA
     // per SM measured faster than 2: fewer CTAs in each grid barrier / reduction)
-    if (pol == 0 || pol == 2) {
+    if ((pol == 0 || pol == 2) && !pending) {
         const int nb = nsm;
         const int64_t rpb = (N + nb - 1) / nb;
         const size_t smem = ((size_t)ncols + 2 + rpb + (size_t)ncols * (rpb + 1) + std::max<int64_t>(256, rpb)) * sizeof(double);
@@ -2107,7 +2207,10 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     if (fs.pre) split_reduce(N, *fs.pre, w, ctrl ? &ctrl->abort : nullptr, s);
     const bool aligned = (ldq % 2 == 0) && ((reinterpret_cast<uintptr_t>(Q) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
-    if (!aligned || ncols > 1024) return false;
+    if (!aligned || ncols > 1024) {
+        flush_pending();  // the caller's split sweeps need the column formed
+        return false;
+    }
     SArgs sa{};
     sa.N = N;
     sa.ncols = ncols;
@@ -2129,11 +2232,25 @@ bool cgs2_fused(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, c
     sa.pre_h = pre_h;
     sa.snake = 1;
     sa.phase = 0;
-    if (pol == 4) return tmap && launch_tma_any(*reinterpret_cast<const CUtensorMap *>(tmap), sa, nsm, s);
+    if (pol == 4) {
+        flush_pending();
+        return tmap && launch_tma_any(*reinterpret_cast<const CUtensorMap *>(tmap), sa, nsm, s);
+    }
     // cp.async register-blocked streaming (measured faster than the TMA variant
     // by 5-10 %); bases wider than its shared-memory ring (about
     // 860 columns) fall back to the split kernels
-    return launch_stream2_any(sa, nsm, s);
+    if (fs.defer_st) {  // deferred second update
+        sa.dst = fs.defer_st;
+        sa.qw = const_cast<double *>(Q);
+        sa.xs = fs.xs;
+        sa.defer = (fs.xs && ncols > 0) ? 1 : 0;
+    }
+    if (!launch_stream2_any(sa, nsm, s)) {
+        flush_pending();
+        return false;
+    }
+    if (fs.deferred) *fs.deferred = sa.defer != 0;
+    return true;
 }
 
 // Multi-GPU CGS2 (P > 1): the streaming kernel in three launches, split at its
@@ -2183,6 +2300,37 @@ bool cgs2_phased(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, 
     comm->allreduce_sum(fs.h2, (size_t)ncols + 1, s);
     launch(3);
     return true;
+}
+
+namespace {
+// a pending column formed outside the streaming kernel: (w' - Q h2) / beta
+// (pass end, before a breakdown repair, or before a non-streaming CGS2 call)
+__global__ void __launch_bounds__(256) k_flush_deferred(int64_t N, double *__restrict__ Q, int64_t ldq,
+                                                        const DeferState *__restrict__ st) {
+    if (!*(volatile const int *)&st->flag) return;
+    const int pc = st->col;
+    const double rb = st->rbeta;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        int j = 0;
+        for (; j + 1 < pc; j += 2) {
+            s0 = fma(Q[r + (int64_t)j * ldq], st->h[j], s0);
+            s1 = fma(Q[r + (int64_t)(j + 1) * ldq], st->h[j + 1], s1);
+        }
+        if (j < pc) s0 = fma(Q[r + (int64_t)j * ldq], st->h[j], s0);
+        Q[r + (int64_t)pc * ldq] = (Q[r + (int64_t)pc * ldq] - (s0 + s1)) * rb;
+    }
+}
+__global__ void k_flush_clear(DeferState *st) { st->flag = 0; }
+}  // namespace
+
+void flush_deferred(int64_t N, double *Q, int64_t ldq, DeferState *st, int nsm, cudaStream_t s) {
+    if (N > 0) {
+        k_flush_deferred<<<nsm * 8, 256, 0, s>>>(N, Q, ldq, st);
+        count_launch();
+    }
+    k_flush_clear<<<1, 1, 0, s>>>(st);
+    count_launch();
 }
 
 size_t peer_mailbox_bytes(int P, int PS) { return kPeerHdrBytes + (size_t)2 * P * PS * sizeof(double); }

@@ -148,6 +148,22 @@ void gemv_n_partial(const DenseOp &A, const double *x, PreReduce &pr, const doub
 void gemv_t_partial(const DenseOp &A, const double *x, PreReduce &pr, const double *c_dev, const double *yprev,
                     const int *abort, cudaStream_t s);
 
+// Deferred second update of the streaming CGS2 (single GPU, DESIGN.md 7
+// "deferred sweep C"): a call that defers leaves w' (after the first pass) in
+// its basis column and records the second-pass coefficients h2 and 1/beta here;
+// the SpMV that follows reads xs = w' / beta, and the next call on the same
+// side (or flush_deferred) forms the column's final value
+// (w' - Q[:, 0:col] h2) / beta while streaming the same tiles.
+constexpr int kDeferMaxCols = 1032;
+struct DeferState {
+    int flag;     // 1: column `col` of this side still holds w' (pending)
+    int col;
+    double rbeta;
+    double h[kDeferMaxCols];
+};
+// materialize a pending column (no-op if none): one sweep over its basis
+void flush_deferred(int64_t N, double *Q, int64_t ldq, DeferState *st, int nsm, cudaStream_t s);
+
 struct FusedScratch {
     double *partial;      // >= 2*nsm x (ncols+2)
     double *h1, *h2, *h3; // >= ncols+2
@@ -159,6 +175,14 @@ struct FusedScratch {
     // returns right after preparing the next barrier slot
     const int *gate = nullptr;
     int gate_want = 1;
+    // deferred second update (streaming kernel only): st = this side's state
+    // (its pending column, if flagged, is formed in the first sweep; with defer,
+    // this call leaves its own column pending and writes xs = w' / beta);
+    // *deferred (host) reports whether the launch took the deferring path
+    DeferState *defer_st = nullptr;
+    double *xs = nullptr;
+    bool *deferred = nullptr;
+    bool maybe_pending = false;  // host: the previous call on this side deferred
 };
 // false: the fused path is not applicable (caller uses cgs_p1/p2/p3 + normalize)
 // tmap: optional CUtensorMap (128 B) of Q for the TMA streaming variant

@@ -211,6 +211,10 @@ struct Ws {
     Ctrl *ctrl = nullptr;
     int64_t ldu = 0, ldv = 0, nv = 0, n_pad = 0;
     double *cm1 = nullptr;  // P > 1: the constant -1 (z += Arem v_full as z = Arem v_full - (-1) z)
+    // deferred second update of the streaming CGS2 (P = 1): per
+    // side (0 = V, 1 = U) the pending-column state and the next product's input
+    DeferState *dst[2] = {nullptr, nullptr};
+    double *xs[2] = {nullptr, nullptr};
     int ldt = 0;
 };
 
@@ -252,6 +256,10 @@ size_t carve(Ws &w, void *base, int64_t m, int64_t n, int t, int k, int P) {
     w.pro_mu = c.take<double>(t + 2);
     w.pro_nu = c.take<double>(t + 2);
     w.pro_part = c.take<double>(kMaxBlocks);
+    w.dst[0] = c.take<DeferState>(1);
+    w.dst[1] = c.take<DeferState>(1);
+    w.xs[0] = c.take<double>(roundup(std::max<int64_t>(w.nv, 1), 32));
+    w.xs[1] = c.take<double>(roundup(std::max<int64_t>(m, 1), 32));
     if (P > 1) {
         w.yfull = c.take<double>(w.n_pad);
         w.vfull = c.take<double>(w.n_pad);
@@ -390,12 +398,35 @@ struct Solver {
     // peer mailboxes of the in-kernel all-reduces (NCCL backend, P > 1, or
     // SVDSC_POLICY_CGS2 = 6 with a one-rank communicator); NULL: not used
     const PeerArgs *peer = nullptr;
+    // deferred second update (P = 1, full CGS2): maypend[side] = the last column
+    // written on that side was left pending (its product input is w.xs[side]);
+    // pend_cols[side] = that column's index (for the byte model of the flush)
+    bool maypend[2] = {false, false};
+    int pend_cols[2] = {0, 0};
+    bool defer_ok() const { return P == 1 && !peer && o->reorth == 2; }
+    // form pending columns (pass end: the small SVD's recombination and the
+    // restart read the bases; flush kernels are no-ops if the device shows none)
+    void flush_pending() {
+        const int64_t Ns[2] = {nv, m};
+        double *base[2] = {w.V, w.U};
+        const int64_t ld[2] = {w.ldv, w.ldu};
+        for (int sd = 0; sd < 2; sd++) {
+            if (!maypend[sd]) continue;
+            flush_deferred(Ns[sd], base[sd], ld[sd], w.dst[sd], nsm, s);
+            bytes_model += 8 * Ns[sd] * ((int64_t)pend_cols[sd] + 2);
+            maypend[sd] = false;
+        }
+    }
     alignas(64) unsigned char tmapU[128], tmapV[128];
     bool have_tmap = false;
     // re-orthogonalize wv against Q(:, 0:ncols) (optionally after wv -= Q pre_h),
     // then beta = ||wv||, breakdown test, T entry, wv /= beta.
+    // side: 0 = V, 1 = U (deferred second update), -1 = none.  Returns whether
+    // the call left its column pending (the product reads w.xs[side])
+    bool last_deferred = false;
     void orth_norm(int64_t N, int ncols, const double *Q, int64_t ldq, double *wv, double *t_entry, int chk,
-                   const double *pre_h) {
+                   const double *pre_h, int side = -1) {
+        last_deferred = false;
         if (peer && o->reorth != 0 && fused_ok) {
             // one launch: CGS2 + norm + normalization with the cross-rank
             // reductions completed inside the kernel
@@ -411,13 +442,26 @@ struct Solver {
         if (P == 1 && o->reorth != 0 && fused_ok) {
             FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches),
                             pending.partial ? &pending : nullptr};
+            bool dflag = false;
+            if (side >= 0 && defer_ok()) {
+                fs.defer_st = w.dst[side];
+                fs.xs = w.xs[side];
+                fs.deferred = &dflag;
+                fs.maybe_pending = maypend[side];
+            }
             H->prof.begin(11, s);
             const void *tm = have_tmap ? (Q == w.U ? (const void *)tmapU : (Q == w.V ? (const void *)tmapV : nullptr))
                                        : nullptr;
             const bool ok = cgs2_fused(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s, tm);
             H->prof.end(s);
+            if (side >= 0) {  // a pending input column was formed (or flushed) by this call
+                if (maypend[side]) bytes_model += 8 * N, bytes_reorth += 8 * N;
+                maypend[side] = ok && dflag;
+                if (dflag) pend_cols[side] = ncols;
+            }
             if (ok) {
                 pending = PreReduce{};
+                last_deferred = dflag;
                 return;
             }
             fused_ok = false;
@@ -476,43 +520,48 @@ struct Solver {
         switch (h.kind) {
             case 0:  // Alg. 1 lines 2-3
                 Av(Vcol(0), Ucol(0), nullptr, nullptr);
-                orth_norm(m, 0, w.U, w.ldu, Ucol(0), Tm(0, 0), chk, nullptr);
+                orth_norm(m, 0, w.U, w.ldu, Ucol(0), Tm(0, 0), chk, nullptr, 1);
                 bytes_model += bytesA + 8 * m * 5;
                 bytes_reorth += 8 * m * 5;
                 break;
             case 1: {  // Alg. 1 lines 5-6 + re-orthogonalization
                 const int i = h.i;
-                Atu(Ucol(i - 1), Vcol(i), Tm(i - 1, i - 1), Vcol(i - 1));
+                // a pending u_i / v_i: the product reads w' / beta
+                Atu(maypend[1] ? w.xs[1] : Ucol(i - 1), Vcol(i), Tm(i - 1, i - 1),
+                    maypend[0] ? w.xs[0] : Vcol(i - 1));
                 if (o->reorth == 1) {
                     orth_norm_pro(0, i, nv, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk);
                 } else {
-                    orth_norm(nv, i, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk, nullptr);
+                    orth_norm(nv, i, w.V, w.ldv, Vcol(i), Tm(i - 1, i), chk, nullptr, 0);
                     reorth_halves += o->reorth == 2;
                 }
                 steps++;
-                bytes_model += bytesA + 8 * nv * (3 * (int64_t)i + 5);
-                if (o->reorth == 2) bytes_reorth += 8 * nv * (3 * (int64_t)i + 5);
+                const int64_t cb = 8 * nv * ((last_deferred ? 2 : 3) * (int64_t)i + 5);
+                bytes_model += bytesA + cb;
+                if (o->reorth == 2) bytes_reorth += cb;
                 break;
             }
             case 2: {  // Alg. 1 lines 7-8 + re-orthogonalization
                 const int i = h.i;
-                Av(Vcol(i), Ucol(i), Tm(i - 1, i), Ucol(i - 1));
+                Av(maypend[0] ? w.xs[0] : Vcol(i), Ucol(i), Tm(i - 1, i), maypend[1] ? w.xs[1] : Ucol(i - 1));
                 if (o->reorth == 1) {
                     orth_norm_pro(1, i, m, w.U, w.ldu, Ucol(i), Tm(i, i), chk);
                 } else {
-                    orth_norm(m, i, w.U, w.ldu, Ucol(i), Tm(i, i), chk, nullptr);
+                    orth_norm(m, i, w.U, w.ldu, Ucol(i), Tm(i, i), chk, nullptr, 1);
                     reorth_halves += o->reorth == 2;
                 }
-                bytes_model += bytesA + 8 * m * (3 * (int64_t)i + 5);
-                if (o->reorth == 2) bytes_reorth += 8 * m * (3 * (int64_t)i + 5);
+                const int64_t cb = 8 * m * ((last_deferred ? 2 : 3) * (int64_t)i + 5);
+                bytes_model += bytesA + cb;
+                if (o->reorth == 2) bytes_reorth += cb;
                 break;
             }
             case 3: {  // Alg. 2 steps 10-11: u_{k+1} = A v_{k+1} - Uk rho, re-orth
                 Av(Vcol(k), Ucol(k), nullptr, nullptr);
-                orth_norm(m, k, w.U, w.ldu, Ucol(k), Tm(k, k), chk, w.rho);
+                orth_norm(m, k, w.U, w.ldu, Ucol(k), Tm(k, k), chk, w.rho, 1);
                 // the product, the Ũ_k rho sweep and the CGS2 against Ũ_k
-                bytes_model += bytesA + 8 * m * (4 * (int64_t)k + 5);
-                if (o->reorth != 0) bytes_reorth += 8 * m * (4 * (int64_t)k + 5);
+                const int64_t cb = 8 * m * ((last_deferred ? 3 : 4) * (int64_t)k + 5);
+                bytes_model += bytesA + cb;
+                if (o->reorth != 0) bytes_reorth += cb;
                 break;
             }
         }
@@ -571,6 +620,9 @@ struct Solver {
     // replayed (one launch per pass instead of one per kernel).
     void enqueue_plan(const std::vector<Half> &plan, size_t pos, bool with_svd) {
         for (size_t idx = pos; idx < plan.size(); idx++) run_half(plan[idx], (int)idx);
+        // pending columns are formed before anything reads the bases (a
+        // breakdown's repair, the restart's recombination, the final assembly)
+        flush_pending();
         if (with_svd) {
             H->prof.begin(6, s);
             small_svd(t, w.T, w.ldt, w.W, w.Vw, w.Uh, w.Sh, w.Vh, k, w.ctrl, abort, w.tlog, s);
@@ -661,6 +713,7 @@ struct Solver {
             const int idx = c.abort_check;
             if (c.abort_kind == 2)
                 throw CommError(SVDSC_ENCCL, "multi-GPU CGS2: a peer rank did not arrive at an in-kernel all-reduce");
+            if (c.abort_kind == 3) throw SvdscError(SVDSC_ECUDA, "deferred CGS2 update: pending column mismatch");
             if (idx < 0 || idx >= (int)plan.size()) throw SvdscError(SVDSC_ECUDA, "breakdown bookkeeping");
             const int zero[2] = {0, 0};
             ck(cudaMemcpyAsync(&w.ctrl->abort, &zero[0], sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
@@ -690,6 +743,9 @@ struct Solver {
         bytesA = M->kind == 0 ? 12 * M->nnz + 4 * (m + 1) : 8 * m * n;
         ck(cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s), "memset");
         ck(cudaMemsetAsync(w.T, 0, sizeof(double) * (t + 1) * (t + 1), s), "memset");
+        ck(cudaMemsetAsync(w.dst[0], 0, sizeof(DeferState), s), "memset");
+        ck(cudaMemsetAsync(w.dst[1], 0, sizeof(DeferState), s), "memset");
+        maypend[0] = maypend[1] = false;
         if (o->reorth == 1) pro_init(t, w.pro_mu, w.pro_nu, s);
         if (P > 1) {
             static const double minus_one = -1.0;
