@@ -1149,13 +1149,14 @@ bool launch_stream2(const SArgs &a0, int nsm, cudaStream_t s) {
     return true;
 }
 
-// ring depth: as many 32-row stages as fit in shared memory up to 128 / 192
-// columns (5 and 4 stages measured 1-2 % faster than 4 and 3 at config 4;
-// 16-row tiles with 4 stages and the register-lean w' sweep were slower, 11a)
+// ring depth: as many 32-row stages as fit in shared memory up to 192 columns,
+// but 4 (not 5) up to 128: with the deferred update's first sweep the 5-stage
+// instance spills (80 B) and measured 1-2 % slower (config 3: 982 vs 959 ms);
+// 16-row tiles with 4 stages and the register-lean w' sweep were slower, 11a
 bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
     const int nc = a.ncols;
     if (nc <= 64) return launch_stream2<32, 4, 2>(a, nsm, s);
-    if (nc <= 128) return launch_stream2<32, 5, 4>(a, nsm, s);
+    if (nc <= 128) return launch_stream2<32, 4, 4>(a, nsm, s);
     if (nc <= 192) return launch_stream2<32, 4, 6>(a, nsm, s);
     if (nc <= 256) return launch_stream2<32, 3, 8>(a, nsm, s);
     if (nc <= 320) return launch_stream2<32, 2, 10>(a, nsm, s);
