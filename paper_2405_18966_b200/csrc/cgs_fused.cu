@@ -821,24 +821,54 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 const int j = lane + 32 * m;
                 hreg[m] = j < pc ? __ldcg(a.dst->h + j) : 0.0;
             }
-            run_tiles([&](int k, const double *T, const double *W) {
-                double s[RPW];
-                rowdots(T, hreg, s);
-                allrows(s);
+            if constexpr (RPW * M > 20 || M > 16) {  // wide bases: the tile is read twice from shared memory
+                run_tiles([&](int k, const double *T, const double *W) {
+                    double s[RPW];
+                    rowdots(T, hreg, s);
+                    allrows(s);
 #pragma unroll
-                for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
-                    const int64_t r = rb + (int64_t)k * RT + rr;
-                    const double u = (T[pc * RT + (((rr >> 1) ^ (pc & (kCh - 1))) << 1) + (rr & 1)] - s[q]) * prb;
-                    if (lane == q * kHalf && r < re) a.qw[r + (int64_t)pc * a.ldq] = u;
-                    const double x = W[rr];
+                    for (int q = 0; q < RPW; q++) {
+                        const int rr = wid + NW * q;
+                        const int64_t r = rb + (int64_t)k * RT + rr;
+                        const double u = (T[pc * RT + (((rr >> 1) ^ (pc & (kCh - 1))) << 1) + (rr & 1)] - s[q]) * prb;
+                        if (lane == q * kHalf && r < re) a.qw[r + (int64_t)pc * a.ldq] = u;
+                        const double x = W[rr];
 #pragma unroll
-                    for (int m = 0; m < M; m++) {
-                        const int j = lane + 32 * m;
-                        if (j < ncols) acc[m] = fma(j == pc ? u : tval(T, rr, m), x, acc[m]);
+                        for (int m = 0; m < M; m++) {
+                            const int j = lane + 32 * m;
+                            if (j < ncols) acc[m] = fma(j == pc ? u : tval(T, rr, m), x, acc[m]);
+                        }
                     }
-                }
-            });
+                });
+            } else {  // the tile values read once, kept in registers (as in phase B)
+                run_tiles([&](int k, const double *T, const double *W) {
+                    double tv[RPW][M], part[RPW];
+#pragma unroll
+                    for (int q = 0; q < RPW; q++) {
+                        const int rr = wid + NW * q;
+                        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                        for (int m = 0; m < M; m++) {
+                            tv[q][m] = (lane + 32 * m < ncols) ? tval(T, rr, m) : 0.0;
+                            if (m & 1) s1 = fma(tv[q][m], hreg[m], s1);
+                            else s0 = fma(tv[q][m], hreg[m], s0);
+                        }
+                        part[q] = s0 + s1;
+                    }
+                    reduce_rows(part);
+                    allrows(part);
+#pragma unroll
+                    for (int q = 0; q < RPW; q++) {
+                        const int rr = wid + NW * q;
+                        const int64_t r = rb + (int64_t)k * RT + rr;
+                        const double u = (T[pc * RT + (((rr >> 1) ^ (pc & (kCh - 1))) << 1) + (rr & 1)] - part[q]) * prb;
+                        if (lane == q * kHalf && r < re) a.qw[r + (int64_t)pc * a.ldq] = u;
+                        const double x = W[rr];
+#pragma unroll
+                        for (int m = 0; m < M; m++) acc[m] = fma(lane + 32 * m == pc ? u : tv[q][m], x, acc[m]);
+                    }
+                });
+            }
         } else {
         run_tiles([&](int, const double *T, const double *W) {
 #pragma unroll
