@@ -774,7 +774,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     // pending: it is formed in this call's first sweep, (w' - Q h2) / beta
     int pend = 0;
     double prb = 0.0;
-    if constexpr (!PEER) {
+    {  // (single GPU and multi-GPU peer kernels alike)
         if (a.dst && ncols > 0 && *(volatile const int *)&a.dst->flag) {
             pend = 1;
             prb = a.dst->rbeta;
@@ -972,7 +972,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             const double bn = block_sum_all(nrm_wp, sh);
             if (tid == 0) a.partial[(int64_t)bid * a.PS + ncols] = bn;
         }
-        if (ncols > 0 && ph == 0 && !(PEER ? 0 : a.defer)) {  // phase C reads w' written above by this CTA
+        if (ncols > 0 && ph == 0 && !a.defer) {  // phase C reads w' written above by this CTA
             __threadfence();
             __syncthreads();
             prefetch();
@@ -1012,7 +1012,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     if (pyth) {
         beta = sqrt(beta2);
         bd = !(beta > thr);
-        if (!PEER && a.defer && !bd && ncols > 0) {
+        if (a.defer && !bd && ncols > 0) {
             // deferred second update: the column keeps w'; the next product reads
             // xs = w' / beta (differs from the final vector by -Q h2 / beta, in
             // span(Q): DESIGN.md 7), the next call on this side forms the column
@@ -1093,7 +1093,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             for (int64_t r = rb + tid; r < re; r += kSThr) a.w[r] = a.w[r] / beta;
     }
     cp_wait<0>();  // a prefetch may be pending if phase C was skipped
-    if constexpr (!PEER) {
+    {
         if (a.dst) {
             if (a.defer && !deferred && !bd) {
                 // the final vector was formed here after all (explicit norm, reading
@@ -2407,9 +2407,27 @@ bool peer_applicable(int ncols, const double *Q, int64_t ldq, const double *w) {
 bool cgs2_peer(int64_t N, int ncols, const double *Q, int64_t ldq, double *w, const double *pre_h,
                const FusedScratch &fs, Ctrl *ctrl, double *t_entry, int check, int nb, cudaStream_t s,
                const PeerArgs *peer) {
-    if (!peer || N < 1 || !peer_applicable(ncols, Q, ldq, w)) return false;
+    // the deferred second update (reading G5) works per rank: the pending
+    // column is formed from local rows with the (replicated) h2 and 1/beta
+    const bool pending = fs.defer_st && fs.maybe_pending;
+    if (fs.deferred) *fs.deferred = false;
+    if (!peer || N < 1 || !peer_applicable(ncols, Q, ldq, w)) {
+        if (pending) flush_deferred(N, const_cast<double *>(Q), ldq, fs.defer_st, nb, s);
+        return false;
+    }
     SArgs sa = peer_sargs(N, ncols, Q, ldq, w, pre_h, fs, ctrl, t_entry, check, peer);
-    return launch_stream2p_any(&sa, 1, nb, nullptr, s);
+    if (fs.defer_st) {
+        sa.dst = fs.defer_st;
+        sa.qw = const_cast<double *>(Q);
+        sa.xs = fs.xs;
+        sa.defer = (fs.xs && ncols > 0) ? 1 : 0;
+    }
+    if (!launch_stream2p_any(&sa, 1, nb, nullptr, s)) {
+        if (pending) flush_deferred(N, const_cast<double *>(Q), ldq, fs.defer_st, nb, s);
+        return false;
+    }
+    if (fs.deferred) *fs.deferred = sa.defer != 0;
+    return true;
 }
 
 size_t cgs2_peer_emulate_grp_bytes(int P) { return (size_t)P * sizeof(SArgs); }

@@ -403,7 +403,9 @@ struct Solver {
     // pend_cols[side] = that column's index (for the byte model of the flush)
     bool maypend[2] = {false, false};
     int pend_cols[2] = {0, 0};
-    bool defer_ok() const { return P == 1 && !peer && o->reorth == 2; }
+    // single GPU, or the multi-GPU peer kernel (the phased / loopback path keeps
+    // the three sweeps)
+    bool defer_ok() const { return o->reorth == 2 && (P == 1 || peer); }
     // form pending columns (pass end: the small SVD's recombination and the
     // restart read the bases; flush kernels are no-ops if the device shows none)
     void flush_pending() {
@@ -431,11 +433,26 @@ struct Solver {
             // one launch: CGS2 + norm + normalization with the cross-rank
             // reductions completed inside the kernel
             FusedScratch fs{w.partial, w.h1, w.h2, w.nrm, w.ctrl->gflags, 16u * (++fused_launches), nullptr};
+            bool dflag = false;
+            if (side >= 0 && defer_ok()) {
+                fs.defer_st = w.dst[side];
+                fs.xs = w.xs[side];
+                fs.deferred = &dflag;
+                fs.maybe_pending = maypend[side];
+            }
             if (pending.partial) finish_pending(N, wv);
             H->prof.begin(11, s);
             const bool ok = cgs2_peer(N, ncols, Q, ldq, wv, pre_h, fs, w.ctrl, t_entry, chk, nsm, s, peer);
             H->prof.end(s);
-            if (ok) return;
+            if (side >= 0) {
+                if (maypend[side]) bytes_model += 8 * N, bytes_reorth += 8 * N;
+                maypend[side] = ok && dflag;
+                if (dflag) pend_cols[side] = ncols;
+            }
+            if (ok) {
+                last_deferred = dflag;
+                return;
+            }
             // not applicable (identical shapes on every rank: every rank falls back)
             --fused_launches;
         }

@@ -114,11 +114,11 @@ def test_peer_emulate_rejects_bad_partition(S, H):
 @pytest.mark.parametrize("cid,scale", [(1, 1), (3, 20)])
 def test_solver_peer_path_one_rank(S, cid, scale):
     """The solver's multi-GPU CGS2 path on a one-rank NCCL communicator
-    (SVDSC_POLICY_CGS2 = 6) against the same solve with the single-GPU streaming
-    kernel and against the oracle.  (The single-GPU solve defers the second
-    CGS2 update into the next sweep and feeds its products w' / beta, DESIGN.md
-    7; the peer path does not, so the two agree to rounding, not bitwise -- the
-    kernel-level P = 1 bitwise check is test_peer_one_rank_bitwise_equals_streaming_kernel.)"""
+    (SVDSC_POLICY_CGS2 = 6: mailbox setup, per-solve reset, device-resident
+    sequence under graph replay, the deferred second update of reading G5)
+    bitwise equal to the same solve with the single-GPU streaming kernel (the
+    one-rank exchange sums the same values in the same order), and within the
+    north_star tolerances of the oracle."""
     wl = W.config(cid, scale=scale)
     r_or = O.svds(wl.A, wl.k, wl.v0, tol=wl.tol, t=wl.t, maxit=wl.maxit)
     res = []
@@ -133,8 +133,7 @@ def test_solver_peer_path_one_rank(S, cid, scale):
         res.append((r.S.cpu().numpy(), r.U.cpu().numpy(), r.V.cpu().numpy()))
         M.close()
         h.close()
-    (s0, u0, v0), (s1, u1, v1) = res
-    assert np.abs(s0 - s1).max() <= 1e-12 * s0[0]
-    assert sin_max_angle(u0, u1) <= 1e-8 and sin_max_angle(v0, v1) <= 1e-8
-    for s in (s0, s1):
-        assert np.abs(s - r_or.S).max() <= 1e-10 * r_or.S[0]
+    for a, b in zip(res[0], res[1]):
+        assert np.array_equal(a, b)
+    assert np.abs(res[1][0] - r_or.S).max() <= 1e-10 * r_or.S[0]
+    assert sin_max_angle(res[1][2], r_or.V) <= 1e-8
