@@ -701,12 +701,16 @@ def main():
                                   "partial (omega recurrence, DESIGN.md Q20; not the paper's method; "
                                   "step_bytes_model still counts every half-step's CGS2)")},
             "roofline": {"bound": "hbm",
-                         "kernel": ("fused CGS2 re-orthogonalization (3 sweeps of U_i / V_i)" if fam == "cgs2_fused"
+                         "kernel": ("fused CGS2 re-orthogonalization (the streaming kernel: 2 sweeps of U_i / V_i "
+                                    "per half-step with the deferred second update, DESIGN.md G5)" if fam == "cgs2_fused"
                                     else f"{fam} product ({'gemv' if Al.kind == 'dense' else 'spmv'})"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "bytes_per_launch": bytes_per_launch, "avg_launch_us": 1e3 * f_ms / max(f_calls, 1),
+                         "bytes_note": ("bytes the executed CGS2 moves, 8N(2i+5) (+8N forming the pending column) "
+                                        "per deferred half-step; the paper's three-sweep CGS2 moves 8N(3i+5), ~1.5x "
+                                        "these bytes for the same result" if fam == "cgs2_fused" else None),
                          "share_of_step": f_ms / ms_roof if ms_roof else None, "peak_source": peak_src,
                          "timing": "CUDA events around every launch of the family in a second timed region "
                                    "of the same solves (eager launches), right after the headline one"},
