@@ -248,10 +248,15 @@ SVDSC_API svdsc_status svdsc_profile_read(const svdsc_handle *h, double *ms, int
  *                           block Jacobi + rotation replay), 1 one-CTA Jacobi,
  *                           2 register Jacobi (p <= 64, else auto), 3 cluster
  *                           block Jacobi + rotation replay
+ *   SVDSC_POLICY_DEFER:     0 auto (the streaming CGS2 defers its second update
+ *                           into the next same-side sweep, DESIGN.md reading
+ *                           G5), 1 off (three sweeps per half-step, as written
+ *                           in PAPER.md:121; for A/B measurements)
  * EINVAL for an unknown key or value. */
 #define SVDSC_POLICY_SPMV 0
 #define SVDSC_POLICY_CGS2 1
 #define SVDSC_POLICY_SMALL_SVD 2
+#define SVDSC_POLICY_DEFER 3
 SVDSC_API svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t value);
 
 /* ---- multi-GPU (row-partitioned A) -------------------------- */

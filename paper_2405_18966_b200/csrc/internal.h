@@ -332,6 +332,7 @@ struct Policy {
     int spmv = 0;       // SVDSC_POLICY_SPMV
     int cgs2 = 0;       // SVDSC_POLICY_CGS2
     int small_svd = 0;  // SVDSC_POLICY_SMALL_SVD
+    int defer = 0;      // SVDSC_POLICY_DEFER
 };
 extern thread_local Policy g_policy;
 

@@ -405,7 +405,7 @@ struct Solver {
     int pend_cols[2] = {0, 0};
     // single GPU, or the multi-GPU peer kernel (the phased / loopback path keeps
     // the three sweeps)
-    bool defer_ok() const { return o->reorth == 2 && (P == 1 || peer); }
+    bool defer_ok() const { return o->reorth == 2 && (P == 1 || peer) && g_policy.defer == 0; }
     // form pending columns (pass end: the small SVD's recombination and the
     // restart read the bases; flush kernels are no-ops if the device shows none)
     void flush_pending() {
@@ -1608,13 +1608,14 @@ svdsc_status svdsc_comm_init_group(svdsc_handle *h, svdsc_group *g, int rank) {
 
 svdsc_status svdsc_set_policy(svdsc_handle *h, int32_t key, int32_t value) {
     if (!h) return SVDSC_EINVAL;
-    const int maxv[3] = {2, 7, 3};
-    if (key < 0 || key > 2 || value < 0 || value > maxv[key]) {
+    const int maxv[4] = {2, 7, 3, 1};
+    if (key < 0 || key > 3 || value < 0 || value > maxv[key]) {
         h->err = "svdsc_set_policy: unknown key or value";
         return SVDSC_EINVAL;
     }
     if (key == SVDSC_POLICY_SPMV) h->policy.spmv = value;
     else if (key == SVDSC_POLICY_CGS2) h->policy.cgs2 = value;
+    else if (key == SVDSC_POLICY_DEFER) h->policy.defer = value;
     else h->policy.small_svd = value;
     return SVDSC_OK;
 }

@@ -71,10 +71,11 @@ EXPORTS = ["svdsc_create", "svdsc_set_stream", "svdsc_destroy", "svdsc_last_erro
            "svdsc_profile_enable", "svdsc_profile_read", "svdsc_set_policy",
            "svdsc_group_create", "svdsc_group_destroy", "svdsc_comm_init_group", "svdsc_comm_check"]
 # svdsc_set_policy keys / values (include/svdsc.h)
-POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD = 0, 1, 2
+POLICY_SPMV, POLICY_CGS2, POLICY_SMALL_SVD, POLICY_DEFER = 0, 1, 2, 3
 SPMV = {"auto": 0, "bins": 1, "seg": 2}
 CGS2 = {"auto": 0, "split": 1, "qs": 2, "stream": 3, "tma": 4, "cluster": 5, "peer": 6, "phased": 7}
 SMALL_SVD = {"auto": 0, "one_cta": 1, "register": 2, "block": 3}
+DEFER = {"auto": 0, "off": 1}
 PROF_FAMILIES = ["Av", "ATu", "cgs_p1", "cgs_p2", "cgs_p3", "normalize", "small_svd", "residuals",
                  "recombine", "restart_misc", "collectives", "cgs2_fused", "pro_decide"]
 
@@ -193,10 +194,10 @@ class Handle:
         self._check(lib().svdsc_comm_init_group(self.ptr, group.ptr, rank))
         self.nranks, self.rank = group.nranks, rank
 
-    def set_policy(self, spmv=None, cgs2=None, small_svd=None):
-        """Force a kernel schedule (svdsc_set_policy); names from SPMV / CGS2 / SMALL_SVD."""
+    def set_policy(self, spmv=None, cgs2=None, small_svd=None, defer=None):
+        """Force a kernel schedule (svdsc_set_policy); names from SPMV / CGS2 / SMALL_SVD / DEFER."""
         for key, table, v in ((POLICY_SPMV, SPMV, spmv), (POLICY_CGS2, CGS2, cgs2),
-                              (POLICY_SMALL_SVD, SMALL_SVD, small_svd)):
+                              (POLICY_SMALL_SVD, SMALL_SVD, small_svd), (POLICY_DEFER, DEFER, defer)):
             if v is not None:
                 self._check(lib().svdsc_set_policy(self.ptr, key, table[v] if isinstance(v, str) else int(v)))
 

@@ -121,3 +121,24 @@ def test_deferred_deterministic(S, Hs):
     Hs.profile(False)
     assert torch.equal(a.S, b.S) and torch.equal(a.U, b.U) and torch.equal(a.V, b.V)
     M.close()
+
+
+def test_defer_policy_off(S):
+    """SVDSC_POLICY_DEFER = off: the literal three-sweep CGS2 of PAPER.md:121 in
+    the same streaming kernel; the two agree to rounding and with the oracle."""
+    wl = W.config(3, scale=20)
+    r_or = O.svds(wl.A, wl.k, wl.v0, tol=wl.tol, t=wl.t, maxit=wl.maxit)
+    out = {}
+    for d in ("auto", "off"):
+        h = S.Handle()
+        h.set_policy(cgs2="stream", defer=d)
+        M = S.Matrix.from_host(h, wl.A)
+        r = S.svds_c(M, wl.k, tol=wl.tol, t=wl.t, maxit=wl.maxit, v0=dev(wl.v0), fixed_passes=r_or.passes)
+        out[d] = (r.S.cpu().numpy(), r.V.cpu().numpy(), r.info["bytes_reorth"])
+        M.close()
+        h.close()
+    for s, V, _ in out.values():
+        assert np.abs(s - r_or.S).max() <= 1e-10 * r_or.S[0]
+        assert sin_max_angle(V, r_or.V) <= 1e-8
+    assert np.abs(out["auto"][0] - out["off"][0]).max() <= 1e-12 * r_or.S[0]
+    assert out["auto"][2] < 0.8 * out["off"][2]
