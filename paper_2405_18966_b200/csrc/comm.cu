@@ -48,6 +48,7 @@ struct Nccl {
     ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*ReduceScatter)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -68,10 +69,11 @@ bool nccl_load() {
     SYM("ncclCommAbort", CommAbort);
     SYM("ncclAllReduce", AllReduce);
     SYM("ncclReduceScatter", ReduceScatter);
+    SYM("ncclReduce", Reduce);
     SYM("ncclAllGather", AllGather);
     SYM("ncclGetErrorString", GetErrorString);
 #undef SYM
-    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter && g_nccl.Reduce &&
                 g_nccl.AllGather;
     return g_nccl.ok;
 }
@@ -191,6 +193,9 @@ struct NcclComm : Comm {
     void reduce_scatter_sum(const double *in, double *out, size_t n_each, cudaStream_t s) override {
         ckn(g_nccl.ReduceScatter(in, out, n_each, kNcclFloat64, kNcclSum, c, s), "ncclReduceScatter");
     }
+    void reduce_sum(const double *in, double *out, size_t n, int root, cudaStream_t s) override {
+        ckn(g_nccl.Reduce(in, out, n, kNcclFloat64, kNcclSum, root, c, s), "ncclReduce");
+    }
     void allgather(const double *in, double *out, size_t n_each, cudaStream_t s) override {
         ckn(g_nccl.AllGather(in, out, n_each, kNcclFloat64, c, s), "ncclAllGather");
     }
@@ -291,6 +296,12 @@ struct LoopbackComm : Comm {
         ckc(cudaStreamSynchronize(s), "sync");
         g->barrier();  // every rank has read every buffer
         ckc(cudaMemcpyAsync(buf, tmp, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
+    }
+    void reduce_sum(const double *in, double *out, size_t n, int root, cudaStream_t s) override {
+        publish(in, s);
+        if (rank == root) sum_into(0, n, out, s);
+        ckc(cudaStreamSynchronize(s), "sync");
+        g->barrier();
     }
     void reduce_scatter_sum(const double *in, double *out, size_t n_each, cudaStream_t s) override {
         publish(in, s);

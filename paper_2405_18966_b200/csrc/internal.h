@@ -93,6 +93,9 @@ void csr_free(CsrOp &op);
 // multi-GPU: split a rank's rows by column into loc (columns [c0, c1), rebased)
 // and rem (the rest, global columns); both analysed (bins / seg tables)
 void csr_split_columns(const CsrOp &a, int64_t c0, int64_t c1, CsrOp &loc, CsrOp &rem, cudaStream_t s);
+// rows [r0, r1) of `a` as a standalone operand (rebased row pointers, shared
+// column / value arrays); multi-GPU Aᵀu per owner slice
+void csr_row_slice(const CsrOp &a, int64_t r0, int64_t r1, CsrOp &out, cudaStream_t s);
 
 // y = A x - c yprev (c = *c_dev if c_dev, else 0).  abort: skip if *abort.
 void spmv_csr(const CsrOp &A, const double *x, double *y, const double *c_dev,
@@ -297,6 +300,8 @@ struct Comm {
     // enqueued on s (NCCL) or completed before return (loopback)
     virtual void allreduce_sum(double *buf, size_t n, cudaStream_t s) = 0;
     virtual void reduce_scatter_sum(const double *in, double *out, size_t n_each, cudaStream_t s) = 0;
+    // sum of every rank's in[0, n) into out on rank `root` only (out ignored elsewhere)
+    virtual void reduce_sum(const double *in, double *out, size_t n, int root, cudaStream_t s) = 0;
     virtual void allgather(const double *in, double *out, size_t n_each, cudaStream_t s) = 0;
     // blocking: the minimum of v over the ranks (status agreement before compute)
     virtual int allreduce_min_int(int v, cudaStream_t s) = 0;

@@ -1325,4 +1325,31 @@ void csr_split_columns(const CsrOp &a, int64_t c0, int64_t c1, CsrOp &loc, CsrOp
     csr_analyze(rem, s);
 }
 
+// rows [r0, r1) of a CSR operand as a standalone operand (row pointers rebased,
+// column / value arrays shared with `a`), analysed for the product kernels
+namespace {
+__global__ void k_rebase_rows(int64_t n, const int64_t *__restrict__ rp, int64_t base, int64_t *__restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n; r += (int64_t)gridDim.x * blockDim.x)
+        out[r] = rp[r] - base;
+}
+}  // namespace
+
+void csr_row_slice(const CsrOp &a, int64_t r0, int64_t r1, CsrOp &out, cudaStream_t s) {
+    int64_t b[2] = {0, 0};
+    check(cudaMemcpyAsync(&b[0], a.row_ptr + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaMemcpyAsync(&b[1], a.row_ptr + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    const int64_t n = r1 - r0;
+    int64_t *rp = dev_alloc<int64_t>(out, (size_t)n + 1);
+    k_rebase_rows<<<grid_for(n + 1, 256), 256, 0, s>>>(n, a.row_ptr + r0, b[0], rp);
+    check(cudaGetLastError(), "k_rebase_rows");
+    out.nrows = n;
+    out.ncols = a.ncols;
+    out.nnz = b[1] - b[0];
+    out.row_ptr = rp;
+    out.col = a.col + b[0];
+    out.val = a.val + b[0];
+    csr_analyze(out, s);
+}
+
 }  // namespace svdsc

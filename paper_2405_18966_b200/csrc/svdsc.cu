@@ -139,6 +139,9 @@ struct svdsc_matrix {
     bool split = false;
     int split_P = 0;
     CsrOp Aloc, Arem;
+    // P > 1 (CSR): the CSC copy cut into the owners' slices of Aᵀu, so each
+    // slice's reduction to its owner overlaps the next slice's product
+    std::vector<CsrOp> AtS;
     DenseOp D;
     double *dense_partial = nullptr;
     double seconds_analysis = 0.0;  // host wall time of svdsc_matrix_* (validation, bins, CSC)
@@ -363,6 +366,21 @@ struct Solver {
             else if (defer_reduce()) gemv_t_partial(M->D, u, pending, c_dev, wprev, abort, s);
             else gemv_t(M->D, u, wcol, c_dev, wprev, abort, s);
             H->prof.end(s);
+        } else if (M->kind == 0 && (int)M->AtS.size() == P && H->comm_stream) {
+            // the owners' slices of Aᵀu in owner order; slice
+            // q's reduction to rank q (comm stream) overlaps slice q+1's product
+            H->prof.begin(1, s);
+            for (int q = 0; q < P; q++) {
+                double *yq = w.yfull + (int64_t)q * nv;
+                if (M->AtS[(size_t)q].nrows > 0) spmv_csr(M->AtS[(size_t)q], u, yq, nullptr, nullptr, abort, s);
+                ck(cudaEventRecord(H->ev_v, s), "event");
+                ck(cudaStreamWaitEvent(H->comm_stream, H->ev_v, 0), "wait");
+                H->comm->reduce_sum(yq, wcol, (size_t)nv, q, H->comm_stream);
+            }
+            ck(cudaEventRecord(H->ev_g, H->comm_stream), "event");
+            ck(cudaStreamWaitEvent(s, H->ev_g, 0), "wait");
+            H->prof.end(s);
+            if (c_dev) axpy_dev(nv, wcol, c_dev, wprev, abort, s);
         } else {
             if (M->kind == 0) spmv_csr(M->At, u, w.yfull, nullptr, nullptr, abort, s);
             else gemv_t(M->D, u, w.yfull, nullptr, nullptr, abort, s);
@@ -767,7 +785,7 @@ struct Solver {
         if (P > 1) {
             static const double minus_one = -1.0;
             ck(cudaMemcpyAsync(w.cm1, &minus_one, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
-            if (M->split && !H->comm_stream) {
+            if ((M->split || !M->AtS.empty()) && !H->comm_stream) {
                 ck(cudaStreamCreateWithFlags(&H->comm_stream, cudaStreamNonBlocking), "stream");
                 ck(cudaEventCreateWithFlags(&H->ev_v, cudaEventDisableTiming), "event");
                 ck(cudaEventCreateWithFlags(&H->ev_g, cudaEventDisableTiming), "event");
@@ -1103,6 +1121,11 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
                 M->split = true;
                 M->split_P = (int)P;
             }
+            M->AtS.resize((size_t)P);
+            for (int64_t q = 0; q < P; q++) {
+                const int64_t r0 = std::min<int64_t>(ncols, q * nv), r1 = std::min<int64_t>(ncols, r0 + nv);
+                csr_row_slice(M->At, r0, r1, M->AtS[(size_t)q], s);
+            }
         }
         M->seconds_analysis = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
@@ -1111,6 +1134,7 @@ svdsc_status svdsc_matrix_csr(svdsc_handle *h, int64_t nrows, int64_t ncols, int
         csr_free(M->At);
         csr_free(M->Aloc);
         csr_free(M->Arem);
+        for (CsrOp &op : M->AtS) csr_free(op);
         delete M;
         return st;
     }
@@ -1167,6 +1191,7 @@ void svdsc_matrix_destroy(svdsc_matrix *M) {
     csr_free(M->At);
     csr_free(M->Aloc);
     csr_free(M->Arem);
+    for (CsrOp &op : M->AtS) csr_free(op);
     if (M->dense_partial) cudaFree(M->dense_partial);
     delete M;
 }
