@@ -640,6 +640,11 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     auto tval = [&](const double *T, int rr, int m) -> double {
         return T[(lane + 32 * m) * RT + (((rr >> 1) ^ sw) << 1) + (rr & 1)];
     };
+    // RPW == 2: the warp's rows are 2 wid and 2 wid + 1, one 16-byte chunk of
+    // the swizzled tile per column -- both with one shared load
+    auto tpair = [&](const double *T, int m) -> double2 {
+        return *reinterpret_cast<const double2 *>(T + (lane + 32 * m) * RT + ((wid ^ sw) << 1));
+    };
     // sums of the warp's RPW row partials.  RPW == 2 is a reduce-scatter: the
     // first level swaps the other row's partial across the half-warps, so both
     // rows take 5 shuffles instead of 10.  Afterwards p[q] is valid on lanes
@@ -661,18 +666,73 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     };
     // the warp's RPW row dots with the lane's coefficients hreg
     auto rowdots = [&](const double *T, const double (&hreg)[M], double (&out)[RPW]) {
+        if constexpr (RPW == 2) {
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
-        for (int q = 0; q < RPW; q++) {
-            const int rr = wid + NW * q;
-            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int m = 0; m < M; m += 2) {
-                if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
-                if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+            for (int m = 0; m < M; m++) {
+                if (lane + 32 * m < ncols) {
+                    const double2 t = tpair(T, m);
+                    if (m & 1) {
+                        a1 = fma(t.x, hreg[m], a1);
+                        b1 = fma(t.y, hreg[m], b1);
+                    } else {
+                        a0 = fma(t.x, hreg[m], a0);
+                        b0 = fma(t.y, hreg[m], b0);
+                    }
+                }
             }
-            out[q] = s0 + s1;
+            out[0] = a0 + a1;
+            out[1] = b0 + b1;
+        } else {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = RPW * wid + q;
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int m = 0; m < M; m += 2) {
+                    if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
+                    if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
+                }
+                out[q] = s0 + s1;
+            }
         }
         reduce_rows(out);
+    };
+    // the tile's values of the warp's rows into registers (zeros past ncols)
+    // and their row dots with hreg: part[q] before the cross-lane reduction
+    auto load_tile_rows = [&](const double *T, const double (&hreg)[M], double (&tv)[RPW][M], double (&part)[RPW]) {
+        if constexpr (RPW == 2) {
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < M; m++) {
+                double2 t = make_double2(0.0, 0.0);
+                if (lane + 32 * m < ncols) t = tpair(T, m);
+                tv[0][m] = t.x;
+                tv[1][m] = t.y;
+                if (m & 1) {
+                    a1 = fma(t.x, hreg[m], a1);
+                    b1 = fma(t.y, hreg[m], b1);
+                } else {
+                    a0 = fma(t.x, hreg[m], a0);
+                    b0 = fma(t.y, hreg[m], b0);
+                }
+            }
+            part[0] = a0 + a1;
+            part[1] = b0 + b1;
+        } else {
+#pragma unroll
+            for (int q = 0; q < RPW; q++) {
+                const int rr = RPW * wid + q;
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int m = 0; m < M; m++) {
+                    tv[q][m] = (lane + 32 * m < ncols) ? tval(T, rr, m) : 0.0;
+                    if (m & 1) s1 = fma(tv[q][m], hreg[m], s1);
+                    else s0 = fma(tv[q][m], hreg[m], s0);
+                }
+                part[q] = s0 + s1;
+            }
+        }
     };
     // every lane needs both rows' values (phase B's column accumulation)
     auto allrows = [&](double (&p)[RPW]) {
@@ -796,7 +856,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             rowdots(T, hreg, s);
 #pragma unroll
             for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
+                const int rr = RPW * wid + q;
                 const int64_t r = rb + (int64_t)k * RT + rr;
                 if (lane == q * kHalf && r < re) a.w[r] = W[rr] - s[q];
             }
@@ -828,7 +888,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                     allrows(s);
 #pragma unroll
                     for (int q = 0; q < RPW; q++) {
-                        const int rr = wid + NW * q;
+                        const int rr = RPW * wid + q;
                         const int64_t r = rb + (int64_t)k * RT + rr;
                         const double u = (T[pc * RT + (((rr >> 1) ^ (pc & (kCh - 1))) << 1) + (rr & 1)] - s[q]) * prb;
                         if (lane == q * kHalf && r < re) a.qw[r + (int64_t)pc * a.ldq] = u;
@@ -843,23 +903,12 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             } else {  // the tile values read once, kept in registers (as in phase B)
                 run_tiles([&](int k, const double *T, const double *W) {
                     double tv[RPW][M], part[RPW];
-#pragma unroll
-                    for (int q = 0; q < RPW; q++) {
-                        const int rr = wid + NW * q;
-                        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-                        for (int m = 0; m < M; m++) {
-                            tv[q][m] = (lane + 32 * m < ncols) ? tval(T, rr, m) : 0.0;
-                            if (m & 1) s1 = fma(tv[q][m], hreg[m], s1);
-                            else s0 = fma(tv[q][m], hreg[m], s0);
-                        }
-                        part[q] = s0 + s1;
-                    }
+                    load_tile_rows(T, hreg, tv, part);
                     reduce_rows(part);
                     allrows(part);
 #pragma unroll
                     for (int q = 0; q < RPW; q++) {
-                        const int rr = wid + NW * q;
+                        const int rr = RPW * wid + q;
                         const int64_t r = rb + (int64_t)k * RT + rr;
                         const double u = (T[pc * RT + (((rr >> 1) ^ (pc & (kCh - 1))) << 1) + (rr & 1)] - part[q]) * prb;
                         if (lane == q * kHalf && r < re) a.qw[r + (int64_t)pc * a.ldq] = u;
@@ -871,13 +920,23 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             }
         } else {
         run_tiles([&](int, const double *T, const double *W) {
-#pragma unroll
-            for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
-                const double x = W[rr];
+            if constexpr (RPW == 2) {
+                const double x0 = W[2 * wid], x1 = W[2 * wid + 1];
 #pragma unroll
                 for (int m = 0; m < M; m++)
-                    if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
+                    if (lane + 32 * m < ncols) {
+                        const double2 t = tpair(T, m);
+                        acc[m] = fma(t.y, x1, fma(t.x, x0, acc[m]));
+                    }
+            } else {
+#pragma unroll
+                for (int q = 0; q < RPW; q++) {
+                    const int rr = RPW * wid + q;
+                    const double x = W[rr];
+#pragma unroll
+                    for (int m = 0; m < M; m++)
+                        if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
+                }
             }
         });
         }
@@ -912,7 +971,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 allrows(part);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
+                    const int rr = RPW * wid + q;
                     const int64_t r = rb + (int64_t)k * RT + rr;
                     const double v = (r < re) ? W[rr] - part[q] : 0.0;
                     if (lane == q * kHalf && r < re) {
@@ -927,23 +986,12 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
         } else {  // the tile values read from shared memory once, kept in registers
             run_tiles([&](int k, const double *T, const double *W) {
                 double tv[RPW][M], part[RPW];
-#pragma unroll
-                for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
-                    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-                    for (int m = 0; m < M; m++) {
-                        tv[q][m] = (lane + 32 * m < ncols) ? tval(T, rr, m) : 0.0;
-                        if (m & 1) s1 = fma(tv[q][m], hreg[m], s1);
-                        else s0 = fma(tv[q][m], hreg[m], s0);
-                    }
-                    part[q] = s0 + s1;
-                }
+                load_tile_rows(T, hreg, tv, part);
                 reduce_rows(part);
                 allrows(part);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
+                    const int rr = RPW * wid + q;
                     const int64_t r = rb + (int64_t)k * RT + rr;
                     const double v = (r < re) ? W[rr] - part[q] : 0.0;
                     if (lane == q * kHalf && r < re) {
@@ -960,7 +1008,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
         run_tiles([&](int k, const double *, const double *W) {
 #pragma unroll
             for (int q = 0; q < RPW; q++) {
-                const int rr = wid + NW * q;
+                const int rr = RPW * wid + q;
                 const int64_t r = rb + (int64_t)k * RT + rr;
                 if (lane == q * kHalf && r < re) nrm_wp = fma(W[rr], W[rr], nrm_wp);
             }
@@ -1028,7 +1076,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 rowdots(T, hreg, s);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
+                    const int rr = RPW * wid + q;
                     const int64_t r = rb + (int64_t)k * RT + rr;
                     if (lane == q * kHalf && r < re) a.w[r] = (W[rr] - s[q]) * rbeta;
                 }
@@ -1045,7 +1093,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 rowdots(T, hreg, s);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
+                    const int rr = RPW * wid + q;
                     const int64_t r = rb + (int64_t)k * RT + rr;
                     if (lane == q * kHalf && r < re) a.w[r] = W[rr] - s[q];
                 }
@@ -1066,7 +1114,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 rowdots(T, hreg, s);
 #pragma unroll
                 for (int q = 0; q < RPW; q++) {
-                    const int rr = wid + NW * q;
+                    const int rr = RPW * wid + q;
                     const int64_t r = rb + (int64_t)k * RT + rr;
                     if (lane == q * kHalf && r < re) {
                         const double v = W[rr] - s[q];
