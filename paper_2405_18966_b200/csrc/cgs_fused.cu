@@ -558,6 +558,14 @@ __device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, int bid
 // bid / nb: this CTA's index among the rank's CTAs and their number (the grid,
 // except in an emulated multi-rank launch).  PEER: the global reductions are
 // completed across the ranks inside the kernel (PeerArgs, internal.h).
+// RT = 32 instances keep the shared-memory tile 32 M columns wide (columns
+// past ncols zero): the sweeps then read the lane's columns unpredicated.  The
+// RT = 16 instances (up to 1024 columns) keep the tight layout
+template <int RT>
+__host__ __device__ constexpr bool stream2_pad() { return RT == 32; }
+template <int RT, int M>
+__host__ __device__ inline int stream2_tcols(int ncols) { return stream2_pad<RT>() ? 32 * M : ncols; }
+
 template <int RT, int NS, int M, bool PEER>
 __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid, const int nb) {
     constexpr int kSThr = 512, NW = 16, RPW = RT / NW, kCh = RT / 2;
@@ -569,9 +577,20 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     __shared__ double sh[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int ncols = a.ncols;
-    const int tile_d = ncols * RT;
-    double *buf = smem_s;               // NS x ncols x RT (swizzled)
+    constexpr bool kPad = stream2_pad<RT>();
+    const int tile_d = stream2_tcols<RT, M>(ncols) * RT;
+    double *buf = smem_s;               // NS x tcols x RT (swizzled)
     double *wt = buf + NS * tile_d;     // NS x RT
+    // columns [ncols, 32 M) of every stage: zero once per launch (the ring's
+    // copies write columns < ncols only, the reduction scratch `red` stays
+    // below 16 (ncols + 1) <= 32 ncols doubles of stage 0), so every sweep
+    // reads the lane's M columns without a predicate (0 x 0 terms)
+    if constexpr (kPad) {
+        const int pad = (32 * M - ncols) * RT;
+        for (int p = 0; p < NS; p++)
+            for (int i = tid; i < pad; i += kSThr) buf[p * tile_d + ncols * RT + i] = 0.0;
+    }
+    auto colok = [&](int m) { return kPad || lane + 32 * m < ncols; };
     // NW x ncols cross-warp column sums: aliases the ring, which is idle when
     // a phase flushes (its last tile consumed, the next prefetch not issued)
     double *red = buf;
@@ -670,7 +689,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
             double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
             for (int m = 0; m < M; m++) {
-                if (lane + 32 * m < ncols) {
+                if (colok(m)) {
                     const double2 t = tpair(T, m);
                     if (m & 1) {
                         a1 = fma(t.x, hreg[m], a1);
@@ -690,7 +709,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 double s0 = 0.0, s1 = 0.0;
 #pragma unroll
                 for (int m = 0; m < M; m += 2) {
-                    if (lane + 32 * m < ncols) s0 = fma(tval(T, rr, m), hreg[m], s0);
+                    if (colok(m)) s0 = fma(tval(T, rr, m), hreg[m], s0);
                     if (m + 1 < M && lane + 32 * (m + 1) < ncols) s1 = fma(tval(T, rr, m + 1), hreg[m + 1], s1);
                 }
                 out[q] = s0 + s1;
@@ -706,7 +725,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
 #pragma unroll
             for (int m = 0; m < M; m++) {
                 double2 t = make_double2(0.0, 0.0);
-                if (lane + 32 * m < ncols) t = tpair(T, m);
+                if (colok(m)) t = tpair(T, m);
                 tv[0][m] = t.x;
                 tv[1][m] = t.y;
                 if (m & 1) {
@@ -726,7 +745,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 double s0 = 0.0, s1 = 0.0;
 #pragma unroll
                 for (int m = 0; m < M; m++) {
-                    tv[q][m] = (lane + 32 * m < ncols) ? tval(T, rr, m) : 0.0;
+                    tv[q][m] = colok(m) ? tval(T, rr, m) : 0.0;
                     if (m & 1) s1 = fma(tv[q][m], hreg[m], s1);
                     else s0 = fma(tv[q][m], hreg[m], s0);
                 }
@@ -896,7 +915,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
 #pragma unroll
                         for (int m = 0; m < M; m++) {
                             const int j = lane + 32 * m;
-                            if (j < ncols) acc[m] = fma(j == pc ? u : tval(T, rr, m), x, acc[m]);
+                            if (colok(m)) acc[m] = fma(j == pc ? u : tval(T, rr, m), x, acc[m]);
                         }
                     }
                 });
@@ -924,7 +943,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                 const double x0 = W[2 * wid], x1 = W[2 * wid + 1];
 #pragma unroll
                 for (int m = 0; m < M; m++)
-                    if (lane + 32 * m < ncols) {
+                    if (colok(m)) {
                         const double2 t = tpair(T, m);
                         acc[m] = fma(t.y, x1, fma(t.x, x0, acc[m]));
                     }
@@ -935,7 +954,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                     const double x = W[rr];
 #pragma unroll
                     for (int m = 0; m < M; m++)
-                        if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), x, acc[m]);
+                        if (colok(m)) acc[m] = fma(tval(T, rr, m), x, acc[m]);
                 }
             }
         });
@@ -980,7 +999,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
                     }
 #pragma unroll
                     for (int m = 0; m < M; m++)
-                        if (lane + 32 * m < ncols) acc[m] = fma(tval(T, rr, m), v, acc[m]);
+                        if (colok(m)) acc[m] = fma(tval(T, rr, m), v, acc[m]);
                 }
             });
         } else {  // the tile values read from shared memory once, kept in registers
@@ -1203,7 +1222,7 @@ __global__ void __launch_bounds__(512) k_cgs2_stream2e(const SArgs *__restrict__
 template <int RT, int NS, int M>
 bool launch_stream2(const SArgs &a0, int nsm, cudaStream_t s) {
     SArgs a = a0;
-    const size_t smem = ((size_t)NS * a.ncols * RT + NS * RT) * sizeof(double);
+    const size_t smem = ((size_t)NS * stream2_tcols<RT, M>(a.ncols) * RT + NS * RT) * sizeof(double);
     if (smem > 220 * 1024 || a.ncols > 32 * M) return false;
     static bool attr = false;
     if (!attr) {
@@ -1251,7 +1270,7 @@ bool launch_stream2_any(const SArgs &a, int nsm, cudaStream_t s) {
 template <int RT, int NS, int M>
 bool launch_stream2p(SArgs *ga, int ngroups, int nb, void *grp_dev, cudaStream_t s) {
     const int ncols = ga[0].ncols;
-    const size_t smem = ((size_t)NS * ncols * RT + NS * RT) * sizeof(double);
+    const size_t smem = ((size_t)NS * stream2_tcols<RT, M>(ncols) * RT + NS * RT) * sizeof(double);
     if (smem > 220 * 1024 || ncols > 32 * M || nb < 1) return false;
     static bool attr = false;
     if (!attr) {
