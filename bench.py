@@ -208,6 +208,19 @@ def relaunch_distributed(args_list, n):
     return subprocess.call(cmd)
 
 
+def workload_config(name, m, n, nnz, k, t, tol, maxit, dense, world, reorth):
+    """The `config` object of the bench line: names the workload only (nothing
+    measured, which goes to `run`), so both arms (this library and --impl
+    reference) print the same dict for the same command line."""
+    mb = (8 * m * n if dense else 12 * nnz) >> 20
+    return {"workload": name, "m": int(m), "n": int(n), "nnz": int(nnz), "k": int(k), "t": int(t),
+            "tol": tol, "maxit": int(maxit), "l2": f"inputs larger than L2 (A = {mb} MB per pass)",
+            "parallelism": f"rows{world}" if world > 1 else "single",
+            "reorth": ("full CGS2 every half-step (PAPER.md:121)" if reorth == 2 else
+                       "partial (omega recurrence, DESIGN.md Q20; not the paper's method; "
+                       "step_bytes_model still counts every half-step's CGS2)")}
+
+
 def run_loopback(args):
     """--comm loopback: N ranks as threads of this process (svdsc_group_*), each
     with its own handle, stream, rank-local rows and device (rank % visible).
@@ -381,8 +394,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": wl.name, "m": A.m, "n": A.n, "nnz": A.nnz, "k": wl.k, "t": wl.t,
-                       "tol": wl.tol, "l2": "inputs larger than L2 (A is %d MB)" % (A.bytes_one_pass() >> 20)},
+            "config": workload_config(wl.name, A.m, A.n, A.nnz, wl.k, wl.t, wl.tol, wl.maxit,
+                                      A.kind == "dense", args.gpus, args.reorth),
             "cpu_baseline": {"value": val, "unit": "steps/s", "cores": 1, "kind": "oracle",
                              "sample": f"each step = one Lanczos step of {wl.name} at basis size i_r = {i_r} "
                                        f"(the restart passes' average): the oracle's A v, A^T u and CGS2 of "
@@ -688,18 +701,12 @@ def main():
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl_full.name, "m": m_global, "n": n_cols, "nnz": nnz_global, "k": k, "t": t,
-                       "tol": wl_full.tol, "maxit": wl_full.maxit, "passes_per_solve": passes,
-                       "lanczos_steps_per_solve": steps_total // args.steps,
-                       "time_to_k_ms": ms / args.steps,
-                       "l2": f"inputs larger than L2 (A = {(12 * nnz_global if Al.kind == 'csr' else 8 * m_global * n_cols) >> 20} MB per pass)",
-                       "parallelism": f"rows{world}" if world > 1 else "single",
-                       "rank0_rows": [r0, r1],
-                       "step_hbm_gb_per_s": step_bytes * (steps_total / (ms / 1e3)) / 1e9,
-                       "step_bytes_model": step_bytes,
-                       "reorth": ("full CGS2 every half-step (PAPER.md:121)" if args.reorth == 2 else
-                                  "partial (omega recurrence, DESIGN.md Q20; not the paper's method; "
-                                  "step_bytes_model still counts every half-step's CGS2)")},
+            "config": workload_config(wl_full.name, m_global, n_cols, nnz_global, k, t, wl_full.tol, wl_full.maxit,
+                                      Al.kind == "dense", world, args.reorth),
+            "run": {"passes_per_solve": passes, "lanczos_steps_per_solve": steps_total // args.steps,
+                    "time_to_k_ms": ms / args.steps, "rank0_rows": [r0, r1],
+                    "step_hbm_gb_per_s": step_bytes * (steps_total / (ms / 1e3)) / 1e9,
+                    "step_bytes_model": step_bytes},
             "roofline": {"bound": "hbm",
                          "kernel": ("fused CGS2 re-orthogonalization (the streaming kernel: 2 sweeps of U_i / V_i "
                                     "per half-step with the deferred second update, DESIGN.md G5)" if fam == "cgs2_fused"

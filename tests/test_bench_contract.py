@@ -44,6 +44,7 @@ def test_reference_arm_line():
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["e2e"]["value"] == d["value"]
+    assert {"workload", "m", "n", "nnz", "k", "t", "tol", "maxit", "l2", "parallelism", "reorth"} == set(d["config"])
 
 
 @pytest.mark.gpu
@@ -61,7 +62,10 @@ def test_gpu_arm_line():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
-    assert d["config"]["lanczos_steps_per_solve"] > 0
+    assert d["run"]["lanczos_steps_per_solve"] > 0 and d["run"]["time_to_k_ms"] > 0
+    # `config` names the workload only: the reference arm prints the same dict
+    ref = run_bench("--impl", "reference", "--workload", "1", "--steps", "1", "--warmup", "0", timeout=600)
+    assert ref["config"] == d["config"]
 
 
 @pytest.mark.gpu
