@@ -558,13 +558,15 @@ __device__ void sreduce_cols(const SArgs &a, int ncols_tot, double *out, int bid
 // bid / nb: this CTA's index among the rank's CTAs and their number (the grid,
 // except in an emulated multi-rank launch).  PEER: the global reductions are
 // completed across the ranks inside the kernel (PeerArgs, internal.h).
-// RT = 32 instances keep the shared-memory tile 32 M columns wide (columns
-// past ncols zero): the sweeps then read the lane's columns unpredicated.  The
-// RT = 16 instances (up to 1024 columns) keep the tight layout
-template <int RT>
-__host__ __device__ constexpr bool stream2_pad() { return RT == 32; }
+// RT = 32 instances with M >= 6 keep the shared-memory tile 32 M columns wide
+// (columns past ncols zero): the sweeps then read the lane's columns
+// unpredicated.  The M = 2, 4 instances measured slower padded (r02p launch
+// list: 876 vs 786 us, 1194 vs 1095 us; <32,4,4> spills once unpredicated) and
+// the RT = 16 instances (up to 1024 columns) keep the tight layout
 template <int RT, int M>
-__host__ __device__ inline int stream2_tcols(int ncols) { return stream2_pad<RT>() ? 32 * M : ncols; }
+__host__ __device__ constexpr bool stream2_pad() { return RT == 32 && M >= 6; }
+template <int RT, int M>
+__host__ __device__ inline int stream2_tcols(int ncols) { return stream2_pad<RT, M>() ? 32 * M : ncols; }
 
 template <int RT, int NS, int M, bool PEER>
 __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid, const int nb) {
@@ -577,7 +579,7 @@ __device__ __forceinline__ void cgs2_stream2_body(const SArgs &a, const int bid,
     __shared__ double sh[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int ncols = a.ncols;
-    constexpr bool kPad = stream2_pad<RT>();
+    constexpr bool kPad = stream2_pad<RT, M>();
     const int tile_d = stream2_tcols<RT, M>(ncols) * RT;
     double *buf = smem_s;               // NS x tcols x RT (swizzled)
     double *wt = buf + NS * tile_d;     // NS x RT
