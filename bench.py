@@ -213,8 +213,17 @@ def workload_config(name, m, n, nnz, k, t, tol, maxit, dense, world, reorth):
     measured, which goes to `run`), so both arms (this library and --impl
     reference) print the same dict for the same command line."""
     mb = (8 * m * n if dense else 12 * nnz) >> 20
+    bases_mb = (8 * (m + n) * (t + 1)) >> 20
+    ws_mb = (1 if dense else 2) * mb + bases_mb  # A (+ its CSC copy) and the Lanczos bases U, V at i = t
+    if ws_mb > 126:
+        l2 = (f"inputs larger than L2 (A = {mb} MB per pass, bases {bases_mb} MB at i = t; "
+              f"working set {ws_mb} MB vs 126 MB of L2): no flush")
+    else:
+        l2 = (f"working set {ws_mb} MB is L2-resident by design (SURVEY 8(d): the latency-bound parity config; "
+              "every step of the iteration re-reads A and the bases, so no flush between steps; "
+              "its HBM fraction is not meaningful)")
     return {"workload": name, "m": int(m), "n": int(n), "nnz": int(nnz), "k": int(k), "t": int(t),
-            "tol": tol, "maxit": int(maxit), "l2": f"inputs larger than L2 (A = {mb} MB per pass)",
+            "tol": tol, "maxit": int(maxit), "l2": l2,
             "parallelism": f"rows{world}" if world > 1 else "single",
             "reorth": ("full CGS2 every half-step (PAPER.md:121)" if reorth == 2 else
                        "partial (omega recurrence, DESIGN.md Q20; not the paper's method; "
